@@ -1,0 +1,121 @@
+/*
+ * usbs_b200.h -- C ABI of the B200-native USBS hot path (sm_100a).
+ *
+ * Drop-in boundary for the per-iteration hot path of the reference package
+ * specbundle 0.1.0 (arXiv 2312.11801).  The reference is pure Python, so
+ * there is no FFI today; each entry point below names the Python interface
+ * it replaces (paths relative to /root/reference/pkg/src/specbundle/).  The
+ * Python host layer (paper_2312_11801_b200/) binds this header with ctypes
+ * and mirrors the reference operator/solver interfaces on top of it.
+ *
+ * Conventions
+ *   - plain C types only: pointers, int32/int64, double.  No torch types.
+ *   - "host" pointers are read synchronously; "dev" pointers are device
+ *     addresses (caller-owned buffers, e.g. torch CUDA tensors) consumed on
+ *     the context's stream.  Calls returning host scalars synchronise.
+ *   - dense n x k blocks are ROW-MAJOR with leading dimension ld >= k (the
+ *     reference's C-order numpy layout); small k x k / d x d matrices are
+ *     dense row-major with ld = k (symmetric ones are stored in full).
+ *   - all arithmetic is FP64.
+ *   - status codes map 1:1 onto the reference exceptions (see usbs_status).
+ */
+#ifndef USBS_B200_H
+#define USBS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define USBS_ABI_VERSION 1
+
+typedef enum {
+  USBS_OK = 0,
+  USBS_ERR_SHAPE = 1,       /* ValueError (shapes / dimensions)                 */
+  USBS_ERR_CONFIG = 2,      /* ValueError (invalid configuration)               */
+  USBS_ERR_NONFINITE = 3,   /* eigsolve.NumericError       eigsolve.py:21-22    */
+  USBS_ERR_NOT_PD = 4,      /* symlin.ConditioningError    symlin.py:34-35      */
+  USBS_ERR_STEP_FAIL = 5,   /* subqp.StepFailureError      subqp.py:56-57       */
+  USBS_ERR_EMPTY_BASIS = 6, /* symlin.EmptyBasisError      symlin.py:38-39      */
+  USBS_ERR_CUDA = 7,        /* CUDA runtime failure (RuntimeError)              */
+  USBS_ERR_CALLBACK = 8     /* a host callback reported failure                 */
+} usbs_status;
+
+typedef struct usbs_ctx usbs_ctx;
+typedef struct usbs_problem usbs_problem;
+
+/* ---- context ------------------------------------------------------------ */
+int usbs_abi_version(void);
+/* Message for the last non-OK status returned on this thread. */
+const char* usbs_last_error(void);
+/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or
+ * NULL for a library-owned stream. */
+usbs_status usbs_ctx_create(int device, void* stream, usbs_ctx** out);
+usbs_status usbs_ctx_destroy(usbs_ctx* ctx);
+usbs_status usbs_ctx_sync(usbs_ctx* ctx);
+/* number of kernel launches issued by this context so far (bench evidence) */
+int64_t usbs_ctx_launches(usbs_ctx* ctx);
+/* stream-ordered host <-> device copies of plain buffers (synchronising) */
+usbs_status usbs_memcpy_h2d(usbs_ctx* ctx, void* dst_dev, const void* src_host, int64_t bytes);
+usbs_status usbs_memcpy_d2h(usbs_ctx* ctx, void* dst_host, const void* src_dev, int64_t bytes);
+
+/* ---- problem upload: SdpProblem.cost + constraint bundle ----------------
+ * Replaces the scipy CSR + constraint objects consumed by
+ * problem.py:311-314 (dual_slack_operator), 284-289 (cost_quad,
+ * cost_factor_ip), 144-243 (DiagonalConstraints / SparseConstraintFamilies).
+ * C: CSR (host, int64 indptr, int32 indices, sorted or not, no duplicates).
+ * Constraints as flat entries (host): constraint e_idx[e] has
+ * A[e_rows[e], e_cols[e]] = A[e_cols[e], e_rows[e]] = e_vals[e], rows <= cols.
+ * Diagonal constraints (MaxCut) are passed as entries (i, i, i, 1.0) and
+ * flagged diag_only = 1, which enables the row-wise fast paths.
+ * The library builds the merged pattern of C - A*(y) once (the reference
+ * rebuilds that CSR on every evaluation, problem.py:313). */
+usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m,
+                                const int64_t* c_indptr, const int32_t* c_indices,
+                                const double* c_data, int64_t n_entries,
+                                const int64_t* e_idx, const int64_t* e_rows,
+                                const int64_t* e_cols, const double* e_vals,
+                                int diag_only, usbs_problem** out);
+usbs_status usbs_problem_destroy(usbs_problem* p);
+/* nnz of the merged slack pattern and the lanczos grid size (for reporting) */
+usbs_status usbs_problem_info(usbs_problem* p, int64_t* nnz_z, int64_t* nnz_c,
+                              int* lanczos_blocks, int* spmv_group);
+
+/* ---- K1: operator apply ------------------------------------------------- */
+/* Z = C - A*(y) assembled in place (problem.py:313 "(cost - adjoint_matrix(y))"). */
+usbs_status usbs_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y_dev);
+/* Y = M V with M = C (which = 0) or the assembled Z (which = 1), V n x k;
+ * optionally gram = sym(V^T Y) (k x k, dev).  Replaces LinOp.matmat
+ * (eigsolve.py:25-36 via problem.py:314), cost_quad (problem.py:284-286) and
+ * the Z-Gram of assemble_eval_coeffs (subqp.py:459). */
+usbs_status usbs_op_apply(usbs_ctx* ctx, usbs_problem* p, int which, const double* v_dev,
+                          int64_t ldv, int k, double* y_dev, int64_t ldy, double* gram_dev);
+
+/* ---- K2/K3: thick-restart Lanczos --------------------------------------- */
+/* Host callback producing the PCG64 stream of eigsolve._seeded_unit for a
+ * counter (eigsolve.py:49-52) into a device n-vector (unnormalised normals).
+ * Returns 0 on success. */
+typedef int (*usbs_rng_fill_fn)(void* user, int64_t counter, double* out_dev, int64_t n);
+/* lanczos_top (eigsolve.py:83-181) on M = C (which = 0) or Z (which = 1).
+ * v0_dev: the normalised start vector _seeded_unit(n, seed, 0).
+ * Outputs: vals (host, k_c, descending), vecs_dev (n x k_c row-major, ld),
+ * res (host, k_c), *converged, *restarts, ritz_hist (host, >= max_restarts+1
+ * entries, *n_hist written), *matvecs.  tol < 0 means the default 1e-9. */
+usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int which, int k_c,
+                             int inner_iters, int max_restarts, double tol,
+                             const double* v0_dev, usbs_rng_fill_fn reseed, void* user,
+                             double* vals, double* vecs_dev, int64_t ldvecs, double* res,
+                             int* converged, int* restarts, double* ritz_hist, int* n_hist,
+                             int* matvecs);
+
+/* ---- K3: small symmetric eigendecomposition ----------------------------- */
+/* small_eigh (symlin.py:193-198): symmetrise, eigendecompose, descending.
+ * k <= 64; a_dev, vals_dev (k), vecs_dev (k x k, columns = eigenvectors). */
+usbs_status usbs_small_eigh(usbs_ctx* ctx, int k, const double* a_dev, double* vals_dev,
+                            double* vecs_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* USBS_B200_H */

@@ -1,0 +1,187 @@
+// Shared internals of libusbs_b200 (sm_100a).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <unordered_map>
+
+#include "../../include/usbs_b200.h"
+
+namespace usbs {
+
+void set_error(const std::string& msg);
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+#define USBS_CUDA(call)                                                        \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) throw ::usbs::CudaError{_e, #call};                 \
+  } while (0)
+
+struct StatusError {
+  usbs_status s;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(usbs_status s, const std::string& m) { throw StatusError{s, m}; }
+
+// Scratch buffer cache keyed by slot id; grows on demand, never shrinks.
+struct Workspace {
+  std::unordered_map<int, std::pair<void*, size_t>> bufs;
+  void* get(int slot, size_t bytes) {
+    auto& b = bufs[slot];
+    if (b.second < bytes) {
+      if (b.first) cudaFree(b.first);
+      size_t nb = bytes < 256 ? 256 : bytes;
+      USBS_CUDA(cudaMalloc(&b.first, nb));
+      b.second = nb;
+    }
+    return b.first;
+  }
+  void release() {
+    for (auto& kv : bufs)
+      if (kv.second.first) cudaFree(kv.second.first);
+    bufs.clear();
+  }
+};
+
+}  // namespace usbs
+
+struct usbs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int64_t launches = 0;
+  usbs::Workspace ws;
+  double* pinned = nullptr;  // 4096 doubles of pinned host scratch
+  int* pinned_i = nullptr;   // 256 ints
+};
+
+struct usbs_problem {
+  usbs_ctx* ctx = nullptr;
+  int64_t n = 0, m = 0, nnz = 0, nnz_c = 0, ne = 0;
+  bool diag_only = false;
+  // merged CSR pattern of C - A*(y)
+  int* rowptr = nullptr;
+  int* col = nullptr;
+  double* cval = nullptr;  // C values in the merged pattern (0 where only A* lives)
+  double* zval = nullptr;  // assembled Z = C - A*(y)
+  int* diag_slot = nullptr;  // slot of (i,i) (diag_only)
+  // slack assembly: slot -> contributing entries
+  int* aptr = nullptr;   // nnz + 1
+  int* aent = nullptr;   // entry ids
+  // flat constraint entries (device copies)
+  int* e_idx = nullptr;
+  int* e_row = nullptr;
+  int* e_col = nullptr;
+  double* e_val = nullptr;
+  // SpMM work items: row segments (rows longer than SEG are split)
+  int n_items = 0;
+  int* it_row = nullptr;
+  int* it_beg = nullptr;
+  int* it_end = nullptr;
+  int* it_slot = nullptr;  // -1: whole row, else index into the split-partial scratch
+  int n_split_items = 0;
+  int n_split_rows = 0;
+  int* sr_row = nullptr;    // split rows
+  int* sr_first = nullptr;  // first split slot
+  int* sr_count = nullptr;
+  int* sr_block = nullptr;  // owning Lanczos block of each split row (ascending)
+  // Lanczos partition: block b owns items [blk_item[b], blk_item[b+1]) and
+  // rows [blk_row[b], blk_row[b+1]); split rows [blk_sr[b], blk_sr[b+1])
+  int lz_blocks = 0;
+  int spmv_group = 32;
+  int* blk_item = nullptr;
+  int* blk_row = nullptr;
+  int* blk_sr = nullptr;
+  std::vector<void*> owned;
+};
+
+namespace usbs {
+
+template <typename T>
+T* dev_upload(usbs_problem* p, const T* host, size_t count) {
+  T* d = nullptr;
+  size_t bytes = count * sizeof(T);
+  USBS_CUDA(cudaMalloc(&d, bytes < 16 ? 16 : bytes));
+  if (count) USBS_CUDA(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+  p->owned.push_back(d);
+  return d;
+}
+
+template <typename T>
+T* dev_alloc(usbs_problem* p, size_t count) {
+  T* d = nullptr;
+  size_t bytes = count * sizeof(T);
+  USBS_CUDA(cudaMalloc(&d, bytes < 16 ? 16 : bytes));
+  p->owned.push_back(d);
+  return d;
+}
+
+inline void note_launch(usbs_ctx* c, int n = 1) { c->launches += n; }
+
+inline void check_launch(usbs_ctx* c) {
+  note_launch(c);
+  USBS_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- device utils
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// block-wide sum, result broadcast to all threads; red must hold >= 32 doubles
+__device__ inline double block_sum(double v, double* red) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ double ldg_nc(const double* p) { return __ldg(p); }
+
+}  // namespace usbs
+
+// Every C-ABI entry point is wrapped in this to map exceptions to statuses.
+#define USBS_API_BEGIN try {
+#define USBS_API_END                                                              \
+  }                                                                               \
+  catch (const ::usbs::StatusError& e) {                                          \
+    ::usbs::set_error(e.msg);                                                     \
+    return e.s;                                                                   \
+  }                                                                               \
+  catch (const ::usbs::CudaError& e) {                                            \
+    ::usbs::set_error(std::string(e.what) + ": " + cudaGetErrorString(e.e));      \
+    return USBS_ERR_CUDA;                                                         \
+  }                                                                               \
+  catch (const std::exception& e) {                                               \
+    ::usbs::set_error(e.what());                                                  \
+    return USBS_ERR_CUDA;                                                         \
+  }                                                                               \
+  return USBS_OK;

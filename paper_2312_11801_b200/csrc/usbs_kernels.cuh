@@ -1,0 +1,35 @@
+// Internal launch helpers shared between translation units.
+#pragma once
+#include "usbs_common.cuh"
+
+namespace usbs {
+
+// workspace slot ids
+enum WsSlot {
+  WS_SPMM_PARTIAL = 1,
+  WS_GRAM_PARTIAL = 2,
+  WS_LZ_Q = 10,
+  WS_LZ_W = 11,
+  WS_LZ_H = 12,
+  WS_LZ_P = 13,
+  WS_LZ_SPLIT = 14,
+  WS_LZ_FLAGS = 15,
+  WS_LZ_OUT = 16,
+  WS_LZ_TMP = 17,
+  WS_SMALL = 20,
+  WS_RED = 21,
+  WS_IPM = 30,
+  WS_BOOK = 40,
+};
+
+void launch_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y);
+void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int64_t ldv, int k,
+                 double* Y, int64_t ldy);
+// out (ka x kb, row-major, dev) = A^T B for row-major n x ka A and n x kb B;
+// sym: out = 0.5 (G + G^T) (requires ka == kb)
+void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B,
+                    int64_t ldb, int kb, double* out, bool sym);
+// deterministic sum-of-squares / dot over n (result in dev scalar)
+void launch_dot(usbs_ctx* ctx, int64_t n, const double* x, const double* y, double* out);
+
+}  // namespace usbs

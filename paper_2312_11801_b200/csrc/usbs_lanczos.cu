@@ -1,0 +1,704 @@
+// K2/K3: thick-restart Lanczos with full (CGS2) reorthogonalisation as ONE
+// persistent cooperative kernel per lanczos_top call.
+//
+// Follows eigsolve.py:83-181 step for step:
+//   m = max(inner, k_c+1, 2); tol default 1e-9; q_0 = seeded unit vector
+//   per step j: w = Z q_j; c = Q^T w; w -= Q c; c' = Q^T w; w -= Q c';
+//               h[:j+1, j] = c + c'; beta = ||w||;
+//               beta <= 1e-13 max(1, max|c+c'|) -> fresh direction (host RNG)
+//   per cycle:  theta, Y = eigh(H[:m,:m]) (descending); res = |beta_m Y[m-1,:]|
+//               converged iff all res[:k_c] <= tol (1 + |theta_0|)
+//               thick restart: ell = max(1, min(k_c+3, m-2)),
+//               Q[:, :ell] = Q[:, :m] Y[:, :ell], Q[:, ell] = q_m, H = diag(theta[:ell])
+//
+// Device layout: Q column-major (ldq >= n), two n-vectors W0/W1 (double
+// buffered so the SpMV of step j+1 can gather w''_j / beta_j from any row
+// while this step's w is being written), H (m+1)^2 row-major in global.
+// Grid: G blocks (one per SM at most), each owning a contiguous row range
+// balanced on nnz; 3 grid barriers per step:
+//   A: q_j = w''_{j-1}/beta (own rows), w = Z q_j (row segments, split rows
+//      combined in-block), partial Q^T w  --sync--
+//   B: c = sum of partials; w' = w - Q c; partial Q^T w'  --sync--
+//   C: c' = sum; w'' = w' - Q c'; partial ||w''||^2; H column j  --sync--
+// The column reductions use a warp butterfly reduce-scatter (lane t ends with
+// the 32-row sum of column t): each Q element is read once per phase.
+// Rayleigh-Ritz runs redundantly in every block (identical Jacobi), so no
+// extra barrier is needed before the restart.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "usbs_common.cuh"
+#include "usbs_jacobi.cuh"
+#include "usbs_kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace usbs {
+
+enum LzFlag { F_EXIT = 0, F_J = 1, F_CYCLE = 2, F_ELL = 3, F_RESTARTS = 4, F_CONV = 5, F_NHIST = 6,
+              F_MATVECS = 7, F_NONFINITE = 8, F_PENDING = 9 };
+enum LzExit { EXIT_DONE = 0, EXIT_BREAKDOWN = 1, EXIT_NONFINITE = 2 };
+
+struct LzArgs {
+  int n, m, k_c, max_restarts;
+  int64_t ldq;
+  double tol;
+  const int* rowptr;
+  const int* col;
+  const double* val;
+  const int* it_row;
+  const int* it_beg;
+  const int* it_end;
+  const int* it_slot;
+  const int* blk_item;
+  const int* blk_row;
+  const int* blk_sr;
+  const int* sr_row;
+  const int* sr_first;
+  const int* sr_count;
+  double* Q;
+  double* W0;
+  double* W1;
+  double* H;
+  double* P1;  // [G][64]
+  double* P2;  // [G][64]
+  double* P3;  // [G]
+  double* split;
+  int* flags;
+  double* theta;  // [m]   output (after the last Rayleigh-Ritz)
+  double* Y;      // [m*m] output
+  double* res;    // [m]
+  double* hist;   // [max_restarts + 1]
+  // resume state
+  int cycle0, ell0, j0, restarts0, nhist0, matvecs0, wbuf0;
+  double beta_prev;  // beta of the step before j0 (only used if first step gathers from W)
+  int first_from_q;  // 1: q_{j0} is materialised in Q (start/restart/reseed)
+  double* vecs_out;  // n x k_c row-major (written when done)
+  int64_t ldvecs;
+};
+
+template <int LG>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = LG / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, LG);
+  return v;
+}
+
+// butterfly reduce-scatter over a warp: on exit lane l holds sum_lanes v[l]
+__device__ __forceinline__ double butterfly32(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      double send = up ? v[i] : v[i + s];
+      double keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+// Per-block column sums sum_{own rows i} Q[i,t] * x_i for t <= j (MAXQ = 32*NH),
+// with x_i produced by `rowfn(i, q[], &x)` which may also update the row.
+// Result: red[t] (smem) for t < 32*NH, summed over warps in fixed order.
+template <int NH, typename RowFn>
+__device__ __forceinline__ void column_reduce(const LzArgs& a, int j, int r0, int r1, double* wred,
+                                              double* red, RowFn rowfn) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double acc[NH];
+#pragma unroll
+  for (int h = 0; h < NH; ++h) acc[h] = 0.0;
+  for (int base = r0 + warp * 32; base < r1; base += nw * 32) {
+    const int i = base + lane;
+    const bool live = i < r1;
+    double q[NH][32];
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int tt = h * 32 + t;
+        q[h][t] = (live && tt <= j) ? a.Q[(int64_t)tt * a.ldq + i] : 0.0;
+      }
+    double x = 0.0;
+    if (live) x = rowfn(i, q);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) q[h][t] *= x;
+      acc[h] += butterfly32(q[h]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < NH; ++h) wred[warp * (32 * NH) + h * 32 + lane] = acc[h];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * NH; t += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += wred[w * (32 * NH) + t];
+    red[t] = s;
+  }
+  __syncthreads();
+}
+
+template <int LG, int NH>
+__global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int m = a.m, M1 = m + 1;
+  const int tid = threadIdx.x, nth = blockDim.x, nw = nth >> 5;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int r0 = a.blk_row[b], r1 = a.blk_row[b + 1];
+  const int i0 = a.blk_item[b], i1 = a.blk_item[b + 1];
+  const int s0 = a.blk_sr[b], s1 = a.blk_sr[b + 1];
+
+  // shared memory carve-up
+  double* wred = (double*)smem_raw;              // nw * 32 * NH
+  double* cvec = wred + nw * 32 * NH;            // 64
+  double* c2vec = cvec + 64;                     // 64
+  double* red = c2vec + 64;                      // 64
+  double* misc = red + 64;                       // 8
+  double* thetaS = misc + 8;                     // 64
+  double* Ys = thetaS + 64;                      // m*m
+  JacobiSmem js;
+  js.A = Ys + m * m;
+  js.A2 = js.A + m * m;
+  js.V = js.A2 + m * m;
+  js.V2 = js.V + m * m;
+  js.cself = js.V2 + m * m;
+  js.cmate = js.cself + 64;
+  js.red = js.cmate + 64;
+  js.mate = (int*)(js.red + 32);
+  js.flag = js.mate + 64;
+
+  int cycle = a.cycle0, ell = a.ell0, jstart = a.j0, restarts = a.restarts0, nhist = a.nhist0;
+  int matvecs = a.matvecs0, wb = a.wbuf0;
+  double beta = a.beta_prev;
+  bool from_q = a.first_from_q != 0;
+  bool pending = false;  // w''_{m-1} waits in W[wb^1] to become q_m
+  int converged = 0;
+
+  for (; cycle <= a.max_restarts; ++cycle) {
+    for (int j = jstart; j < m; ++j) {
+      double* Wprev = wb ? a.W1 : a.W0;
+      double* Wcur = wb ? a.W0 : a.W1;
+      // ------------------------------------------------------------ phase A
+      const double* xsrc;
+      double xs;
+      if (from_q) {
+        xsrc = a.Q + (int64_t)j * a.ldq;
+        xs = 1.0;
+      } else {
+        xsrc = Wprev;
+        xs = 1.0 / beta;
+        for (int i = r0 + tid; i < r1; i += nth) a.Q[(int64_t)j * a.ldq + i] = Wprev[i] * xs;
+        if (b == 0 && tid == 0) {
+          a.H[j * M1 + (j - 1)] = beta;
+          a.H[(j - 1) * M1 + j] = beta;
+        }
+      }
+      {
+        const int gpb = nth / LG, g = tid / LG, t = tid % LG;
+        for (int it = i0 + g; it < i1; it += gpb) {
+          const int rb = a.it_beg[it], re = a.it_end[it];
+          double acc = 0.0;
+          for (int z = rb + t; z < re; z += LG) acc = fma(a.val[z], xsrc[a.col[z]] * xs, acc);
+          acc = group_sum<LG>(acc);
+          if (t == 0) {
+            const int sl = a.it_slot[it];
+            if (sl < 0) Wcur[a.it_row[it]] = acc;
+            else a.split[sl] = acc;
+          }
+        }
+        __syncthreads();
+        for (int s = s0 + tid; s < s1; s += nth) {
+          const int f = a.sr_first[s], cnt = a.sr_count[s];
+          double acc = 0.0;
+          for (int u = 0; u < cnt; ++u) acc += a.split[f + u];
+          Wcur[a.sr_row[s]] = acc;
+        }
+        __syncthreads();
+      }
+      ++matvecs;
+      {
+        int bad = 0;
+        column_reduce<NH>(a, j, r0, r1, wred, red, [&](int i, double (&q)[NH][32]) {
+          double w = Wcur[i];
+          if (!isfinite(w)) bad = 1;
+          return w;
+        });
+        if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.flags[F_NONFINITE], 1);
+        for (int t = tid; t <= j; t += nth) a.P1[(int64_t)b * 64 + t] = red[t];
+      }
+      grid.sync();
+      // ------------------------------------------------------------ phase B
+      if (*(volatile int*)&a.flags[F_NONFINITE]) {
+        if (b == 0 && tid == 0) {
+          a.flags[F_EXIT] = EXIT_NONFINITE;
+          a.flags[F_MATVECS] = matvecs;
+        }
+        return;
+      }
+      for (int t = tid; t <= j; t += nth) {
+        double s = 0.0;
+        for (int bb = 0; bb < G; ++bb) s += a.P1[(int64_t)bb * 64 + t];
+        cvec[t] = s;
+      }
+      __syncthreads();
+      column_reduce<NH>(a, j, r0, r1, wred, red, [&](int i, double (&q)[NH][32]) {
+        double s = 0.0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (h * 32 + t <= j) s = fma(q[h][t], cvec[h * 32 + t], s);
+        double w = Wcur[i] - s;
+        Wcur[i] = w;
+        return w;
+      });
+      for (int t = tid; t <= j; t += nth) a.P2[(int64_t)b * 64 + t] = red[t];
+      grid.sync();
+      // ------------------------------------------------------------ phase C
+      for (int t = tid; t <= j; t += nth) {
+        double s = 0.0;
+        for (int bb = 0; bb < G; ++bb) s += a.P2[(int64_t)bb * 64 + t];
+        c2vec[t] = s;
+      }
+      __syncthreads();
+      {
+        double ss = 0.0;
+        for (int i = r0 + tid; i < r1; i += nth) {
+          double s = 0.0;
+          for (int t = 0; t <= j; ++t) s = fma(a.Q[(int64_t)t * a.ldq + i], c2vec[t], s);
+          double w = Wcur[i] - s;
+          Wcur[i] = w;
+          ss = fma(w, w, ss);
+        }
+        ss = block_sum(ss, red);
+        if (tid == 0) a.P3[b] = ss;
+      }
+      // coefficients, scale (identical in every block)
+      for (int t = tid; t <= j; t += nth) cvec[t] += c2vec[t];
+      __syncthreads();
+      if (b == 0)
+        for (int t = tid; t <= j; t += nth) {
+          a.H[t * M1 + j] = cvec[t];
+          a.H[j * M1 + t] = cvec[t];
+        }
+      if (tid == 0) {
+        double mx = 0.0;
+        for (int t = 0; t <= j; ++t) mx = fmax(mx, fabs(cvec[t]));
+        misc[0] = fmax(1.0, mx);
+      }
+      grid.sync();
+      if (tid == 0) {
+        double s = 0.0;
+        for (int bb = 0; bb < G; ++bb) s += a.P3[bb];
+        misc[1] = sqrt(s);
+      }
+      __syncthreads();
+      beta = misc[1];
+      const double scale = misc[0];
+      wb ^= 1;  // Wcur becomes Wprev for the next step
+      from_q = false;
+      if (beta <= 1e-13 * scale) {
+        if (b == 0 && tid == 0) {
+          a.flags[F_EXIT] = EXIT_BREAKDOWN;
+          a.flags[F_J] = j;
+          a.flags[F_CYCLE] = cycle;
+          a.flags[F_ELL] = ell;
+          a.flags[F_RESTARTS] = restarts;
+          a.flags[F_NHIST] = nhist;
+          a.flags[F_MATVECS] = matvecs;
+          a.flags[F_PENDING] = wb;
+        }
+        return;
+      }
+      pending = (j == m - 1);
+    }
+    // ---------------------------------------------------------- end of cycle
+    if (pending) {
+      double* Wprev = wb ? a.W1 : a.W0;
+      const double xs = 1.0 / beta;
+      for (int i = r0 + tid; i < r1; i += nth) a.Q[(int64_t)m * a.ldq + i] = Wprev[i] * xs;
+      if (b == 0 && tid == 0) {
+        a.H[m * M1 + (m - 1)] = beta;
+        a.H[(m - 1) * M1 + m] = beta;
+      }
+      pending = false;
+    }
+    grid.sync();
+    // Rayleigh-Ritz (every block, identical)
+    for (int x = tid; x < m * m; x += nth) js.A[x] = a.H[(x / m) * M1 + (x % m)];
+    __syncthreads();
+    jacobi_eigh(m, js, thetaS, Ys, m);
+    const double beta_last = a.H[m * M1 + (m - 1)];
+    if (tid == 0) {
+      bool ok = true;
+      const double tol_eff = a.tol * (1.0 + fabs(thetaS[0]));
+      for (int u = 0; u < a.k_c; ++u) {
+        double r = fabs(beta_last * Ys[(m - 1) * m + u]);
+        if (!(r <= tol_eff)) ok = false;
+      }
+      misc[2] = ok ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (b == 0) {
+      for (int u = tid; u < m; u += nth) {
+        a.theta[u] = thetaS[u];
+        a.res[u] = fabs(beta_last * Ys[(m - 1) * m + u]);
+      }
+      for (int x = tid; x < m * m; x += nth) a.Y[x] = Ys[x];
+      if (tid == 0) a.hist[nhist] = thetaS[0];
+    }
+    ++nhist;
+    if (misc[2] != 0.0) { converged = 1; break; }
+    if (cycle == a.max_restarts) break;
+    // thick restart
+    ell = max(1, min(a.k_c + 3, m - 2));
+    for (int i = r0 + tid; i < r1; i += nth) {
+      double qrow[64];
+      for (int t = 0; t < m; ++t) qrow[t] = a.Q[(int64_t)t * a.ldq + i];
+      for (int u = 0; u < ell; ++u) {
+        double s = 0.0;
+        for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
+        a.Q[(int64_t)u * a.ldq + i] = s;
+      }
+      a.Q[(int64_t)ell * a.ldq + i] = a.Q[(int64_t)m * a.ldq + i];
+    }
+    ++restarts;
+    jstart = ell;
+    from_q = true;
+    grid.sync();
+    // H reset after the barrier: every block has read H for its Rayleigh-Ritz;
+    // only block 0 writes H, and it does so in program order from here on
+    if (b == 0) {
+      for (int x = tid; x < M1 * M1; x += nth) a.H[x] = 0.0;
+      __syncthreads();
+      for (int u = tid; u < ell; u += nth) a.H[u * M1 + u] = thetaS[u];
+      __syncthreads();
+    }
+  }
+  // ---------------------------------------------------------------- output
+  for (int i = r0 + tid; i < r1; i += nth) {
+    double qrow[64];
+    for (int t = 0; t < m; ++t) qrow[t] = a.Q[(int64_t)t * a.ldq + i];
+    for (int u = 0; u < a.k_c; ++u) {
+      double s = 0.0;
+      for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
+      a.vecs_out[(int64_t)i * a.ldvecs + u] = s;
+    }
+  }
+  if (b == 0 && tid == 0) {
+    a.flags[F_EXIT] = EXIT_DONE;
+    a.flags[F_CONV] = converged;
+    a.flags[F_RESTARTS] = restarts;
+    a.flags[F_NHIST] = nhist;
+    a.flags[F_MATVECS] = matvecs;
+  }
+}
+
+// ------------------------------------------------------------ small kernels
+__global__ void k_copy(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+
+// c[t] = Q[:, t] . v  for t < used  (one block per column, deterministic)
+__global__ void k_colmajor_dot(int64_t n, const double* __restrict__ Q, int64_t ldq,
+                               const double* __restrict__ v, double* __restrict__ c) {
+  __shared__ double red[32];
+  const int t = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(Q[(int64_t)t * ldq + i], v[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) c[t] = s;
+}
+
+// v -= Q[:, :used] c ; then scale v by 1/||v|| is done separately
+__global__ void k_colmajor_sub(int64_t n, const double* __restrict__ Q, int64_t ldq, int used,
+                               const double* __restrict__ c, double* __restrict__ v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < used; ++t) s = fma(Q[(int64_t)t * ldq + i], c[t], s);
+    v[i] -= s;
+  }
+}
+
+__global__ void k_norm2(int64_t n, const double* __restrict__ v, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(v[i], v[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void k_scale_into(int64_t n, const double* __restrict__ v, double s, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v[i] * s;
+}
+
+// dense fallback (eigsolve.py:66-80): Z = M I densely, symmetrise, eigh
+__global__ void k_dense_eigh(int n, const int* __restrict__ rowptr, const int* __restrict__ col,
+                             const double* __restrict__ val, int k, double* vals_out, double* vecs_out,
+                             int64_t ldv, int* nonfinite) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* base = (double*)smem_raw;
+  JacobiSmem js;
+  js.A = base;
+  js.A2 = js.A + n * n;
+  js.V = js.A2 + n * n;
+  js.V2 = js.V + n * n;
+  double* vals = js.V2 + n * n;
+  double* vecs = vals + 64;
+  js.cself = vecs + n * n;
+  js.cmate = js.cself + 64;
+  js.red = js.cmate + 64;
+  js.mate = (int*)(js.red + 32);
+  js.flag = js.mate + 64;
+  for (int x = threadIdx.x; x < n * n; x += blockDim.x) js.A[x] = 0.0;
+  __syncthreads();
+  int bad = 0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x)
+    for (int z = rowptr[r]; z < rowptr[r + 1]; ++z) {
+      double v = val[z];
+      if (!isfinite(v)) bad = 1;
+      js.A[r * n + col[z]] += v;
+    }
+  bad = __syncthreads_or(bad);
+  if (bad) {
+    if (threadIdx.x == 0) *nonfinite = 1;
+    return;
+  }
+  jacobi_eigh(n, js, vals, vecs, n);
+  for (int u = threadIdx.x; u < k; u += blockDim.x) vals_out[u] = vals[u];
+  for (int x = threadIdx.x; x < n * k; x += blockDim.x) {
+    int r = x / k, u = x % k;
+    vecs_out[(int64_t)r * ldv + u] = vecs[r * n + u];
+  }
+}
+
+__global__ void k_small_eigh(int k, const double* __restrict__ a, double* vals_out, double* vecs_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* base = (double*)smem_raw;
+  JacobiSmem js;
+  js.A = base;
+  js.A2 = js.A + k * k;
+  js.V = js.A2 + k * k;
+  js.V2 = js.V + k * k;
+  double* vals = js.V2 + k * k;
+  double* vecs = vals + 64;
+  js.cself = vecs + k * k;
+  js.cmate = js.cself + 64;
+  js.red = js.cmate + 64;
+  js.mate = (int*)(js.red + 32);
+  js.flag = js.mate + 64;
+  for (int x = threadIdx.x; x < k * k; x += blockDim.x) js.A[x] = a[x];
+  __syncthreads();
+  jacobi_eigh(k, js, vals, vecs, k);
+  for (int u = threadIdx.x; u < k; u += blockDim.x) vals_out[u] = vals[u];
+  for (int x = threadIdx.x; x < k * k; x += blockDim.x) vecs_out[x] = vecs[x];
+}
+
+static size_t eigh_smem(int n) {
+  return (size_t)(5 * n * n + 64 * 3 + 32) * sizeof(double) + 65 * sizeof(int) + 64;
+}
+
+void launch_small_eigh(usbs_ctx* ctx, int k, const double* a, double* vals, double* vecs) {
+  size_t sm = eigh_smem(k);
+  static bool attr = false;
+  if (!attr) {
+    USBS_CUDA(cudaFuncSetAttribute(k_small_eigh, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_small_eigh<<<1, 256, sm, ctx->stream>>>(k, a, vals, vecs);
+  check_launch(ctx);
+}
+
+template <int LG, int NH>
+static void lz_launch(usbs_ctx* ctx, LzArgs& a, int G, size_t smem) {
+  auto fn = k_lanczos<LG, NH>;
+  static bool attr = false;
+  if (!attr) {
+    USBS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const int threads = NH == 1 ? 512 : 256;
+  int per_sm = 0;
+  USBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  if (per_sm * ctx->num_sms < G) fail(USBS_ERR_CUDA, "lanczos grid exceeds co-resident capacity");
+  void* args[] = {&a};
+  USBS_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(threads), args, smem, ctx->stream));
+  check_launch(ctx);
+}
+
+template <int NH>
+static void lz_dispatch(usbs_ctx* ctx, LzArgs& a, int G, int LG, size_t smem) {
+  switch (LG) {
+    case 4: lz_launch<4, NH>(ctx, a, G, smem); break;
+    case 8: lz_launch<8, NH>(ctx, a, G, smem); break;
+    case 16: lz_launch<16, NH>(ctx, a, G, smem); break;
+    default: lz_launch<32, NH>(ctx, a, G, smem); break;
+  }
+}
+
+}  // namespace usbs
+
+using namespace usbs;
+
+extern "C" usbs_status usbs_small_eigh(usbs_ctx* ctx, int k, const double* a, double* vals, double* vecs) {
+  USBS_API_BEGIN
+  if (k < 1 || k > 64) fail(USBS_ERR_SHAPE, "small_eigh supports 1 <= k <= 64");
+  launch_small_eigh(ctx, k, a, vals, vecs);
+  USBS_API_END
+}
+
+extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int which, int k_c, int inner_iters,
+                                        int max_restarts, double tol, const double* v0, usbs_rng_fill_fn reseed,
+                                        void* user, double* vals, double* vecs_dev, int64_t ldvecs, double* res,
+                                        int* converged, int* restarts, double* ritz_hist, int* n_hist,
+                                        int* matvecs) {
+  USBS_API_BEGIN
+  const int64_t n = p->n;
+  if (k_c < 1) fail(USBS_ERR_CONFIG, "k_c must be at least 1");
+  if (max_restarts < 0 || inner_iters < 0) fail(USBS_ERR_CONFIG, "invalid Lanczos budget");
+  if (ldvecs < k_c) fail(USBS_ERR_SHAPE, "ldvecs < k_c");
+  const double* val = which ? p->zval : p->cval;
+  cudaStream_t st = ctx->stream;
+  const int m = std::max(std::max(inner_iters, k_c + 1), 2);
+  if (k_c >= n || inner_iters >= n || m >= n) {
+    // dense fallback
+    if (n > 40) fail(USBS_ERR_CONFIG, "dense Lanczos fallback supports n <= 40");
+    int* nf = (int*)ctx->ws.get(WS_LZ_FLAGS, 64 * sizeof(int));
+    USBS_CUDA(cudaMemsetAsync(nf, 0, sizeof(int), st));
+    double* dv = (double*)ctx->ws.get(WS_LZ_OUT, 64 * sizeof(double));
+    const int k = (int)std::min<int64_t>(k_c, n);
+    static bool attr = false;
+    if (!attr) {
+      USBS_CUDA(cudaFuncSetAttribute(k_dense_eigh, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_dense_eigh<<<1, 256, eigh_smem((int)n), st>>>((int)n, p->rowptr, p->col, val, k, dv, vecs_dev, ldvecs, nf);
+    check_launch(ctx);
+    USBS_CUDA(cudaMemcpyAsync(ctx->pinned, dv, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    USBS_CUDA(cudaMemcpyAsync(ctx->pinned_i, nf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    USBS_CUDA(cudaStreamSynchronize(st));
+    if (ctx->pinned_i[0]) fail(USBS_ERR_NONFINITE, "matvec returned non-finite values");
+    for (int u = 0; u < k; ++u) {
+      vals[u] = ctx->pinned[u];
+      res[u] = 0.0;
+    }
+    *converged = 1;
+    *restarts = 0;
+    ritz_hist[0] = ctx->pinned[0];
+    *n_hist = 1;
+    *matvecs = (int)n;
+    return USBS_OK;
+  }
+  if (m > 64) fail(USBS_ERR_CONFIG, "Lanczos basis size m > 64 is not supported");
+  const int NH = m <= 32 ? 1 : 2;
+  const int G = p->lz_blocks;
+  const int64_t ldq = (n + 31) / 32 * 32;
+  double* Q = (double*)ctx->ws.get(WS_LZ_Q, (size_t)ldq * (m + 1) * sizeof(double));
+  double* W = (double*)ctx->ws.get(WS_LZ_W, (size_t)2 * ldq * sizeof(double));
+  double* H = (double*)ctx->ws.get(WS_LZ_H, (size_t)(m + 1) * (m + 1) * sizeof(double));
+  double* P = (double*)ctx->ws.get(WS_LZ_P, (size_t)(G * 64 * 2 + G) * sizeof(double));
+  double* SP = (double*)ctx->ws.get(WS_LZ_SPLIT, (size_t)std::max(1, p->n_split_items) * sizeof(double));
+  int* flags = (int*)ctx->ws.get(WS_LZ_FLAGS, 64 * sizeof(int));
+  double* out = (double*)ctx->ws.get(WS_LZ_OUT, (size_t)(m + m * m + m + max_restarts + 1 + 8) * sizeof(double));
+  double* tmp = (double*)ctx->ws.get(WS_LZ_TMP, (size_t)(ldq + 128) * sizeof(double));
+  USBS_CUDA(cudaMemsetAsync(H, 0, (size_t)(m + 1) * (m + 1) * sizeof(double), st));
+  USBS_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), st));
+  USBS_CUDA(cudaMemcpyAsync(Q, v0, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+
+  LzArgs a{};
+  a.n = (int)n; a.m = m; a.k_c = k_c; a.max_restarts = max_restarts; a.ldq = ldq;
+  a.tol = tol < 0 ? 1e-9 : tol;
+  a.rowptr = p->rowptr; a.col = p->col; a.val = val;
+  a.it_row = p->it_row; a.it_beg = p->it_beg; a.it_end = p->it_end; a.it_slot = p->it_slot;
+  a.blk_item = p->blk_item; a.blk_row = p->blk_row; a.blk_sr = p->blk_sr;
+  a.sr_row = p->sr_row; a.sr_first = p->sr_first; a.sr_count = p->sr_count;
+  a.Q = Q; a.W0 = W; a.W1 = W + ldq; a.H = H;
+  a.P1 = P; a.P2 = P + G * 64; a.P3 = P + 2 * G * 64;
+  a.split = SP; a.flags = flags;
+  a.theta = out; a.Y = out + m; a.res = out + m + m * m; a.hist = out + 2 * m + m * m;
+  a.vecs_out = vecs_dev; a.ldvecs = ldvecs;
+  a.cycle0 = 0; a.ell0 = 0; a.j0 = 0; a.restarts0 = 0; a.nhist0 = 0; a.matvecs0 = 0; a.wbuf0 = 0;
+  a.beta_prev = 1.0; a.first_from_q = 1;
+
+  const int nw = (NH == 1 ? 512 : 256) / 32;
+  size_t smem = (size_t)(nw * 32 * NH + 64 * 3 + 8 + 64 + m * m + 4 * m * m + 64 * 2 + 32) * sizeof(double) +
+                65 * sizeof(int) + 64;
+  int64_t ctr = 0;
+  int* hf = ctx->pinned_i;
+  for (;;) {
+    if (NH == 1) lz_dispatch<1>(ctx, a, G, p->spmv_group, smem);
+    else lz_dispatch<2>(ctx, a, G, p->spmv_group, smem);
+    USBS_CUDA(cudaMemcpyAsync(hf, flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    USBS_CUDA(cudaStreamSynchronize(st));
+    if (hf[F_EXIT] == EXIT_NONFINITE) fail(USBS_ERR_NONFINITE, "matvec returned non-finite values");
+    if (hf[F_EXIT] == EXIT_DONE) break;
+    // breakdown at step j: fresh direction for q_{j+1} (eigsolve.py:136-147, 55-63)
+    const int j = hf[F_J], used = j + 1;
+    ctr += 16;
+    double* v = tmp;
+    double* cbuf = tmp + ldq;
+    bool got = false;
+    for (int att = 0; att < 8 && !got; ++att) {
+      if (!reseed) fail(USBS_ERR_CALLBACK, "Lanczos breakdown needs a reseed callback");
+      if (reseed(user, ctr + att + 1, v, n) != 0) fail(USBS_ERR_CALLBACK, "reseed callback failed");
+      // _seeded_unit normalises, then the projection, then the norm test
+      k_norm2<<<1, 1024, 0, st>>>(n, v, cbuf + 64);
+      check_launch(ctx);
+      USBS_CUDA(cudaMemcpyAsync(ctx->pinned, cbuf + 64, sizeof(double), cudaMemcpyDeviceToHost, st));
+      USBS_CUDA(cudaStreamSynchronize(st));
+      double nv0 = std::sqrt(ctx->pinned[0]);
+      int thr = 256, bl = (int)std::min<int64_t>((n + thr - 1) / thr, 4 * ctx->num_sms);
+      k_scale_into<<<bl, thr, 0, st>>>(n, v, 1.0 / nv0, v);
+      check_launch(ctx);
+      k_colmajor_dot<<<used, 512, 0, st>>>(n, Q, ldq, v, cbuf);
+      check_launch(ctx);
+      k_colmajor_sub<<<bl, thr, 0, st>>>(n, Q, ldq, used, cbuf, v);
+      check_launch(ctx);
+      k_norm2<<<1, 1024, 0, st>>>(n, v, cbuf + 64);
+      check_launch(ctx);
+      USBS_CUDA(cudaMemcpyAsync(ctx->pinned, cbuf + 64, sizeof(double), cudaMemcpyDeviceToHost, st));
+      USBS_CUDA(cudaStreamSynchronize(st));
+      double nv = std::sqrt(ctx->pinned[0]);
+      if (nv > 1e-8) {
+        k_scale_into<<<bl, thr, 0, st>>>(n, v, 1.0 / nv, Q + (int64_t)(j + 1) * ldq);
+        check_launch(ctx);
+        got = true;
+      }
+    }
+    if (!got) USBS_CUDA(cudaMemsetAsync(Q + (int64_t)(j + 1) * ldq, 0, n * sizeof(double), st));
+    const int M1 = m + 1;
+    double zero = 0.0;
+    USBS_CUDA(cudaMemcpyAsync(H + (j + 1) * M1 + j, &zero, sizeof(double), cudaMemcpyHostToDevice, st));
+    USBS_CUDA(cudaMemcpyAsync(H + j * M1 + (j + 1), &zero, sizeof(double), cudaMemcpyHostToDevice, st));
+    USBS_CUDA(cudaStreamSynchronize(st));
+    a.cycle0 = hf[F_CYCLE]; a.ell0 = hf[F_ELL]; a.j0 = j + 1; a.restarts0 = hf[F_RESTARTS];
+    a.nhist0 = hf[F_NHIST]; a.matvecs0 = hf[F_MATVECS]; a.wbuf0 = hf[F_PENDING];
+    a.first_from_q = 1;
+    USBS_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), st));
+  }
+  const int nh = hf[F_NHIST];
+  double* ho = ctx->pinned;
+  USBS_CUDA(cudaMemcpyAsync(ho, a.theta, (size_t)k_c * sizeof(double), cudaMemcpyDeviceToHost, st));
+  USBS_CUDA(cudaMemcpyAsync(ho + 64, a.res, (size_t)k_c * sizeof(double), cudaMemcpyDeviceToHost, st));
+  USBS_CUDA(cudaMemcpyAsync(ho + 128, a.hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, st));
+  USBS_CUDA(cudaStreamSynchronize(st));
+  for (int u = 0; u < k_c; ++u) {
+    vals[u] = ho[u];
+    res[u] = ho[64 + u];
+  }
+  for (int h = 0; h < nh; ++h) ritz_hist[h] = ho[128 + h];
+  *converged = hf[F_CONV];
+  *restarts = hf[F_RESTARTS];
+  *n_hist = nh;
+  *matvecs = hf[F_MATVECS];
+  USBS_API_END
+}

@@ -1,0 +1,457 @@
+// Context, problem upload, slack assembly (Z = C - A*(y)) and the
+// operator apply Y = M V (K1) with an optional V^T Y Gram epilogue.
+//
+// Reference behaviour replaced (paths under /root/reference/pkg/src/specbundle):
+//   problem.py:311-314  dual_slack_operator: CSR of C - A*(y) rebuilt per call,
+//                       matvec/matmat through scipy _sparsetools csr_matvec(s)
+//   problem.py:160-161, 214-220  adjoint_matrix (diag / entry families)
+//   problem.py:284-286  cost_quad = sym(V^T C V)
+//   subqp.py:459        V^T A*(y) V - V^T C V  (= -sym(V^T Z V))
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "usbs_common.cuh"
+#include "usbs_kernels.cuh"
+
+namespace usbs {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+// ----------------------------------------------------------------- assembly
+// zval[s] = cval[s] - sum_{e in slot s} y[idx[e]] * val[e]   (problem.py:313)
+__global__ void k_slack_assemble(int64_t nnz, const double* __restrict__ cval,
+                                 const int* __restrict__ aptr, const int* __restrict__ aent,
+                                 const int* __restrict__ eidx, const double* __restrict__ eval,
+                                 const double* __restrict__ y, double* __restrict__ zval) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int a = aptr[s], b = aptr[s + 1];
+    double acc = 0.0;
+    for (int t = a; t < b; ++t) {
+      int e = aent[t];
+      acc += y[eidx[e]] * eval[e];
+    }
+    zval[s] = (a == b) ? cval[s] : cval[s] - acc;
+  }
+}
+
+// diag_only fast path: copy C values, then overwrite the n diagonal slots
+__global__ void k_slack_diag(int64_t n, const int* __restrict__ dslot, const double* __restrict__ cval,
+                             const double* __restrict__ y, double* __restrict__ zval) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int s = dslot[i];
+    zval[s] = cval[s] - y[i];
+  }
+}
+
+// ----------------------------------------------------------------- SpMM
+// Y[row, :] = sum_nz M[row, col] * V[col, :], one LG-lane group per item,
+// lane t owns output column t (column chunks of LG for k > LG).
+template <int LG>
+__global__ void __launch_bounds__(256) k_spmm(int n_items, const int* __restrict__ it_row,
+                                              const int* __restrict__ it_beg,
+                                              const int* __restrict__ it_end,
+                                              const int* __restrict__ it_slot,
+                                              const int* __restrict__ col,
+                                              const double* __restrict__ val,
+                                              const double* __restrict__ V, int64_t ldv, int k,
+                                              double* __restrict__ Y, int64_t ldy,
+                                              double* __restrict__ partial) {
+  const int groups_per_block = blockDim.x / LG;
+  const int g = threadIdx.x / LG, t = threadIdx.x % LG;
+  for (int it = blockIdx.x * groups_per_block + g; it < n_items; it += gridDim.x * groups_per_block) {
+    const int row = it_row[it], b = it_beg[it], e = it_end[it], slot = it_slot[it];
+    for (int c0 = 0; c0 < k; c0 += LG) {
+      const int c = c0 + t;
+      const bool on = c < k;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int z = b;
+      for (; z + 4 <= e; z += 4) {
+        int j0 = col[z], j1 = col[z + 1], j2 = col[z + 2], j3 = col[z + 3];
+        double v0 = val[z], v1 = val[z + 1], v2 = val[z + 2], v3 = val[z + 3];
+        if (on) {
+          a0 = fma(v0, V[(int64_t)j0 * ldv + c], a0);
+          a1 = fma(v1, V[(int64_t)j1 * ldv + c], a1);
+          a2 = fma(v2, V[(int64_t)j2 * ldv + c], a2);
+          a3 = fma(v3, V[(int64_t)j3 * ldv + c], a3);
+        }
+      }
+      for (; z < e; ++z) {
+        int j0 = col[z];
+        double v0 = val[z];
+        if (on) a0 = fma(v0, V[(int64_t)j0 * ldv + c], a0);
+      }
+      double acc = (a0 + a1) + (a2 + a3);
+      if (on) {
+        if (slot < 0) Y[(int64_t)row * ldy + c] = acc;
+        else partial[(int64_t)slot * k + c] = acc;
+      }
+    }
+  }
+}
+
+// combine the partials of split rows in a fixed order (deterministic)
+__global__ void k_spmm_combine(int n_sr, const int* __restrict__ sr_row, const int* __restrict__ sr_first,
+                               const int* __restrict__ sr_count, const double* __restrict__ partial,
+                               int k, double* __restrict__ Y, int64_t ldy) {
+  int64_t total = (int64_t)n_sr * k;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(x / k), c = (int)(x % k);
+    int f = sr_first[r], cnt = sr_count[r];
+    double acc = 0.0;
+    for (int s = 0; s < cnt; ++s) acc += partial[(int64_t)(f + s) * k + c];
+    Y[(int64_t)sr_row[r] * ldy + c] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- host helpers
+static int pick_group(double avg) {
+  int g = 4;
+  while (g < 32 && g < avg) g <<= 1;
+  return g;
+}
+
+}  // namespace usbs
+
+using namespace usbs;
+
+extern "C" {
+
+int usbs_abi_version(void) { return USBS_ABI_VERSION; }
+
+const char* usbs_last_error(void) { return g_err.c_str(); }
+
+usbs_status usbs_ctx_create(int device, void* stream, usbs_ctx** out) {
+  USBS_API_BEGIN
+  if (!out) fail(USBS_ERR_CONFIG, "null output pointer");
+  USBS_CUDA(cudaSetDevice(device));
+  auto* c = new usbs_ctx();
+  c->device = device;
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    USBS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  cudaDeviceProp prop;
+  USBS_CUDA(cudaGetDeviceProperties(&prop, device));
+  c->num_sms = prop.multiProcessorCount;
+  USBS_CUDA(cudaMallocHost(&c->pinned, 4096 * sizeof(double)));
+  USBS_CUDA(cudaMallocHost(&c->pinned_i, 256 * sizeof(int)));
+  *out = c;
+  USBS_API_END
+}
+
+usbs_status usbs_ctx_destroy(usbs_ctx* c) {
+  USBS_API_BEGIN
+  if (!c) return USBS_OK;
+  cudaStreamSynchronize(c->stream);
+  c->ws.release();
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->pinned_i) cudaFreeHost(c->pinned_i);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  USBS_API_END
+}
+
+usbs_status usbs_ctx_sync(usbs_ctx* c) {
+  USBS_API_BEGIN
+  USBS_CUDA(cudaStreamSynchronize(c->stream));
+  USBS_API_END
+}
+
+int64_t usbs_ctx_launches(usbs_ctx* c) { return c ? c->launches : -1; }
+
+usbs_status usbs_memcpy_h2d(usbs_ctx* c, void* dst, const void* src, int64_t bytes) {
+  USBS_API_BEGIN
+  if (bytes > 0) {
+    USBS_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, c->stream));
+    USBS_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  USBS_API_END
+}
+
+usbs_status usbs_memcpy_d2h(usbs_ctx* c, void* dst, const void* src, int64_t bytes) {
+  USBS_API_BEGIN
+  if (bytes > 0) {
+    USBS_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, c->stream));
+    USBS_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  USBS_API_END
+}
+
+usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64_t* c_indptr,
+                                const int32_t* c_indices, const double* c_data, int64_t ne,
+                                const int64_t* e_idx, const int64_t* e_rows, const int64_t* e_cols,
+                                const double* e_vals, int diag_only, usbs_problem** out) {
+  USBS_API_BEGIN
+  if (!ctx || !out) fail(USBS_ERR_CONFIG, "null context/output");
+  if (n < 1 || m < 0 || ne < 0) fail(USBS_ERR_SHAPE, "invalid problem dimensions");
+  if (n >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "n exceeds int32 indexing");
+  USBS_CUDA(cudaSetDevice(ctx->device));
+  auto* p = new usbs_problem();
+  p->ctx = ctx;
+  p->n = n;
+  p->m = m;
+  p->ne = ne;
+  p->diag_only = diag_only != 0;
+  p->nnz_c = c_indptr[n];
+
+  // --- extra (row, col, entry, role) pairs from the constraint entries
+  std::vector<int64_t> xcnt(n + 1, 0);
+  for (int64_t e = 0; e < ne; ++e) {
+    int64_t r = e_rows[e], c = e_cols[e], ci = e_idx[e];
+    if (r < 0 || c < 0 || r >= n || c >= n || r > c) fail(USBS_ERR_SHAPE, "constraint entry out of range or rows > cols");
+    if (ci < 0 || ci >= m) fail(USBS_ERR_SHAPE, "constraint index out of range");
+    xcnt[r + 1]++;
+    if (r != c) xcnt[c + 1]++;
+  }
+  for (int64_t i = 0; i < n; ++i) xcnt[i + 1] += xcnt[i];
+  std::vector<int32_t> xcol(xcnt[n]);
+  std::vector<int64_t> xent(xcnt[n]);
+  {
+    std::vector<int64_t> pos(xcnt.begin(), xcnt.end() - 1);
+    for (int64_t e = 0; e < ne; ++e) {
+      int64_t r = e_rows[e], c = e_cols[e];
+      xcol[pos[r]] = (int32_t)c;
+      xent[pos[r]++] = e;
+      if (r != c) {
+        xcol[pos[c]] = (int32_t)r;
+        xent[pos[c]++] = e;
+      }
+    }
+  }
+  // --- merge per row: C columns (sorted copy) with the extra columns
+  std::vector<int64_t> rowptr(n + 1, 0);
+  std::vector<int32_t> col;
+  std::vector<double> cval;
+  std::vector<int64_t> slot_of_x(xcnt[n]);
+  col.reserve(p->nnz_c + xcnt[n]);
+  cval.reserve(p->nnz_c + xcnt[n]);
+  std::vector<std::pair<int32_t, double>> crow;
+  std::vector<std::pair<int32_t, int64_t>> xrow;
+  for (int64_t i = 0; i < n; ++i) {
+    crow.clear();
+    for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) {
+      if (c_indices[z] < 0 || c_indices[z] >= n) fail(USBS_ERR_SHAPE, "cost column index out of range");
+      crow.emplace_back(c_indices[z], c_data[z]);
+    }
+    if (!std::is_sorted(crow.begin(), crow.end(),
+                        [](auto& a, auto& b) { return a.first < b.first; }))
+      std::stable_sort(crow.begin(), crow.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    xrow.clear();
+    for (int64_t t = xcnt[i]; t < xcnt[i + 1]; ++t) xrow.emplace_back(xcol[t], t);
+    std::stable_sort(xrow.begin(), xrow.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    size_t a = 0, b = 0;
+    while (a < crow.size() || b < xrow.size()) {
+      int32_t cc = INT32_MAX;
+      if (a < crow.size()) cc = crow[a].first;
+      if (b < xrow.size()) cc = std::min(cc, xrow[b].first);
+      double v = 0.0;
+      while (a < crow.size() && crow[a].first == cc) v += crow[a++].second;  // duplicate C entries summed
+      int64_t s = (int64_t)col.size();
+      while (b < xrow.size() && xrow[b].first == cc) slot_of_x[xrow[b++].second] = s;
+      col.push_back(cc);
+      cval.push_back(v);
+    }
+    rowptr[i + 1] = (int64_t)col.size();
+  }
+  p->nnz = (int64_t)col.size();
+  if (p->nnz >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "nnz exceeds int32 indexing");
+  // --- slot -> entries (ascending entry id within a slot)
+  std::vector<int32_t> aptr(p->nnz + 1, 0);
+  for (int64_t t = 0; t < (int64_t)slot_of_x.size(); ++t) aptr[slot_of_x[t] + 1]++;
+  for (int64_t s = 0; s < p->nnz; ++s) aptr[s + 1] += aptr[s];
+  std::vector<int32_t> aent(aptr[p->nnz]);
+  {
+    std::vector<std::pair<int64_t, int64_t>> tmp(slot_of_x.size());
+    for (int64_t t = 0; t < (int64_t)slot_of_x.size(); ++t) tmp[t] = {slot_of_x[t], xent[t]};
+    std::sort(tmp.begin(), tmp.end());
+    for (size_t t = 0; t < tmp.size(); ++t) aent[t] = (int32_t)tmp[t].second;
+  }
+  std::vector<int32_t> rp32(n + 1);
+  for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rowptr[i];
+
+  // --- work items (row segments)
+  double avg = (double)p->nnz / (double)n;
+  p->spmv_group = pick_group(avg);
+  const int SEG = 16 * p->spmv_group;
+  std::vector<int32_t> irow, ibeg, iend, islot, srow, sfirst, scount;
+  int nsplit = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t b = rp32[i], e = rp32[i + 1];
+    if (e - b <= SEG) {
+      irow.push_back((int32_t)i); ibeg.push_back(b); iend.push_back(e); islot.push_back(-1);
+    } else {
+      srow.push_back((int32_t)i); sfirst.push_back(nsplit);
+      int cnt = 0;
+      for (int32_t z = b; z < e; z += SEG) {
+        irow.push_back((int32_t)i); ibeg.push_back(z); iend.push_back(std::min(e, z + SEG));
+        islot.push_back(nsplit++); cnt++;
+      }
+      scount.push_back(cnt);
+    }
+  }
+  p->n_items = (int)irow.size();
+  p->n_split_items = nsplit;
+  p->n_split_rows = (int)srow.size();
+
+  // --- Lanczos block partition (row aligned, balanced on nnz + row cost)
+  int G = (int)std::min<int64_t>(ctx->num_sms,
+                                 std::max<int64_t>(1, std::max<int64_t>((n + 63) / 64, (p->nnz + n + 4095) / 4096)));
+  if (const char* env = getenv("USBS_LZ_BLOCKS")) G = std::max(1, std::min(ctx->num_sms, atoi(env)));
+  p->lz_blocks = G;
+  std::vector<int32_t> blk_row(G + 1, (int32_t)n), blk_item(G + 1, p->n_items), blk_sr(G + 1, p->n_split_rows);
+  {
+    const double ROWCOST = 4.0;
+    double total = (double)p->nnz + ROWCOST * n;
+    double acc = 0.0;
+    int b = 0;
+    blk_row[0] = 0;
+    for (int64_t i = 0; i < n && b + 1 < G; ++i) {
+      acc += (rp32[i + 1] - rp32[i]) + ROWCOST;
+      if (acc >= total * (b + 1) / G) blk_row[++b] = (int32_t)(i + 1);
+    }
+    for (int bb = b + 1; bb < G; ++bb) blk_row[bb] = (int32_t)n;
+    blk_row[G] = (int32_t)n;
+    // items and split rows are sorted by row: locate the boundaries
+    for (int bb = 0; bb <= G; ++bb) {
+      blk_item[bb] = (int32_t)(std::lower_bound(irow.begin(), irow.end(), blk_row[bb]) - irow.begin());
+      blk_sr[bb] = (int32_t)(std::lower_bound(srow.begin(), srow.end(), blk_row[bb]) - srow.begin());
+    }
+  }
+  std::vector<int32_t> diag_slot;
+  if (p->diag_only) {
+    if (m != n || ne != n) fail(USBS_ERR_SHAPE, "diag_only requires m == n == entries");
+    diag_slot.resize(n);
+    for (int64_t e = 0; e < ne; ++e) {
+      if (e_rows[e] != e_cols[e] || e_idx[e] != e_rows[e] || e_vals[e] != 1.0)
+        fail(USBS_ERR_SHAPE, "diag_only entries must be (i, i, i, 1.0)");
+      diag_slot[e_rows[e]] = (int32_t)slot_of_x[xcnt[e_rows[e]] + 0];
+    }
+    // slot_of_x for row r's single extra entry: recompute robustly
+    for (int64_t i = 0; i < n; ++i) {
+      auto it = std::lower_bound(col.begin() + rowptr[i], col.begin() + rowptr[i + 1], (int32_t)i);
+      diag_slot[i] = (int32_t)(it - col.begin());
+    }
+  }
+
+  // --- upload
+  p->rowptr = dev_upload(p, rp32.data(), rp32.size());
+  p->col = dev_upload(p, col.data(), col.size());
+  p->cval = dev_upload(p, cval.data(), cval.size());
+  p->zval = dev_alloc<double>(p, p->nnz);
+  USBS_CUDA(cudaMemcpy(p->zval, p->cval, p->nnz * sizeof(double), cudaMemcpyDeviceToDevice));
+  p->aptr = dev_upload(p, aptr.data(), aptr.size());
+  p->aent = dev_upload(p, aent.data(), aent.size());
+  {
+    std::vector<int32_t> ei(ne), er(ne), ec(ne);
+    for (int64_t e = 0; e < ne; ++e) {
+      ei[e] = (int32_t)e_idx[e]; er[e] = (int32_t)e_rows[e]; ec[e] = (int32_t)e_cols[e];
+    }
+    p->e_idx = dev_upload(p, ei.data(), ne);
+    p->e_row = dev_upload(p, er.data(), ne);
+    p->e_col = dev_upload(p, ec.data(), ne);
+    p->e_val = dev_upload(p, e_vals, ne);
+  }
+  if (p->diag_only) p->diag_slot = dev_upload(p, diag_slot.data(), n);
+  p->it_row = dev_upload(p, irow.data(), irow.size());
+  p->it_beg = dev_upload(p, ibeg.data(), ibeg.size());
+  p->it_end = dev_upload(p, iend.data(), iend.size());
+  p->it_slot = dev_upload(p, islot.data(), islot.size());
+  p->sr_row = dev_upload(p, srow.data(), srow.size());
+  p->sr_first = dev_upload(p, sfirst.data(), sfirst.size());
+  p->sr_count = dev_upload(p, scount.data(), scount.size());
+  p->blk_row = dev_upload(p, blk_row.data(), blk_row.size());
+  p->blk_item = dev_upload(p, blk_item.data(), blk_item.size());
+  p->blk_sr = dev_upload(p, blk_sr.data(), blk_sr.size());
+  *out = p;
+  USBS_API_END
+}
+
+usbs_status usbs_problem_destroy(usbs_problem* p) {
+  USBS_API_BEGIN
+  if (!p) return USBS_OK;
+  cudaStreamSynchronize(p->ctx->stream);
+  for (void* d : p->owned) cudaFree(d);
+  delete p;
+  USBS_API_END
+}
+
+usbs_status usbs_problem_info(usbs_problem* p, int64_t* nnz_z, int64_t* nnz_c, int* lz_blocks,
+                              int* group) {
+  USBS_API_BEGIN
+  if (nnz_z) *nnz_z = p->nnz;
+  if (nnz_c) *nnz_c = p->nnz_c;
+  if (lz_blocks) *lz_blocks = p->lz_blocks;
+  if (group) *group = p->spmv_group;
+  USBS_API_END
+}
+
+usbs_status usbs_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y) {
+  USBS_API_BEGIN
+  launch_slack_assemble(ctx, p, y);
+  USBS_API_END
+}
+
+usbs_status usbs_op_apply(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int64_t ldv, int k,
+                          double* Y, int64_t ldy, double* gram) {
+  USBS_API_BEGIN
+  if (k < 1 || ldv < k || ldy < k) fail(USBS_ERR_SHAPE, "op_apply: bad k / leading dimension");
+  launch_spmm(ctx, p, which, V, ldv, k, Y, ldy);
+  if (gram) launch_gram_tn(ctx, p->n, V, ldv, k, Y, ldy, k, gram, true);
+  USBS_API_END
+}
+
+}  // extern "C"
+
+namespace usbs {
+
+void launch_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y) {
+  if (p->diag_only) {
+    // zval already equals cval off the diagonal (it is only ever written here)
+    int th = 256, bl = (int)std::min<int64_t>((p->n + th - 1) / th, 4 * ctx->num_sms);
+    k_slack_diag<<<bl, th, 0, ctx->stream>>>(p->n, p->diag_slot, p->cval, y, p->zval);
+    check_launch(ctx);
+  } else {
+    int th = 256, bl = (int)std::min<int64_t>((p->nnz + th - 1) / th, 8 * ctx->num_sms);
+    k_slack_assemble<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->nnz, p->cval, p->aptr, p->aent, p->e_idx,
+                                                              p->e_val, y, p->zval);
+    check_launch(ctx);
+  }
+}
+
+void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int64_t ldv, int k,
+                 double* Y, int64_t ldy) {
+  const double* val = which ? p->zval : p->cval;
+  double* partial = nullptr;
+  if (p->n_split_items) partial = (double*)ctx->ws.get(WS_SPMM_PARTIAL, (size_t)p->n_split_items * k * sizeof(double));
+  const int th = 256;
+  if (k <= 16) {
+    int per = th / 16;
+    int bl = (int)std::min<int64_t>((p->n_items + per - 1) / per, 16 * ctx->num_sms);
+    k_spmm<16><<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,
+                                                        p->col, val, V, ldv, k, Y, ldy, partial);
+  } else {
+    int per = th / 32;
+    int bl = (int)std::min<int64_t>((p->n_items + per - 1) / per, 16 * ctx->num_sms);
+    k_spmm<32><<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,
+                                                        p->col, val, V, ldv, k, Y, ldy, partial);
+  }
+  check_launch(ctx);
+  if (p->n_split_rows) {
+    int64_t tot = (int64_t)p->n_split_rows * k;
+    int bl = (int)std::min<int64_t>((tot + 255) / 256, 4 * ctx->num_sms);
+    k_spmm_combine<<<std::max(bl, 1), 256, 0, ctx->stream>>>(p->n_split_rows, p->sr_row, p->sr_first,
+                                                             p->sr_count, partial, k, Y, ldy);
+    check_launch(ctx);
+  }
+}
+
+}  // namespace usbs
