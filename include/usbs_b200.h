@@ -49,8 +49,9 @@ typedef struct usbs_problem usbs_problem;
 int usbs_abi_version(void);
 /* Message for the last non-OK status returned on this thread. */
 const char* usbs_last_error(void);
-/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) or
- * NULL for a library-owned stream. */
+/* stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL is the legacy default stream.  All work of the context is ordered on
+ * it, so caller-side copies on the same stream need no extra sync. */
 usbs_status usbs_ctx_create(int device, void* stream, usbs_ctx** out);
 usbs_status usbs_ctx_destroy(usbs_ctx* ctx);
 usbs_status usbs_ctx_sync(usbs_ctx* ctx);
@@ -114,6 +115,72 @@ usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int which, int k_c,
  * k <= 64; a_dev, vals_dev (k), vecs_dev (k x k, columns = eigenvectors). */
 usbs_status usbs_small_eigh(usbs_ctx* ctx, int k, const double* a_dev, double* vals_dev,
                             double* vecs_dev);
+
+/* ---- K12: interior-point bundle subproblem (single CTA) ------------------
+ * _ipm_solve (subqp.py:353-435) behind ipm_quad / ipm_eval (438-448).
+ * Coefficients (dev): Q11 = quad_ss (d x d, NULL = 0 for ipm_eval),
+ * q12 = quad_s_eta (d, NULL = 0), lin_s (d), scal = [quad_eta, lin_eta].
+ * State (dev, usbs_ipm_state_len(k) doubles): S, T (k x k), eta, zeta, omega,
+ * mu, has_eta, k, valid -- IpmState (subqp.py:111-147).  warm_state may be
+ * NULL (cold start) and may alias state_out.
+ * result (dev, 5): value, newton_iters, exact, eta_opt, trailing failures.
+ * opts (host, 8 or NULL = IpmOptions defaults): mu_tol, kkt_tol, max_newton,
+ * step_frac, backtrack, min_step, max_step_failures, warm_blend. */
+usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const double* Q11_dev,
+                           const double* q12_dev, const double* lin_s_dev, const double* scal_dev,
+                           const double* warm_state_dev, double* state_out_dev, double* result_dev,
+                           const double* opts);
+int usbs_ipm_state_len(int k);
+
+/* ---- K5: constraint image A(V S V^T) ------------------------------------
+ * out = beta * base + A(V S V^T); S k x k (s_is_diag = 0) or its diagonal
+ * (s_is_diag = 1: A(U diag(l) U^T)).  primal_image_lowrank / _factor
+ * (problem.py:151-155, 200-208).  base may be NULL. */
+usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* v_dev, int64_t ldv,
+                            int k, const double* s_dev, int s_is_diag, double s_scale,
+                            const double* beta_dev, double beta, const double* base_dev,
+                            double* out_dev);
+/* (S is scaled by s_scale; beta is multiplied by *beta_dev when non-NULL) */
+
+/* ---- K4/K4w: compressed constraint rows c_i = svec(V^T A_i V) -----------
+ * gram_out = scale_gram * C^T C (d x d), a_out = scale_a * C^T a,
+ * w_out = scale_w * C^T w; any output may be NULL.  compressed_rows
+ * (problem.py:169-173, 229-239) and its uses in assemble_quad_coeffs
+ * (subqp.py:487-498, 510).  C is never materialised. */
+usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* v_dev,
+                                 int64_t ldv, int k, double scale_gram, double* gram_out_dev,
+                                 const double* a_dev, double scale_a, double* a_out_dev,
+                                 const double* w_dev, double scale_w, double* w_out_dev);
+
+/* ---- tall-skinny dense helpers (row-major blocks, k <= 64) -------------- */
+/* Y = alpha (X diag(xs)) B + beta Y0 (X n x ka, B ka x kb with ld ldb, dev;
+ * xs (ka) and Y0 may be NULL; Y0 may alias Y) */
+usbs_status usbs_rowgemm(usbs_ctx* ctx, int64_t n, const double* x_dev, int64_t ldx, int ka,
+                         const double* b_dev, int64_t ldb, int kb, const double* xs_dev,
+                         double alpha, double beta, const double* y0_dev, int64_t ldy0,
+                         double* y_dev, int64_t ldy);
+/* out = A^T B (ka x kb); sym: 0.5 (G + G^T) */
+usbs_status usbs_gram(usbs_ctx* ctx, int64_t n, const double* a_dev, int64_t lda, int ka,
+                      const double* b_dev, int64_t ldb, int kb, double* out_dev, int sym);
+/* out[0] = sum_ij F_ij G_ij w_j  (cost_factor_ip, problem.py:288-289) */
+usbs_status usbs_wcoldot(usbs_ctx* ctx, int64_t n, const double* f_dev, int64_t ldf,
+                         const double* g_dev, int64_t ldg, int k, const double* w_dev,
+                         double* out_dev);
+/* X = eta X + F diag(l) F^T (ExplicitStore.update, bundle.py:108-109) */
+usbs_status usbs_dense_update(usbs_ctx* ctx, int64_t n, double* x_dev, double eta,
+                              const double* f_dev, int64_t ldf, int kc, const double* l_dev);
+/* m-vector operations (op codes in csrc/usbs_book.cu VecOp); red_out (dev, 2)
+ * receives [sum, max] reductions where the op defines them. */
+usbs_status usbs_vec(usbs_ctx* ctx, int op, int64_t m, const double* x, const double* y,
+                     const double* z, const double* b, const double* ineq, double s0, double s1,
+                     double* out, double* red_out);
+/* out (d) = scale * svec(A), A k x k symmetric (symlin.svec, symlin.py:72-79) */
+usbs_status usbs_svec(usbs_ctx* ctx, int k, const double* a_dev, double scale, double* out_dev);
+/* pivoted Cholesky of a c x c Gram with orthonormalize's drop rule
+ * (symlin.py:148-190): perm (dev int, c), Rinv (dev, c x c upper, ld c),
+ * info (dev, 3) = [rank, min selected residual ratio, max column norm]. */
+usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* g_dev, double drop_tol,
+                         int* perm_dev, double* rinv_dev, double* info_dev);
 
 #ifdef __cplusplus
 }

@@ -45,7 +45,23 @@ PROTOS = {
     "usbs_lanczos_top": (_i32, [_p, _p, _i32, _i32, _i32, _i32, C.c_double, _p, RNG_FILL, _p,
                                  _pd, _p, _i64, _pd, _pi, _pi, _pd, _pi, _pi]),
     "usbs_small_eigh": (_i32, [_p, _i32, _p, _p, _p]),
+    "usbs_ipm_solve": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "usbs_ipm_state_len": (_i32, [_i32]),
+    "usbs_cons_image": (_i32, [_p, _p, _p, _i64, _i32, _p, _i32, C.c_double, _p, C.c_double, _p, _p]),
+    "usbs_cons_compressed": (_i32, [_p, _p, _p, _i64, _i32, C.c_double, _p, _p, C.c_double, _p, _p,
+                                    C.c_double, _p]),
+    "usbs_rowgemm": (_i32, [_p, _i64, _p, _i64, _i32, _p, _i64, _i32, _p, C.c_double, C.c_double, _p, _i64, _p,
+                            _i64]),
+    "usbs_gram": (_i32, [_p, _i64, _p, _i64, _i32, _p, _i64, _i32, _p, _i32]),
+    "usbs_wcoldot": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i32, _p, _p]),
+    "usbs_dense_update": (_i32, [_p, _i64, _p, C.c_double, _p, _i64, _i32, _p]),
+    "usbs_vec": (_i32, [_p, _i32, _i64, _p, _p, _p, _p, _p, C.c_double, C.c_double, _p, _p]),
+    "usbs_pivchol": (_i32, [_p, _i32, _p, C.c_double, _p, _p, _p]),
+    "usbs_svec": (_i32, [_p, _i32, _p, C.c_double, _p]),
 }
+
+# VecOp codes (csrc/usbs_book.cu)
+VOP_W, VOP_PROJN, VOP_AXPBY, VOP_NUNEXT, VOP_CAND, VOP_RESID, VOP_DOT, VOP_MINI, VOP_RELU, VOP_DOTAFF = range(10)
 
 # symbols declared in include/usbs_b200.h that must be exported (checked by tests)
 _lib = None

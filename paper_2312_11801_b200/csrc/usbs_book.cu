@@ -1,0 +1,669 @@
+// Low-rank primal bookkeeping kernels (K4, K4w, K5, K8, K10, K13, K14 of
+// SURVEY 2.2).  Reference behaviour (paths under pkg/src/specbundle/):
+//   problem.py:151-155, 200-208  primal_image_lowrank / primal_image_factor
+//   problem.py:169-173, 229-239  compressed_rows (never materialised here:
+//                                rows are generated tile by tile in smem)
+//   subqp.py:487-498, 509-510    quad_ss = a^2/rho C^T C, quad_s_eta, C^T w
+//   bundle.py:307-316            F = V Q_c, trace / cost / image statistics
+//   sketch.py:58-74              P <- eta P + (F L)(F^T Psi)
+//   bundle.py:108-109            Xbar <- eta Xbar + F L F^T
+//   problem.py:292-308, bundle.py:239-255, 344-372, subqp.py:595-598
+//                                projections, candidate, residual norms
+#include <algorithm>
+#include <cmath>
+
+#include "usbs_common.cuh"
+#include "usbs_kernels.cuh"
+
+namespace usbs {
+
+// ------------------------------------------------------------- K5 images
+// out[i] = beta*base[i] + A_i(V S V^T); S full k x k (sdiag=0) or diag (sdiag=1)
+__global__ void k_image_diag(int64_t n, const double* __restrict__ V, int64_t ldv, int k,
+                             const double* __restrict__ S, int sdiag, double sscale, const double* beta_dev,
+                             double beta, const double* __restrict__ base, double* __restrict__ out) {
+  __shared__ double Ss[64 * 64];
+  for (int x = threadIdx.x; x < (sdiag ? k : k * k); x += blockDim.x) Ss[x] = sscale * S[x];
+  if (beta_dev) beta *= beta_dev[0];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* v = V + i * ldv;
+    double acc = 0.0;
+    if (sdiag) {
+      for (int j = 0; j < k; ++j) acc = fma(v[j] * v[j], Ss[j], acc);
+    } else {
+      for (int j = 0; j < k; ++j) {
+        double t = 0.0;
+        for (int l = 0; l < k; ++l) t = fma(Ss[j * k + l], v[l], t);
+        acc = fma(v[j], t, acc);
+      }
+    }
+    out[i] = (base ? beta * base[i] : 0.0) + acc;
+  }
+}
+
+__global__ void k_image_entries(int64_t m, const int* __restrict__ cptr, const int* __restrict__ cent,
+                                const int* __restrict__ erow, const int* __restrict__ ecol,
+                                const double* __restrict__ eval, const double* __restrict__ V, int64_t ldv,
+                                int k, const double* __restrict__ S, int sdiag, double sscale,
+                                const double* beta_dev, double beta, const double* __restrict__ base,
+                                double* __restrict__ out) {
+  __shared__ double Ss[64 * 64];
+  for (int x = threadIdx.x; x < (sdiag ? k : k * k); x += blockDim.x) Ss[x] = sscale * S[x];
+  if (beta_dev) beta *= beta_dev[0];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int t = cptr[i]; t < cptr[i + 1]; ++t) {
+      const int e = cent[t];
+      const int r = erow[e], c = ecol[e];
+      const double* vr = V + (int64_t)r * ldv;
+      const double* vc = V + (int64_t)c * ldv;
+      double q = 0.0;
+      if (sdiag) {
+        for (int j = 0; j < k; ++j) q = fma(vr[j] * Ss[j], vc[j], q);
+      } else {
+        for (int j = 0; j < k; ++j) {
+          double mid = 0.0;
+          for (int l = 0; l < k; ++l) mid = fma(vr[l], Ss[l * k + j], mid);
+          q = fma(mid, vc[j], q);
+        }
+      }
+      const double eff = (r == c) ? eval[e] : 2.0 * eval[e];
+      acc += q * eff;
+    }
+    out[i] = (base ? beta * base[i] : 0.0) + acc;
+  }
+}
+
+// -------------------------------------------------- K4 / K4w compressed rows
+// Row i of the (never stored) compressed matrix: c_i[p] = svec(V^T A_i V)[p].
+// Tiles of TR constraints are generated into smem; each thread accumulates
+// TPT 4x4 lower tiles of C^T C plus its share of C^T a and C^T w.
+constexpr int CTR = 32;
+
+__device__ __forceinline__ double crow_entry(int diag_only, int64_t i, int a, int b, double wp,
+                                             const int* __restrict__ cptr, const int* __restrict__ cent,
+                                             const int* __restrict__ erow, const int* __restrict__ ecol,
+                                             const double* __restrict__ eval, const double* __restrict__ V,
+                                             int64_t ldv) {
+  if (diag_only) {
+    const double* v = V + i * ldv;
+    return v[a] * v[b] * wp;
+  }
+  double s = 0.0;
+  for (int t = cptr[i]; t < cptr[i + 1]; ++t) {
+    const int e = cent[t];
+    const int r = erow[e], c = ecol[e];
+    const double* vr = V + (int64_t)r * ldv;
+    const double* vc = V + (int64_t)c * ldv;
+    double g = vr[a] * vc[b] + vc[a] * vr[b];
+    if (r == c) g *= 0.5;
+    s += g * eval[e] * wp;
+  }
+  return s;
+}
+
+template <int TPT>
+__global__ void __launch_bounds__(256) k_compressed(int64_t m, int diag_only, const int* __restrict__ cptr,
+                                                    const int* __restrict__ cent, const int* __restrict__ erow,
+                                                    const int* __restrict__ ecol, const double* __restrict__ eval,
+                                                    const double* __restrict__ V, int64_t ldv, int k, int d,
+                                                    const double* __restrict__ avec, const double* __restrict__ wvec,
+                                                    int do_gram, double* __restrict__ gpart,
+                                                    double* __restrict__ apart, double* __restrict__ wpart) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int dp = d + 1;  // padded row stride
+  double* tile = (double*)smem_raw;         // CTR * dp
+  double* aw = tile + CTR * dp;              // CTR
+  double* ww = aw + CTR;                     // CTR
+  unsigned char* pi = (unsigned char*)(ww + CTR);
+  unsigned char* pj = pi + 600;
+  if (threadIdx.x == 0) {
+    int p = 0;
+    for (int j = 0; j < k; ++j)
+      for (int i = j; i < k; ++i) { pi[p] = (unsigned char)i; pj[p] = (unsigned char)j; ++p; }
+  }
+  const int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = blockIdx.x * chunk, c1 = min(m, c0 + chunk);
+  const int nt = (d + 3) / 4;
+  const int ntiles = nt * (nt + 1) / 2;
+  double acc[TPT][16];
+  int tr_[TPT], tc_[TPT];
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+#pragma unroll
+    for (int x = 0; x < 16; ++x) acc[u][x] = 0.0;
+    int tix = threadIdx.x + u * 256;
+    tr_[u] = -1;
+    tc_[u] = 0;
+    if (do_gram && tix < ntiles) {
+      int r = (int)((sqrtf(8.0f * tix + 1.0f) - 1.0f) * 0.5f);
+      while (r * (r + 1) / 2 > tix) --r;
+      while ((r + 1) * (r + 2) / 2 <= tix) ++r;
+      tr_[u] = r;
+      tc_[u] = tix - r * (r + 1) / 2;
+    }
+  }
+  double accA[3] = {0, 0, 0}, accW[3] = {0, 0, 0};  // d <= 768 with 256 threads
+  __syncthreads();
+  for (int64_t base = c0; base < c1; base += CTR) {
+    const int rows = (int)min((int64_t)CTR, c1 - base);
+    __syncthreads();
+    for (int x = threadIdx.x; x < CTR * d; x += blockDim.x) {
+      const int r = x / d, p = x % d;
+      double v = 0.0;
+      if (r < rows) {
+        const int a = pi[p], b = pj[p];
+        v = crow_entry(diag_only, base + r, a, b, a == b ? 1.0 : 1.4142135623730951, cptr, cent, erow, ecol,
+                       eval, V, ldv);
+      }
+      tile[r * dp + p] = v;
+    }
+    for (int r = threadIdx.x; r < CTR; r += blockDim.x) {
+      aw[r] = (avec && r < rows) ? avec[base + r] : 0.0;
+      ww[r] = (wvec && r < rows) ? wvec[base + r] : 0.0;
+    }
+    __syncthreads();
+    if (do_gram) {
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        if (tr_[u] < 0) continue;
+        const int pa = tr_[u] * 4, pb = tc_[u] * 4;
+        for (int r = 0; r < rows; ++r) {
+          const double* row = tile + r * dp;
+          double xa[4], xb[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            xa[q] = (pa + q < d) ? row[pa + q] : 0.0;
+            xb[q] = (pb + q < d) ? row[pb + q] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) acc[u][q * 4 + s] = fma(xa[q], xb[s], acc[u][q * 4 + s]);
+        }
+      }
+    }
+    if (avec || wvec) {
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int p = threadIdx.x + u * 256;
+        if (p < d) {
+          double sa = accA[u], sw = accW[u];
+          for (int r = 0; r < rows; ++r) {
+            const double c = tile[r * dp + p];
+            sa = fma(aw[r], c, sa);
+            sw = fma(ww[r], c, sw);
+          }
+          accA[u] = sa;
+          accW[u] = sw;
+        }
+      }
+    }
+  }
+  // partials: gram as full d x d (lower tiles mirrored later), vectors
+  if (do_gram) {
+#pragma unroll
+    for (int u = 0; u < TPT; ++u) {
+      if (tr_[u] < 0) continue;
+      const int pa = tr_[u] * 4, pb = tc_[u] * 4;
+      for (int q = 0; q < 4; ++q)
+        for (int s = 0; s < 4; ++s) {
+          const int P = pa + q, Qc = pb + s;
+          if (P < d && Qc < d && Qc <= P) gpart[(int64_t)blockIdx.x * d * d + (int64_t)P * d + Qc] = acc[u][q * 4 + s];
+        }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int p = threadIdx.x + u * 256;
+    if (p < d) {
+      if (apart) apart[(int64_t)blockIdx.x * d + p] = accA[u];
+      if (wpart) wpart[(int64_t)blockIdx.x * d + p] = accW[u];
+    }
+  }
+}
+
+// sum block partials in fixed order; gram output mirrored to full symmetric
+__global__ void k_compressed_final(int nb, int d, const double* __restrict__ gpart, const double* __restrict__ apart,
+                                   const double* __restrict__ wpart, double sg, double sa, double sw,
+                                   double* __restrict__ G, double* __restrict__ A, double* __restrict__ W) {
+  const int64_t tot = (int64_t)d * d;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot + 2 * d;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (x < tot) {
+      if (!G) continue;
+      const int P = (int)(x / d), Qc = (int)(x % d);
+      if (Qc > P) continue;
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b) s += gpart[(int64_t)b * tot + x];
+      G[(int64_t)P * d + Qc] = sg * s;
+      G[(int64_t)Qc * d + P] = sg * s;
+    } else if (x < tot + d) {
+      if (!A) continue;
+      const int p = (int)(x - tot);
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b) s += apart[(int64_t)b * d + p];
+      A[p] = sa * s;
+    } else {
+      if (!W) continue;
+      const int p = (int)(x - tot - d);
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b) s += wpart[(int64_t)b * d + p];
+      W[p] = sw * s;
+    }
+  }
+}
+
+// ------------------------------------------------------------- row GEMM
+// Y[i,:] = alpha * X[i,:] B + beta * Y0[i,:]   (B ka x kb in smem)
+__global__ void k_rowgemm(int64_t n, const double* __restrict__ X, int64_t ldx, int ka,
+                          const double* __restrict__ B, int64_t ldb, int kb, const double* __restrict__ xs,
+                          double alpha, double beta, const double* Y0, int64_t ldy0, double* Y, int64_t ldy) {
+  // B' = diag(xs) B so that Y = alpha (X diag(xs)) B + beta Y0 (sketch.py:71)
+  __shared__ double Bs[64 * 64];
+  for (int x = threadIdx.x; x < ka * kb; x += blockDim.x) {
+    const int u = x / kb, c = x % kb;
+    Bs[x] = B[(int64_t)u * ldb + c];
+  }
+  __shared__ double xsv[64];
+  for (int u = threadIdx.x; u < ka; u += blockDim.x) xsv[u] = xs ? xs[u] : 1.0;
+  __syncthreads();
+  if (xs) {
+    const int64_t tot = n * kb;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = x / kb;
+      const int c = (int)(x % kb);
+      const double* xr = X + i * ldx;
+      double s = 0.0;
+      for (int u = 0; u < ka; ++u) s = fma(xr[u] * xsv[u], Bs[u * kb + c], s);
+      double v = alpha * s;
+      if (Y0) v += beta * Y0[i * ldy0 + c];
+      Y[i * ldy + c] = v;
+    }
+    return;
+  }
+  const int64_t tot = n * kb;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / kb;
+    const int c = (int)(x % kb);
+    const double* xr = X + i * ldx;
+    double s = 0.0;
+    for (int u = 0; u < ka; ++u) s = fma(xr[u], Bs[u * kb + c], s);
+    double v = alpha * s;
+    if (Y0) v += beta * Y0[i * ldy0 + c];
+    Y[i * ldy + c] = v;
+  }
+}
+
+// sum_i sum_j F[i,j] G[i,j] w[j]  (deterministic two-pass)
+__global__ void k_wcoldot_partial(int64_t n, const double* __restrict__ F, int64_t ldf,
+                                  const double* __restrict__ G, int64_t ldg, int k,
+                                  const double* __restrict__ w, double* __restrict__ part) {
+  __shared__ double red[32];
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  double s = 0.0;
+  for (int64_t x = r0 * k + threadIdx.x; x < r1 * k; x += blockDim.x) {
+    const int64_t i = x / k;
+    const int j = (int)(x % k);
+    s = fma(F[i * ldf + j] * G[i * ldg + j], w[j], s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_sum_partials(int nb, const double* __restrict__ part, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    out[0] = s;
+  }
+}
+
+// X = eta X + F diag(l) F^T  (n x n dense, explicit store)
+__global__ void k_dense_update(int64_t n, double* __restrict__ X, double eta, const double* __restrict__ F,
+                               int64_t ldf, int kc, const double* __restrict__ l) {
+  const int64_t tot = n * n;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = x / n, c = x % n;
+    double s = 0.0;
+    for (int j = 0; j < kc; ++j) s = fma(F[r * ldf + j] * l[j], F[c * ldf + j], s);
+    X[x] = eta * X[x] + s;
+  }
+}
+
+// ------------------------------------------------------------- vector ops
+enum VecOp {
+  VOP_W = 0,         // out = y - (b + nu)/rho
+  VOP_PROJN = 1,     // out = ineq ? min(z, 0) : 0
+  VOP_AXPBY = 2,     // out = a*x + b*y
+  VOP_NUNEXT = 3,    // out = projN(ax + rho*y - b); red0 += (out - nu)^2
+  VOP_CAND = 4,      // out = y - (b - ax)/rho; ineq: nu<0 -> 0 else max(.,0)
+  VOP_RESID = 5,     // diff = ax - projK(ax): red0 += diff^2, red1 = max|diff|
+  VOP_DOT = 6,       // red0 += x*y
+  VOP_MINI = 7,      // red1 = min over ineq of x  (stored as max of -x)
+  VOP_RELU = 8,      // out = max(x, 0)
+  VOP_DOTAFF = 9,    // red_out[0] = s0 * sum x*y + s1   (only one slot written)
+};
+
+// x, y, z are operand vectors; red: per-block partials [nb][2]
+__global__ void k_vec(int op, int64_t m, const double* __restrict__ x, const double* __restrict__ y,
+                      const double* __restrict__ z, const double* __restrict__ b, const double* __restrict__ ineq,
+                      double s0, double s1, double* __restrict__ out, double* __restrict__ red) {
+  __shared__ double sred[32];
+  double r0 = 0.0, r1 = op == VOP_MINI ? -INFINITY : 0.0;
+  const int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * chunk, i1 = min(m, i0 + chunk);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const bool iq = ineq && ineq[i] != 0.0;
+    switch (op) {
+      case VOP_W: out[i] = x[i] - (b[i] + y[i]) / s0; break;
+      case VOP_PROJN: out[i] = iq ? fmin(x[i], 0.0) : 0.0; break;
+      case VOP_AXPBY: out[i] = s0 * x[i] + (y ? s1 * y[i] : 0.0); break;
+      case VOP_NUNEXT: {
+        double t = x[i] + s0 * y[i] - b[i];
+        double v = iq ? fmin(t, 0.0) : 0.0;
+        out[i] = v;
+        double dlt = v - z[i];
+        r0 = fma(dlt, dlt, r0);
+        break;
+      }
+      case VOP_CAND: {
+        double v = y[i] - (b[i] - x[i]) / s0;
+        if (iq) v = (z[i] < 0.0) ? 0.0 : fmax(v, 0.0);
+        out[i] = v;
+        break;
+      }
+      case VOP_RESID: {
+        double pk = iq ? fmin(x[i], b[i]) : b[i];
+        double dlt = x[i] - pk;
+        r0 = fma(dlt, dlt, r0);
+        r1 = fmax(r1, fabs(dlt));
+        break;
+      }
+      case VOP_DOT:
+      case VOP_DOTAFF: r0 = fma(x[i], y[i], r0); break;
+      case VOP_RELU: out[i] = fmax(x[i], 0.0); break;
+      case VOP_MINI:
+        if (iq) r1 = fmax(r1, -x[i]);
+        break;
+    }
+  }
+  if (red) {
+    double t0 = block_sum(r0, sred);
+    double t1 = warp_max(r1);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = t1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mx = op == VOP_MINI ? -INFINITY : 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sred[w]);
+      red[2 * blockIdx.x] = t0;
+      red[2 * blockIdx.x + 1] = mx;
+    }
+  }
+}
+
+__global__ void k_vec_final(int nb, const double* __restrict__ red, double* __restrict__ out, int is_min,
+                            int affine, double s0, double s1) {
+  if (threadIdx.x == 0) {
+    double s = 0.0, mx = is_min ? -INFINITY : 0.0;
+    for (int b = 0; b < nb; ++b) {
+      s += red[2 * b];
+      mx = fmax(mx, red[2 * b + 1]);
+    }
+    if (affine) {
+      out[0] = s0 * s + s1;
+    } else {
+      out[0] = s;
+      out[1] = mx;
+    }
+  }
+}
+
+// pivoted Cholesky of a small Gram (c <= 64) with the column-pivoted
+// Gram-Schmidt drop rule of symlin.orthonormalize (symlin.py:148-190):
+// pick max remaining norm; stop when <= drop_tol * max input column norm.
+// Outputs: perm[r] (chosen columns), rank, Rinv (r x r upper, row-major, ld c),
+// cond flag = min(selected residual / max norm) for the exact-path guard.
+__global__ void k_pivchol(int c, const double* __restrict__ G, double drop_tol, int* __restrict__ perm,
+                          double* __restrict__ Rinv, double* __restrict__ info) {
+  __shared__ double A[40 * 40];
+  __shared__ double R[40 * 40];
+  __shared__ int alive[40];
+  __shared__ int rank_s;
+  __shared__ double minratio_s, maxn_s;
+  for (int x = threadIdx.x; x < c * c; x += blockDim.x) { A[x] = G[x]; R[x] = 0.0; }
+  for (int x = threadIdx.x; x < c; x += blockDim.x) alive[x] = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < c; ++j) mx = fmax(mx, sqrt(fmax(A[j * c + j], 0.0)));
+    maxn_s = mx;
+    const double thresh = drop_tol < 0.0 ? 0.0 : drop_tol * mx;
+    int r = 0;
+    double minratio = 1.0;
+    if (mx > 0.0) {
+      for (int step = 0; step < c; ++step) {
+        int best = -1;
+        double bn = -1.0;
+        for (int j = 0; j < c; ++j)
+          if (alive[j]) {
+            double nj = sqrt(fmax(A[j * c + j], 0.0));
+            if (drop_tol < 0.0) {  // no pivoting: natural column order
+              best = j;
+              bn = nj;
+              break;
+            }
+            if (nj > bn) { bn = nj; best = j; }
+          }
+        if (best < 0 || bn <= thresh) break;
+        alive[best] = 0;
+        minratio = fmin(minratio, bn / mx);
+        // R row r: R[r][best] = bn, R[r][j] = A[best][j]/bn for alive j (Schur update)
+        perm[r] = best;
+        const double rb = sqrt(A[best * c + best]);
+        // Schur complement update on alive columns
+        for (int j = 0; j < c; ++j)
+          if (alive[j]) {
+            const double l = A[best * c + j] / rb;
+            for (int i2 = 0; i2 < c; ++i2)
+              if (alive[i2]) A[i2 * c + j] -= (A[best * c + i2] / rb) * l;
+          }
+        ++r;
+      }
+    }
+    rank_s = r;
+    minratio_s = minratio;
+  }
+  __syncthreads();
+  // R in pivot order from the original Gram: R = chol(G_pp) for the picked columns
+  const int r = rank_s;
+  if (threadIdx.x == 0 && r > 0) {
+    // Cholesky of G restricted to perm (upper R with G_pp = R^T R)
+    for (int a = 0; a < r; ++a)
+      for (int b2 = 0; b2 < r; ++b2) A[a * 40 + b2] = G[perm[a] * c + perm[b2]];
+    int ok = 1;
+    for (int j = 0; j < r && ok; ++j) {
+      double s = A[j * 40 + j];
+      for (int q = 0; q < j; ++q) s -= R[q * 40 + j] * R[q * 40 + j];
+      if (!(s > 0.0)) { ok = 0; break; }
+      const double rjj = sqrt(s);
+      R[j * 40 + j] = rjj;
+      for (int b2 = j + 1; b2 < r; ++b2) {
+        double t = A[j * 40 + b2];
+        for (int q = 0; q < j; ++q) t -= R[q * 40 + j] * R[q * 40 + b2];
+        R[j * 40 + b2] = t / rjj;
+      }
+      for (int b2 = 0; b2 < j; ++b2) R[j * 40 + b2] = 0.0;
+    }
+    if (!ok) minratio_s = 0.0;
+    // Rinv (upper) by back substitution, column by column
+    for (int col = 0; col < r; ++col)
+      for (int row = r - 1; row >= 0; --row) {
+        double s = (row == col) ? 1.0 : 0.0;
+        for (int q = row + 1; q < r; ++q) s -= R[row * 40 + q] * Rinv[q * c + col];
+        Rinv[row * c + col] = (row <= col) ? s / R[row * 40 + row] : 0.0;
+      }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    info[0] = r;
+    info[1] = minratio_s;
+    info[2] = maxn_s;
+  }
+}
+
+}  // namespace usbs
+
+using namespace usbs;
+
+static int nblocks(usbs_ctx* ctx, int64_t work, int per = 256, int mult = 8) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work + per - 1) / per, (int64_t)mult * ctx->num_sms));
+}
+
+extern "C" {
+
+usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k, const double* S,
+                            int s_is_diag, double s_scale, const double* beta_dev, double beta, const double* base,
+                            double* out) {
+  USBS_API_BEGIN
+  if (k < 1 || k > 64) fail(USBS_ERR_SHAPE, "cons_image: 1 <= k <= 64");
+  if (p->diag_only) {
+    k_image_diag<<<nblocks(ctx, p->n), 256, 0, ctx->stream>>>(p->n, V, ldv, k, S, s_is_diag, s_scale, beta_dev, beta,
+                                                              base, out);
+  } else {
+    k_image_entries<<<nblocks(ctx, p->m), 256, 0, ctx->stream>>>(p->m, p->cptr, p->cent, p->e_row, p->e_col,
+                                                                 p->e_val, V, ldv, k, S, s_is_diag, s_scale, beta_dev,
+                                                                 beta, base, out);
+  }
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k,
+                                 double scale_gram, double* gram_out, const double* a_vec, double scale_a,
+                                 double* a_out, const double* w_vec, double scale_w, double* w_out) {
+  USBS_API_BEGIN
+  if (k < 1 || k > 32) fail(USBS_ERR_SHAPE, "cons_compressed: 1 <= k <= 32");
+  const int d = k * (k + 1) / 2;
+  const int nt = (d + 3) / 4, ntiles = nt * (nt + 1) / 2;
+  const int tpt = gram_out ? (ntiles + 255) / 256 : 1;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (p->m + 63) / 64));
+  const size_t gbytes = gram_out ? (size_t)nb * d * d * sizeof(double) : 0;
+  double* ws = (double*)ctx->ws.get(WS_BOOK, gbytes + (size_t)2 * nb * d * sizeof(double) + 64);
+  double* gpart = gram_out ? ws : nullptr;
+  double* apart = a_vec ? ws + (gram_out ? (size_t)nb * d * d : 0) : nullptr;
+  double* wpart = w_vec ? ws + (gram_out ? (size_t)nb * d * d : 0) + (size_t)nb * d : nullptr;
+  const size_t sm = (size_t)(CTR * (d + 1) + 2 * CTR) * sizeof(double) + 1200;
+  const int dg = gram_out ? 1 : 0;
+#define USBS_COMP(T)                                                                                      \
+  {                                                                                                       \
+    static bool attr = false;                                                                             \
+    if (!attr) {                                                                                          \
+      USBS_CUDA(cudaFuncSetAttribute(k_compressed<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+      attr = true;                                                                                        \
+    }                                                                                                     \
+    k_compressed<T><<<nb, 256, sm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row,  \
+                                                  p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, dg, gpart, \
+                                                  apart, wpart);                                          \
+  }
+  if (tpt <= 1) USBS_COMP(1)
+  else if (tpt <= 2) USBS_COMP(2)
+  else if (tpt <= 4) USBS_COMP(4)
+  else if (tpt <= 6) USBS_COMP(6)
+  else if (tpt <= 8) USBS_COMP(8)
+  else fail(USBS_ERR_SHAPE, "cons_compressed: d too large");
+#undef USBS_COMP
+  check_launch(ctx);
+  k_compressed_final<<<nblocks(ctx, (int64_t)d * d + 2 * d), 256, 0, ctx->stream>>>(
+      nb, d, gpart, apart, wpart, scale_gram, scale_a, scale_w, gram_out, a_vec ? a_out : nullptr,
+      w_vec ? w_out : nullptr);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_rowgemm(usbs_ctx* ctx, int64_t n, const double* X, int64_t ldx, int ka, const double* B,
+                         int64_t ldb, int kb, const double* xs, double alpha, double beta, const double* Y0,
+                         int64_t ldy0, double* Y, int64_t ldy) {
+  USBS_API_BEGIN
+  if (ka < 1 || kb < 1 || ka > 64 || ka * kb > 4096) fail(USBS_ERR_SHAPE, "rowgemm: ka <= 64, ka*kb <= 4096");
+  k_rowgemm<<<nblocks(ctx, n * kb), 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y,
+                                                           ldy);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_gram(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B, int64_t ldb,
+                      int kb, double* out, int sym) {
+  USBS_API_BEGIN
+  launch_gram_tn(ctx, n, A, lda, ka, B, ldb, kb, out, sym != 0);
+  USBS_API_END
+}
+
+usbs_status usbs_wcoldot(usbs_ctx* ctx, int64_t n, const double* F, int64_t ldf, const double* G, int64_t ldg, int k,
+                         const double* w, double* out) {
+  USBS_API_BEGIN
+  int nb = (int)std::min<int64_t>(2 * ctx->num_sms, std::max<int64_t>(1, (n * k + 2047) / 2048));
+  double* part = (double*)ctx->ws.get(WS_RED, (size_t)nb * sizeof(double));
+  k_wcoldot_partial<<<nb, 256, 0, ctx->stream>>>(n, F, ldf, G, ldg, k, w, part);
+  check_launch(ctx);
+  k_sum_partials<<<1, 32, 0, ctx->stream>>>(nb, part, out);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_dense_update(usbs_ctx* ctx, int64_t n, double* X, double eta, const double* F, int64_t ldf, int kc,
+                              const double* lams) {
+  USBS_API_BEGIN
+  k_dense_update<<<nblocks(ctx, n * n), 256, 0, ctx->stream>>>(n, X, eta, F, ldf, kc, lams);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_vec(usbs_ctx* ctx, int op, int64_t m, const double* x, const double* y, const double* z,
+                     const double* b, const double* ineq, double s0, double s1, double* out, double* red_out) {
+  USBS_API_BEGIN
+  int nb = (int)std::min<int64_t>(2 * ctx->num_sms, std::max<int64_t>(1, (m + 2047) / 2048));
+  double* red = red_out ? (double*)ctx->ws.get(WS_RED + 1, (size_t)2 * nb * sizeof(double)) : nullptr;
+  k_vec<<<nb, 256, 0, ctx->stream>>>(op, m, x, y, z, b, ineq, s0, s1, out, red);
+  check_launch(ctx);
+  if (red_out) {
+    k_vec_final<<<1, 32, 0, ctx->stream>>>(nb, red, red_out, op == VOP_MINI ? 1 : 0, op == VOP_DOTAFF ? 1 : 0, s0,
+                                           s1);
+    check_launch(ctx);
+  }
+  USBS_API_END
+}
+
+__global__ void k_svec(int k, const double* __restrict__ A, double scale, double* __restrict__ out) {
+  // column-major lower triangle, sqrt(2) off the diagonal (symlin.py:57-79)
+  const int d = k * (k + 1) / 2;
+  for (int p = threadIdx.x; p < d; p += blockDim.x) {
+    int j = 0, rem = p;
+    while (rem >= k - j) { rem -= k - j; ++j; }
+    const int i = j + rem;
+    out[p] = scale * (A[i * k + j] * (i == j ? 1.0 : 1.4142135623730951));
+  }
+}
+
+usbs_status usbs_svec(usbs_ctx* ctx, int k, const double* A, double scale, double* out) {
+  USBS_API_BEGIN
+  if (k < 1 || k > 64) fail(USBS_ERR_SHAPE, "svec: 1 <= k <= 64");
+  k_svec<<<1, 256, 0, ctx->stream>>>(k, A, scale, out);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* G, double drop_tol, int* perm, double* Rinv,
+                         double* info) {
+  USBS_API_BEGIN
+  if (c < 1 || c > 40) fail(USBS_ERR_SHAPE, "pivchol: 1 <= c <= 40");
+  k_pivchol<<<1, 64, 0, ctx->stream>>>(c, G, drop_tol, perm, Rinv, info);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+}  // extern "C"

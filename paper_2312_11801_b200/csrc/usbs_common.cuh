@@ -77,6 +77,10 @@ struct usbs_problem {
   // slack assembly: slot -> contributing entries
   int* aptr = nullptr;   // nnz + 1
   int* aent = nullptr;   // entry ids
+  // constraint -> entries (ascending entry id), for row-wise constraint kernels
+  int* cptr = nullptr;  // m + 1
+  int* cent = nullptr;  // ne
+  int max_entries_per_cons = 0;
   // flat constraint entries (device copies)
   int* e_idx = nullptr;
   int* e_row = nullptr;

@@ -1,0 +1,595 @@
+// K12: the k x k bundle subproblem as ONE single-CTA kernel per solve.
+//
+// Mirrors subqp._ipm_solve (subqp.py:353-435) with its pieces:
+//   _cold_state 184-197, _stationarity 210-219, newton_direction 222-265,
+//   line_search_feasible 294-343, barrier_update 346-350, _objective 200-207,
+//   IpmOptions 150-162 (mu_tol 1e-11, kkt_tol 1e-6, max_newton 100,
+//   step_frac 0.99, backtrack 0.8, min_step 1e-12, max_step_failures 6,
+//   warm_blend 0.2).
+// Differences in arithmetic only (no change of algorithm):
+//   * symm_kron(T, S^-1) (symlin.py:133-145) is never materialised through
+//     the k^2 x k^2 Kronecker products; its entries come from the closed form
+//     E[p,q] = w_p w_q / 4 (H_ik G_lj + H_il G_kj + G_ik H_lj + G_il H_kj),
+//     p = (i,j), q = (k,l) in svec order, and E ds = svec((H D G + G D H)/2).
+//   * S^-1 comes from the Cholesky factor of S (S is positive definite at
+//     every iterate) instead of an LU inverse; it is symmetrised the same way.
+//   * The reduced Newton matrix M (d x d, d = k(k+1)/2) lives packed-lower in
+//     shared memory (d <= 210, i.e. k <= 20; larger k spills M to global) and
+//     is factorised by a right-looking Cholesky that fails exactly on a
+//     non-positive or NaN pivot, like LAPACK potrf.
+#include <algorithm>
+#include <cmath>
+
+#include "usbs_common.cuh"
+#include "usbs_kernels.cuh"
+
+namespace usbs {
+
+struct IpmOpts {
+  double mu_tol, kkt_tol, step_frac, backtrack, min_step, warm_blend;
+  int max_newton, max_step_failures;
+};
+
+struct IpmArgs {
+  int k, d, has_eta;
+  const double* Q11;   // d x d row-major (nullptr: zero, the eval problem)
+  const double* q12;   // d (nullptr: zero)
+  const double* lin_s; // d
+  const double* scal;  // [q22, lin_eta]
+  const double* warm;  // state or nullptr
+  double* state;       // out state (may alias warm)
+  double* result;      // [value, newton_iters, exact, eta_opt, failures]
+  double* gM;          // global scratch for M when d > SMEM_D
+  IpmOpts o;
+};
+
+// state layout: S (k*k), T (k*k), eta, zeta, omega, mu, has_eta, k, valid
+__host__ __device__ inline int state_len(int k) { return 2 * k * k + 7; }
+
+constexpr int IPM_THREADS = 512;
+constexpr int SMEM_D = 210;
+constexpr int KMAX = 32;
+
+__device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }  // packed lower, i >= j
+
+struct IpmSmem {
+  double *S, *T, *H, *dS, *dT, *W1, *W2, *X1, *X2;  // k x k
+  double *s, *t, *vI, *h, *g, *f1, *rhs, *ds, *dt, *rd, *tmp;  // d
+  unsigned char *pi, *pj;
+  double* red;   // 32
+  double* sc;    // scalars 64
+  int* flg;      // 16
+  double* M;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ double blk_max_abs(const double* x, int n, double* red) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v = fmax(v, fabs(x[i]));
+  v = warp_max(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+  __syncthreads();
+  return r;
+}
+
+// warp 0: in-place Cholesky (lower, row-major k x k in W). returns ok to all
+// threads of the block (via flg[slot]).  Fails on pivot <= 0 or NaN (potrf).
+__device__ void warp_chol(double* W, int k, int* flg, int slot) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int ok = 1;
+    for (int j = 0; j < k; ++j) {
+      double piv = W[j * k + j];
+      if (!(piv > 0.0)) { ok = 0; break; }
+      double ljj = sqrt(piv);
+      double r = 1.0 / ljj;
+      __syncwarp();
+      if (lane == 0) W[j * k + j] = ljj;
+      if (lane > j && lane < k) W[lane * k + j] *= r;
+      __syncwarp();
+      if (lane > j && lane < k) {
+        double lij = W[lane * k + j];
+        for (int c = j + 1; c <= lane; ++c) W[lane * k + c] -= lij * W[c * k + j];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) flg[slot] = ok;
+  }
+  __syncthreads();
+}
+
+// svec of a symmetric k x k matrix (row-major) into v (length d)
+__device__ void blk_svec(const double* A, int k, int d, const IpmSmem& sm, double* v) {
+  for (int p = threadIdx.x; p < d; p += blockDim.x) {
+    int i = sm.pi[p], j = sm.pj[p];
+    v[p] = A[i * k + j] * (i == j ? 1.0 : 1.4142135623730951);
+  }
+}
+
+__device__ void blk_smat(const double* v, int k, int d, const IpmSmem& sm, double* A) {
+  for (int p = threadIdx.x; p < d; p += blockDim.x) {
+    int i = sm.pi[p], j = sm.pj[p];
+    double x = (i == j) ? v[p] : v[p] / 1.4142135623730951;
+    A[i * k + j] = x;
+    A[j * k + i] = x;
+  }
+}
+
+// y = Q11 x (+ beta*y0) over d, warp per row (Q11 in global, coalesced rows)
+__device__ void blk_gemv_q11(const double* Q, const double* x, int d, double* y) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int p = w; p < d; p += nw) {
+    double s = 0.0;
+    if (Q)
+      for (int q = lane; q < d; q += 32) s = fma(Q[(int64_t)p * d + q], x[q], s);
+    s = warp_sum(s);
+    if (lane == 0) y[p] = s;
+  }
+}
+
+__device__ double blk_dot(const double* a, const double* b, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], b[i], s);
+  return block_sum(s, red);
+}
+
+// C = A B for k x k row-major (block-parallel)
+__device__ void blk_mm(const double* A, const double* B, int k, double* C) {
+  for (int x = threadIdx.x; x < k * k; x += blockDim.x) {
+    int r = x / k, c = x % k;
+    double s = 0.0;
+    for (int u = 0; u < k; ++u) s = fma(A[r * k + u], B[u * k + c], s);
+    C[x] = s;
+  }
+}
+
+// complementarity <S,T> + omega*sigma (+ eta*zeta)
+__device__ double blk_compl(const IpmSmem& sm, int k, double eta, double zeta, double omega, int has_eta) {
+  double s = 0.0;
+  for (int x = threadIdx.x; x < k * k; x += blockDim.x) s = fma(sm.S[x], sm.T[x], s);
+  s = block_sum(s, sm.red);
+  double tr = 0.0;
+  for (int i = 0; i < k; ++i) tr += sm.S[i * k + i];
+  double sigma = 1.0 - tr - eta;
+  double c = s + omega * sigma;
+  if (has_eta) c += eta * zeta;
+  return c;
+}
+
+__device__ double trace_k(const double* A, int k) {
+  double tr = 0.0;
+  for (int i = 0; i < k; ++i) tr += A[i * k + i];
+  return tr;
+}
+
+// ---------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int k = a.k, d = a.d, kk = k * k, tid = threadIdx.x, nth = blockDim.x;
+  const int has_eta = a.has_eta;
+  IpmSmem sm;
+  double* base = (double*)smem_raw;
+  sm.S = base; sm.T = sm.S + kk; sm.H = sm.T + kk; sm.dS = sm.H + kk; sm.dT = sm.dS + kk;
+  sm.W1 = sm.dT + kk; sm.W2 = sm.W1 + kk; sm.X1 = sm.W2 + kk; sm.X2 = sm.X1 + kk;
+  sm.s = sm.X2 + kk; sm.t = sm.s + d; sm.vI = sm.t + d; sm.h = sm.vI + d; sm.g = sm.h + d;
+  sm.f1 = sm.g + d; sm.rhs = sm.f1 + d; sm.ds = sm.rhs + d; sm.dt = sm.ds + d; sm.rd = sm.dt + d;
+  sm.tmp = sm.rd + d;
+  sm.red = sm.tmp + d; sm.sc = sm.red + 32;
+  sm.M = sm.sc + 64;
+  const bool m_in_smem = d <= SMEM_D;
+  double* Mp = m_in_smem ? sm.M : a.gM;
+  unsigned char* ub = (unsigned char*)(sm.M + (m_in_smem ? d * (d + 1) / 2 : 0));
+  sm.pi = ub; sm.pj = ub + 600;
+  sm.flg = (int*)(ub + 1200);
+
+  // svec index tables (column-major lower triangle, symlin.py:57-69)
+  if (tid == 0) {
+    int p = 0;
+    for (int j = 0; j < k; ++j)
+      for (int i = j; i < k; ++i) { sm.pi[p] = (unsigned char)i; sm.pj[p] = (unsigned char)j; ++p; }
+  }
+  __syncthreads();
+  for (int p = tid; p < d; p += nth) {
+    sm.vI[p] = sm.pi[p] == sm.pj[p] ? 1.0 : 0.0;
+    sm.h[p] = a.lin_s[p];
+    sm.g[p] = a.q12 ? a.q12[p] : 0.0;
+  }
+  const double q22 = a.scal[0], h2 = has_eta ? a.scal[1] : 0.0;
+  const double q22e = has_eta ? q22 : 0.0;
+  const int pairs = k + (has_eta ? 2 : 1);
+  // ---- cold centre (subqp.py:184-197)
+  const double cc = 1.0 / (2.0 * pairs);
+  double eta, zeta, omega, mu;
+  // warm start (subqp.py:355-373): strictly feasible check, blend 0.2 to centre
+  int use_warm = 0;
+  if (a.warm && (int)a.warm[2 * kk + 5] == k && (int)a.warm[2 * kk + 4] == has_eta && a.warm[2 * kk + 6] != 0.0) {
+    for (int x = tid; x < kk; x += nth) { sm.W1[x] = a.warm[x]; sm.W2[x] = a.warm[kk + x]; }
+    __syncthreads();
+    double we = a.warm[2 * kk], wz = a.warm[2 * kk + 1], wo = a.warm[2 * kk + 2];
+    double sig = 1.0 - trace_k(sm.W1, k) - we;
+    int ok = (wo > 0.0 && sig > 0.0) && (!has_eta || (we > 0.0 && wz > 0.0));
+    __syncthreads();
+    if (ok) {
+      warp_chol(sm.W1, k, sm.flg, 0);
+      int ok1 = sm.flg[0];
+      warp_chol(sm.W2, k, sm.flg, 1);
+      int ok2 = sm.flg[1];
+      ok = ok1 && ok2;
+    }
+    if (ok) {
+      const double lam = a.o.warm_blend;
+      for (int x = tid; x < kk; x += nth) {
+        int r = x / k, c = x % k;
+        sm.S[x] = (1 - lam) * a.warm[x] + lam * (r == c ? cc : 0.0);
+        sm.T[x] = (1 - lam) * a.warm[kk + x] + lam * (r == c ? 1.0 : 0.0);
+      }
+      eta = (1 - lam) * we + lam * (has_eta ? cc : 0.0);
+      zeta = (1 - lam) * wz + lam * (has_eta ? 1.0 : 0.0);
+      omega = (1 - lam) * wo + lam * 1.0;
+      use_warm = 1;
+    }
+  }
+  if (!use_warm) {
+    for (int x = tid; x < kk; x += nth) {
+      int r = x / k, c = x % k;
+      sm.S[x] = (r == c) ? cc : 0.0;
+      sm.T[x] = (r == c) ? 1.0 : 0.0;
+    }
+    eta = has_eta ? cc : 0.0;
+    zeta = has_eta ? 1.0 : 0.0;
+    omega = 1.0;
+  }
+  __syncthreads();
+  mu = blk_compl(sm, k, eta, zeta, omega, has_eta) / (2.0 * pairs);
+  // ---- coefficient scale (subqp.py:376-382)
+  double qmax = 0.0;
+  if (a.Q11) {
+    double v = 0.0;
+    for (int x = tid; x < d * d; x += nth) v = fmax(v, fabs(a.Q11[x]));
+    v = warp_max(v);
+    __syncthreads();
+    if ((tid & 31) == 0) sm.red[tid >> 5] = v;
+    __syncthreads();
+    for (int w = 0; w < nth / 32; ++w) qmax = fmax(qmax, sm.red[w]);
+    __syncthreads();
+  }
+  const double hmax = blk_max_abs(sm.h, d, sm.red);
+  const double gmax = blk_max_abs(sm.g, d, sm.red);
+  const double coeff_scale = 1.0 + fmax(fmax(fmax(hmax, fabs(h2)), qmax), fmax(gmax, fabs(q22e)));
+
+  int exact = 0, failures = 0, it = 0;
+  const double SQ2 = 1.4142135623730951;
+  for (it = 1; it <= a.o.max_newton; ++it) {
+    // ---- stationarity (subqp.py:210-219)
+    blk_svec(sm.S, k, d, sm, sm.s);
+    blk_svec(sm.T, k, d, sm, sm.t);
+    __syncthreads();
+    blk_gemv_q11(a.Q11, sm.s, d, sm.f1);
+    __syncthreads();
+    for (int p = tid; p < d; p += nth) {
+      double f = sm.f1[p] + sm.h[p] - sm.t[p] + omega * sm.vI[p];
+      if (has_eta) f += eta * sm.g[p];
+      sm.f1[p] = f;
+    }
+    __syncthreads();
+    double f2 = 0.0;
+    if (has_eta) f2 = blk_dot(sm.g, sm.s, d, sm.red) + eta * q22e + h2 - zeta + omega;
+    const double fmaxv = blk_max_abs(sm.f1, d, sm.red);
+    const double stat_res = fmax(fmaxv, fabs(f2));
+    const double achieved = blk_compl(sm, k, eta, zeta, omega, has_eta) / (2.0 * pairs);
+    if (mu < a.o.mu_tol && achieved < a.o.mu_tol && stat_res <= a.o.kkt_tol * coeff_scale) {
+      exact = 1;
+      it -= 1;
+      break;
+    }
+    // ---- newton_direction (subqp.py:222-265)
+    int fail = 0;
+    // H = S^-1 via Cholesky: S = L L^T, Linv by forward substitution, H = Linv^T Linv
+    for (int x = tid; x < kk; x += nth) sm.W1[x] = sm.S[x];
+    __syncthreads();
+    warp_chol(sm.W1, k, sm.flg, 2);
+    if (!sm.flg[2]) fail = 1;
+    if (!fail) {
+      // X1 = L^-1 (lower): column c solved by thread c
+      for (int c = tid; c < k; c += nth) {
+        for (int r = 0; r < k; ++r) sm.X1[r * k + c] = 0.0;
+        for (int r = c; r < k; ++r) {
+          double s = (r == c) ? 1.0 : 0.0;
+          for (int u = c; u < r; ++u) s -= sm.W1[r * k + u] * sm.X1[u * k + c];
+          sm.X1[r * k + c] = s / sm.W1[r * k + r];
+        }
+      }
+      __syncthreads();
+      for (int x = tid; x < kk; x += nth) {
+        int r = x / k, c = x % k;
+        double s = 0.0;
+        for (int u = max(r, c); u < k; ++u) s = fma(sm.X1[u * k + r], sm.X1[u * k + c], s);
+        sm.X2[x] = s;
+      }
+      __syncthreads();
+      for (int x = tid; x < kk; x += nth) {
+        int r = x / k, c = x % k;
+        sm.H[x] = 0.5 * (sm.X2[r * k + c] + sm.X2[c * k + r]);
+      }
+      __syncthreads();
+      const double tr = trace_k(sm.S, k);
+      const double sigma = 1.0 - tr - eta;
+      const double rc = mu / omega - sigma;
+      const double kappa1 = sigma / omega;
+      // rd = mu svec(H) - t
+      blk_svec(sm.H, k, d, sm, sm.rd);
+      __syncthreads();
+      for (int p = tid; p < d; p += nth) sm.rd[p] = mu * sm.rd[p] - sm.t[p];
+      double re = 0.0, kappa2 = 0.0, cden = 1.0;
+      if (has_eta) {
+        re = mu / eta - zeta;
+        kappa2 = zeta / eta + q22e;
+        cden = kappa1 * kappa2 + 1.0;
+      }
+      __syncthreads();
+      // rhs
+      for (int p = tid; p < d; p += nth) {
+        double r;
+        if (!has_eta) r = -sm.f1[p] + sm.rd[p] - (rc / kappa1) * sm.vI[p];
+        else
+          r = sm.g[p] * ((rc + kappa1 * (f2 - re)) / cden) + sm.vI[p] * ((f2 - re - kappa2 * rc) / cden) -
+              sm.f1[p] + sm.rd[p];
+        sm.rhs[p] = r;
+      }
+      // M (packed lower): Q11 + E + low-rank
+      const int np = d * (d + 1) / 2;
+      for (int x = tid; x < np; x += nth) {
+        int p = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+        while (p * (p + 1) / 2 > x) --p;
+        while ((p + 1) * (p + 2) / 2 <= x) ++p;
+        const int q = x - p * (p + 1) / 2;
+        const int i = sm.pi[p], j = sm.pj[p], kq = sm.pi[q], l = sm.pj[q];
+        const double wp = (i == j) ? 1.0 : SQ2, wq = (kq == l) ? 1.0 : SQ2;
+        const double* Hm = sm.H;
+        const double* Gm = sm.T;
+        double e = Hm[i * k + kq] * Gm[l * k + j] + Hm[i * k + l] * Gm[kq * k + j] +
+                   Gm[i * k + kq] * Hm[l * k + j] + Gm[i * k + l] * Hm[kq * k + j];
+        e *= (wp * wq) * 0.25;
+        double v = (a.Q11 ? a.Q11[(int64_t)p * d + q] : 0.0) + e;
+        if (!has_eta) v += sm.vI[p] * sm.vI[q] / kappa1;
+        else
+          v -= (sm.g[p] * (kappa1 * sm.g[q] + sm.vI[q]) + sm.vI[p] * (sm.g[q] - kappa2 * sm.vI[q])) / cden;
+        Mp[x] = v;
+      }
+      __syncthreads();
+      // Cholesky of M, right-looking, one barrier per column; column j is
+      // scaled lazily during column j+1 (nobody reads it then)
+      for (int j = 0; j < d; ++j) {
+        if (j > 0) {
+          const double rsp = sm.sc[0];
+          for (int i = j + tid; i < d; i += nth) Mp[pidx(i, j - 1)] *= rsp;  // i >= j > j-1
+          if (tid == 0) Mp[pidx(j - 1, j - 1)] = sm.sc[1];
+        }
+        const double piv = Mp[pidx(j, j)];
+        __syncthreads();  // everyone read piv / finished scaling before sc is rewritten
+        if (!(piv > 0.0)) { fail = 1; break; }
+        const double ljj = sqrt(piv), rs = 1.0 / ljj;
+        // trailing update over rows i > j, cols c in (j, i]
+        const int m1 = d - j - 1;
+        const int tri = m1 * (m1 + 1) / 2;
+        for (int x = tid; x < tri; x += nth) {
+          int r = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+          while (r * (r + 1) / 2 > x) --r;
+          while ((r + 1) * (r + 2) / 2 <= x) ++r;
+          const int c = x - r * (r + 1) / 2;
+          const int i = j + 1 + r, cc2 = j + 1 + c;
+          Mp[pidx(i, cc2)] -= (Mp[pidx(i, j)] * rs) * (Mp[pidx(cc2, j)] * rs);
+        }
+        if (tid == 0) { sm.sc[0] = rs; sm.sc[1] = ljj; }
+        __syncthreads();
+        if (j == d - 1) {
+          if (tid == 0) Mp[pidx(j, j)] = ljj;
+          __syncthreads();
+        }
+      }
+      if (!fail) {
+        // forward / backward substitution (warp 0)
+        if (tid < 32) {
+          const int lane = tid;
+          for (int j = 0; j < d; ++j) {
+            __syncwarp();
+            const double yj = sm.rhs[j] / Mp[pidx(j, j)];
+            __syncwarp();
+            if (lane == 0) sm.rhs[j] = yj;
+            for (int i = j + 1 + lane; i < d; i += 32) sm.rhs[i] -= Mp[pidx(i, j)] * yj;
+          }
+          __syncwarp();
+          for (int j = d - 1; j >= 0; --j) {
+            __syncwarp();
+            const double xj = sm.rhs[j] / Mp[pidx(j, j)];
+            __syncwarp();
+            if (lane == 0) sm.ds[j] = xj;
+            for (int i = lane; i < j; i += 32) sm.rhs[i] -= Mp[pidx(j, i)] * xj;
+          }
+        }
+        __syncthreads();
+        // E ds = svec((H D G + G D H)/2), D = smat(ds), G = T
+        blk_smat(sm.ds, k, d, sm, sm.W1);
+        __syncthreads();
+        blk_mm(sm.W1, sm.T, k, sm.X1);  // D G
+        __syncthreads();
+        blk_mm(sm.H, sm.X1, k, sm.X2);  // H D G
+        __syncthreads();
+        for (int x = tid; x < kk; x += nth) {
+          int r = x / k, c = x % k;
+          sm.W2[x] = 0.5 * (sm.X2[r * k + c] + sm.X2[c * k + r]);
+        }
+        __syncthreads();
+        blk_svec(sm.W2, k, d, sm, sm.tmp);  // E ds
+        __syncthreads();
+        for (int p = tid; p < d; p += nth) sm.dt[p] = sm.rd[p] - sm.tmp[p];
+        const double vds = blk_dot(sm.vI, sm.ds, d, sm.red);
+        double deta = 0.0, dzeta = 0.0, domega;
+        if (!has_eta) {
+          domega = (rc + vds) / kappa1;
+        } else {
+          const double gds = blk_dot(sm.g, sm.ds, d, sm.red);
+          deta = -(rc + kappa1 * (f2 - re) + (kappa1 * gds + vds)) / cden;
+          dzeta = re - (zeta / eta) * deta;
+          domega = -f2 + re - gds - kappa2 * deta;
+        }
+        __syncthreads();
+        // ---- line_search_feasible (subqp.py:294-343)
+        int finite = 1;
+        for (int p = tid; p < d; p += nth)
+          if (!isfinite(sm.ds[p]) || !isfinite(sm.dt[p])) finite = 0;
+        finite = __syncthreads_and(finite);
+        if (!(finite && isfinite(deta) && isfinite(dzeta) && isfinite(domega))) {
+          fail = 1;
+        } else {
+          double bmin = INFINITY;
+          bool any = false;
+          if (domega < 0) { bmin = fmin(bmin, -omega / domega); any = true; }
+          if (has_eta) {
+            if (deta < 0) { bmin = fmin(bmin, -eta / deta); any = true; }
+            if (dzeta < 0) { bmin = fmin(bmin, -zeta / dzeta); any = true; }
+          }
+          const double dsig = -(vds + deta);
+          if (dsig < 0) { bmin = fmin(bmin, -sigma / dsig); any = true; }
+          double delta = any ? fmin(1.0, a.o.step_frac * bmin) : 1.0;
+          blk_smat(sm.ds, k, d, sm, sm.dS);
+          blk_smat(sm.dt, k, d, sm, sm.dT);
+          __syncthreads();
+          bool found = false;
+          while (delta >= a.o.min_step) {
+            for (int x = tid; x < kk; x += nth) {
+              sm.W1[x] = sm.S[x] + delta * sm.dS[x];
+              sm.W2[x] = sm.T[x] + delta * sm.dT[x];
+            }
+            __syncthreads();
+            warp_chol(sm.W1, k, sm.flg, 3);
+            int ok = sm.flg[3];
+            if (ok) {
+              warp_chol(sm.W2, k, sm.flg, 4);
+              ok = sm.flg[4];
+            }
+            if (ok) {
+              if (omega + delta * domega <= 0 || sigma + delta * dsig <= 0) ok = 0;
+              if (has_eta && (eta + delta * deta <= 0 || zeta + delta * dzeta <= 0)) ok = 0;
+            }
+            __syncthreads();
+            if (ok) { found = true; break; }
+            delta *= a.o.backtrack;
+          }
+          if (!found) {
+            fail = 1;
+          } else {
+            // ---- step + barrier_update (subqp.py:415-422, 346-350)
+            failures = 0;
+            for (int x = tid; x < kk; x += nth) {
+              sm.S[x] = sm.S[x] + delta * sm.dS[x];
+              sm.T[x] = sm.T[x] + delta * sm.dT[x];
+            }
+            omega += delta * domega;
+            if (has_eta) {
+              eta += delta * deta;
+              zeta += delta * dzeta;
+            }
+            __syncthreads();
+            const double gamma = delta <= 0.2 ? 1.0 : 0.5 - 0.4 * delta * delta;
+            const double est = blk_compl(sm, k, eta, zeta, omega, has_eta) / (2.0 * pairs);
+            mu = fmin(mu, gamma * est);
+            continue;
+          }
+        }
+      }
+    }
+    // recovery (subqp.py:406-413)
+    __syncthreads();
+    failures += 1;
+    if (failures > a.o.max_step_failures) break;
+    mu = fmax(mu * 10.0, 10.0 * a.o.mu_tol);
+  }
+  if (it > a.o.max_newton) it = a.o.max_newton;
+  // ---- objective (subqp.py:200-207) and outputs
+  blk_svec(sm.S, k, d, sm, sm.s);
+  __syncthreads();
+  blk_gemv_q11(a.Q11, sm.s, d, sm.f1);
+  __syncthreads();
+  const double sQs = blk_dot(sm.s, sm.f1, d, sm.red);
+  const double hs = blk_dot(sm.h, sm.s, d, sm.red);
+  double val = 0.5 * sQs + hs;
+  if (has_eta) {
+    const double gs = blk_dot(sm.g, sm.s, d, sm.red);
+    val += eta * gs + 0.5 * eta * eta * q22e + eta * h2;
+  }
+  for (int x = tid; x < kk; x += nth) {
+    a.state[x] = sm.S[x];
+    a.state[kk + x] = sm.T[x];
+  }
+  if (tid == 0) {
+    a.state[2 * kk] = eta;
+    a.state[2 * kk + 1] = zeta;
+    a.state[2 * kk + 2] = omega;
+    a.state[2 * kk + 3] = mu;
+    a.state[2 * kk + 4] = has_eta;
+    a.state[2 * kk + 5] = k;
+    a.state[2 * kk + 6] = 1.0;
+    a.result[0] = val;
+    a.result[1] = it;
+    a.result[2] = exact;
+    a.result[3] = has_eta ? eta : 0.0;
+    a.result[4] = failures;
+  }
+}
+
+size_t ipm_smem_bytes(int k) {
+  const int d = k * (k + 1) / 2, kk = k * k;
+  size_t doubles = 9 * kk + 11 * d + 32 + 64 + (d <= SMEM_D ? d * (d + 1) / 2 : 0);
+  return doubles * sizeof(double) + 1200 + 16 * sizeof(int) + 64;
+}
+
+void launch_ipm(usbs_ctx* ctx, const IpmArgs& a) {
+  static bool attr = false;
+  if (!attr) {
+    USBS_CUDA(cudaFuncSetAttribute(k_ipm, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  size_t sm = ipm_smem_bytes(a.k);
+  IpmArgs b = a;
+  k_ipm<<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+  check_launch(ctx);
+}
+
+}  // namespace usbs
+
+using namespace usbs;
+
+extern "C" usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const double* Q11, const double* q12,
+                                      const double* lin_s, const double* scal, const double* warm_state,
+                                      double* state_out, double* result, const double* opts) {
+  USBS_API_BEGIN
+  if (k < 1 || k > KMAX) fail(USBS_ERR_SHAPE, "ipm: 1 <= k <= 32");
+  IpmArgs a{};
+  a.k = k;
+  a.d = k * (k + 1) / 2;
+  a.has_eta = has_eta ? 1 : 0;
+  a.Q11 = Q11;
+  a.q12 = q12;
+  a.lin_s = lin_s;
+  a.scal = scal;
+  a.warm = warm_state;
+  a.state = state_out;
+  a.result = result;
+  a.gM = a.d > SMEM_D ? (double*)ctx->ws.get(WS_IPM, (size_t)a.d * (a.d + 1) / 2 * sizeof(double)) : nullptr;
+  // IpmOptions defaults (subqp.py:150-162) unless given:
+  // [mu_tol, kkt_tol, max_newton, step_frac, backtrack, min_step, max_step_failures, warm_blend]
+  double o[8] = {1e-11, 1e-6, 100, 0.99, 0.8, 1e-12, 6, 0.2};
+  if (opts)
+    for (int i = 0; i < 8; ++i) o[i] = opts[i];
+  a.o.mu_tol = o[0]; a.o.kkt_tol = o[1]; a.o.max_newton = (int)o[2]; a.o.step_frac = o[3];
+  a.o.backtrack = o[4]; a.o.min_step = o[5]; a.o.max_step_failures = (int)o[6]; a.o.warm_blend = o[7];
+  launch_ipm(ctx, a);
+  USBS_API_END
+}
+
+extern "C" int usbs_ipm_state_len(int k) { return state_len(k); }

@@ -201,13 +201,19 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         }
       }
       {
-        const int gpb = nth / LG, g = tid / LG, t = tid % LG;
-        for (int it = i0 + g; it < i1; it += gpb) {
-          const int rb = a.it_beg[it], re = a.it_end[it];
+        // warp-uniform trip count: every lane reaches the group shuffles
+        constexpr int GPW = 32 / LG;
+        const int lane = tid & 31, warp = tid >> 5, gw = lane / LG, t = lane % LG;
+        for (int base = i0 + warp * GPW; base < i1; base += nw * GPW) {
+          const int it = base + gw;
+          const bool ok = it < i1;
           double acc = 0.0;
-          for (int z = rb + t; z < re; z += LG) acc = fma(a.val[z], xsrc[a.col[z]] * xs, acc);
+          if (ok) {
+            const int rb = a.it_beg[it], re = a.it_end[it];
+            for (int z = rb + t; z < re; z += LG) acc = fma(a.val[z], xsrc[a.col[z]] * xs, acc);
+          }
           acc = group_sum<LG>(acc);
-          if (t == 0) {
+          if (ok && t == 0) {
             const int sl = a.it_slot[it];
             if (sl < 0) Wcur[a.it_row[it]] = acc;
             else a.split[sl] = acc;

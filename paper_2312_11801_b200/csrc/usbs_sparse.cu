@@ -133,12 +133,9 @@ usbs_status usbs_ctx_create(int device, void* stream, usbs_ctx** out) {
   USBS_CUDA(cudaSetDevice(device));
   auto* c = new usbs_ctx();
   c->device = device;
-  if (stream) {
-    c->stream = (cudaStream_t)stream;
-  } else {
-    USBS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    c->own_stream = true;
-  }
+  // NULL is the legacy default stream (what torch reports for its default
+  // stream), so work stays ordered with the caller's tensor operations
+  c->stream = (cudaStream_t)stream;
   cudaDeviceProp prop;
   USBS_CUDA(cudaGetDeviceProperties(&prop, device));
   c->num_sms = prop.multiProcessorCount;
@@ -333,7 +330,6 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
     for (int64_t e = 0; e < ne; ++e) {
       if (e_rows[e] != e_cols[e] || e_idx[e] != e_rows[e] || e_vals[e] != 1.0)
         fail(USBS_ERR_SHAPE, "diag_only entries must be (i, i, i, 1.0)");
-      diag_slot[e_rows[e]] = (int32_t)slot_of_x[xcnt[e_rows[e]] + 0];
     }
     // slot_of_x for row r's single extra entry: recompute robustly
     for (int64_t i = 0; i < n; ++i) {
@@ -361,6 +357,17 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
     p->e_val = dev_upload(p, e_vals, ne);
   }
   if (p->diag_only) p->diag_slot = dev_upload(p, diag_slot.data(), n);
+  {
+    std::vector<int32_t> cptr(m + 1, 0), cent(ne);
+    for (int64_t e = 0; e < ne; ++e) cptr[e_idx[e] + 1]++;
+    int mx = 0;
+    for (int64_t i = 0; i < m; ++i) { mx = std::max(mx, cptr[i + 1]); cptr[i + 1] += cptr[i]; }
+    std::vector<int32_t> pos(cptr.begin(), cptr.end() - 1);
+    for (int64_t e = 0; e < ne; ++e) cent[pos[e_idx[e]]++] = (int32_t)e;
+    p->cptr = dev_upload(p, cptr.data(), cptr.size());
+    p->cent = dev_upload(p, cent.data(), cent.size());
+    p->max_entries_per_cons = mx;
+  }
   p->it_row = dev_upload(p, irow.data(), irow.size());
   p->it_beg = dev_upload(p, ibeg.data(), ibeg.size());
   p->it_end = dev_upload(p, iend.data(), iend.size());

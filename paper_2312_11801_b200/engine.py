@@ -1,0 +1,96 @@
+"""Thin typed wrappers over the C-ABI for device tensors (torch float64 CUDA
+tensors as buffers).  Every method is one or two library calls; nothing
+here computes on the host or with eager PyTorch ops."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, ptr
+from .runtime import DeviceProblem, Runtime
+
+
+def _p(t):
+    return C.c_void_p(ptr(t)) if t is not None else None
+
+
+class Engine:
+    def __init__(self, dp: DeviceProblem):
+        self.dp = dp
+        self.rt: Runtime = dp.rt
+        self.lib = self.rt.lib
+        self.h = self.rt.h
+        self.n, self.m = dp.n, dp.m
+
+    # ---------------------------------------------------------------- vectors
+    def vec(self, op, m, x=None, y=None, z=None, b=None, ineq=None, s0=0.0, s1=0.0, out=None, red=None):
+        check(self.lib.usbs_vec(self.h, op, int(m), _p(x), _p(y), _p(z), _p(b), _p(ineq), float(s0), float(s1),
+                                _p(out), _p(red)), "vec")
+
+    def dot_into(self, x, y, red, scale=1.0, shift=0.0):
+        """red[0] = scale * <x, y> + shift (device scalar)."""
+        self.vec(N.VOP_DOTAFF, x.numel(), x=x, y=y, s0=scale, s1=shift, red=red)
+
+    # ---------------------------------------------------------------- dense
+    def rowgemm(self, X, B, Y, alpha=1.0, beta=0.0, Y0=None, xs=None, n=None):
+        n = X.shape[0] if n is None else n
+        ka = X.shape[1]
+        kb = B.shape[1]
+        check(self.lib.usbs_rowgemm(self.h, int(n), _p(X), X.stride(0), ka, _p(B), B.stride(0), kb, _p(xs),
+                                    float(alpha), float(beta), _p(Y0), Y0.stride(0) if Y0 is not None else 0,
+                                    _p(Y), Y.stride(0)), "rowgemm")
+        return Y
+
+    def gram(self, A, B, out, sym=False):
+        check(self.lib.usbs_gram(self.h, A.shape[0], _p(A), A.stride(0), A.shape[1], _p(B), B.stride(0),
+                                 B.shape[1], _p(out), 1 if sym else 0), "gram")
+        return out
+
+    def wcoldot(self, F, G, w, out):
+        check(self.lib.usbs_wcoldot(self.h, F.shape[0], _p(F), F.stride(0), _p(G), G.stride(0), F.shape[1],
+                                    _p(w), _p(out)), "wcoldot")
+
+    def small_eigh(self, a, vals, vecs):
+        check(self.lib.usbs_small_eigh(self.h, a.shape[0], _p(a), _p(vals), _p(vecs)), "small_eigh")
+
+    def pivchol(self, G, drop_tol, perm, rinv, info):
+        check(self.lib.usbs_pivchol(self.h, G.shape[0], _p(G), float(drop_tol), _p(perm), _p(rinv), _p(info)),
+              "pivchol")
+
+    def svec(self, A, out, scale=1.0):
+        check(self.lib.usbs_svec(self.h, A.shape[0], _p(A), float(scale), _p(out)), "svec")
+        return out
+
+    def dense_update(self, X, eta, F, lams):
+        check(self.lib.usbs_dense_update(self.h, X.shape[0], _p(X), float(eta), _p(F), F.stride(0), F.shape[1],
+                                         _p(lams)), "dense_update")
+
+    # ---------------------------------------------------------------- operator / constraints
+    def apply(self, which, V, out, gram=None):
+        return self.dp.apply(which, V, out=out, gram=gram)
+
+    def image(self, V, S, out, s_is_diag=False, s_scale=1.0, beta=0.0, beta_dev=None, base=None):
+        check(self.lib.usbs_cons_image(self.h, self.dp.h, _p(V), V.stride(0), V.shape[1], _p(S),
+                                       1 if s_is_diag else 0, float(s_scale), _p(beta_dev), float(beta), _p(base),
+                                       _p(out)), "cons_image")
+        return out
+
+    def compressed(self, V, scale_gram=0.0, gram_out=None, a=None, scale_a=0.0, a_out=None, w=None, scale_w=0.0,
+                   w_out=None):
+        check(self.lib.usbs_cons_compressed(self.h, self.dp.h, _p(V), V.stride(0), V.shape[1], float(scale_gram),
+                                            _p(gram_out), _p(a), float(scale_a), _p(a_out), _p(w), float(scale_w),
+                                            _p(w_out)), "cons_compressed")
+
+    # ---------------------------------------------------------------- ipm
+    def ipm(self, k, has_eta, Q11, q12, lin_s, scal, warm, state_out, result, opts=None):
+        o = None
+        if opts is not None:
+            arr = (C.c_double * 8)(*opts)
+            o = arr
+        check(self.lib.usbs_ipm_solve(self.h, int(k), 1 if has_eta else 0, _p(Q11), _p(q12), _p(lin_s),
+                                      _p(scal), _p(warm), _p(state_out), _p(result), o), "ipm_solve")
+
+    def state_len(self, k):
+        return int(self.lib.usbs_ipm_state_len(int(k)))

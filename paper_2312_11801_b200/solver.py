@@ -1,0 +1,725 @@
+"""Device-resident USBS outer loop: the drop-in for specbundle.solve.
+
+Mirrors bundle.py:426-529 (solve), 390-423 (cold_start), 285-341
+(model_update), 344-372 (compute_residuals), 212-261 (penalized_obj,
+candidate_iterate, descent_test) and subqp.py:455-614 (coefficient
+assembly, alternating_max) with every n- and m-sized array and every k x k
+solve on the GPU.  The host keeps only control flow and the scalars the
+reference branches on (lambda_max, f(y), model value, residuals, the
+alternating-pass stop test), fetched in a few small D2H copies per
+iteration.
+
+Configuration objects are duck-typed: a reference ``SolverConfig`` (with
+``lanczos`` and ``ipm`` members) or this module's ``SolverConfig`` work.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as N
+from .eigen import DeviceLinOp, lanczos_top
+from .engine import Engine
+from .errors import EmptyBasisError
+from .runtime import DeviceProblem, runtime
+
+__all__ = ["LanczosSettings", "IpmOptions", "SolverConfig", "AggregateStats", "Residuals", "SolverState",
+           "IterationInfo", "PrimalOutput", "DeviceSolver", "solve"]
+
+
+# ---------------------------------------------------------------------------
+# configuration (bundle.py:64-91, subqp.py:150-162)
+
+
+@dataclass
+class LanczosSettings:
+    inner_iters: int = 32
+    max_restarts: int = 10
+    tol: Optional[float] = None
+
+
+@dataclass
+class IpmOptions:
+    mu_tol: float = 1e-11
+    kkt_tol: float = 1e-6
+    max_newton: int = 100
+    step_frac: float = 0.99
+    backtrack: float = 0.8
+    min_step: float = 1e-12
+    max_step_failures: int = 6
+    warm_blend: float = 0.2
+
+
+@dataclass
+class SolverConfig:
+    rho: float = 0.01
+    beta: float = 0.25
+    k_c: int = 10
+    k_p: int = 1
+    eps: float = 1e-3
+    sketch_rank: int = 0
+    max_iters: int = 1000
+    max_time: Optional[float] = None
+    seed: int = 0
+    lanczos: LanczosSettings = field(default_factory=LanczosSettings)
+    linf_check: bool = False
+    store_psi: bool = True
+    ipm: IpmOptions = field(default_factory=IpmOptions)
+
+    def __post_init__(self):
+        if not (self.rho > 0 and 0 < self.beta < 1 and self.k_c >= 1 and self.k_p >= 0):
+            raise ValueError("invalid solver configuration")
+        if self.eps <= 0 or self.sketch_rank < 0:
+            raise ValueError("invalid solver configuration")
+
+
+def _ipm_opts(cfg):
+    o = getattr(cfg, "ipm", None) or IpmOptions()
+    return [o.mu_tol, o.kkt_tol, o.max_newton, o.step_frac, o.backtrack, o.min_step, o.max_step_failures,
+            o.warm_blend]
+
+
+# ---------------------------------------------------------------------------
+# state records (bundle.py:94-205); arrays live on the device, numpy on demand
+
+
+@dataclass
+class AggregateStats:
+    trace: float
+    cost_ip: float
+    constr_image_dev: object
+
+    @property
+    def constr_image(self) -> np.ndarray:
+        return self.constr_image_dev.cpu().numpy()
+
+
+@dataclass
+class Residuals:
+    rel_subopt: float
+    rel_infeas: float
+    linf_infeas: float
+    dual_gap: float
+    dual_feas: float
+
+    def converged(self, eps: float, linf_check: bool = False) -> bool:
+        ok = self.rel_subopt <= eps and self.rel_infeas <= eps and self.dual_feas <= eps
+        if linf_check:
+            ok = ok and self.linf_infeas <= eps
+        return ok
+
+
+class DeviceSketchStore:
+    """SketchStore + sketch.py on the device: P (n x r), Psi (n x r)."""
+
+    def __init__(self, eng: Engine, n: int, r: int, seed: int, psi_host: Optional[np.ndarray] = None):
+        if not 1 <= r <= n:
+            raise ValueError(f"sketch rank {r} must lie in [1, {n}]")
+        self.eng, self.n, self.r, self.psi_seed = eng, n, r, int(seed)
+        rt = eng.rt
+        if psi_host is None:  # make_test_matrix (sketch.py:25-27): legacy MT19937, host once
+            psi_host = np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))
+        self.psi = rt.upload(psi_host)
+        self.P = rt.zeros(n, r)
+        self.G = rt.empty(64, max(r, 1))
+
+    def update(self, eta: float, F, lams) -> None:
+        """sketch_update with Q = I (sketch.py:58-74): P <- eta P + (F L)(F^T Psi)."""
+        if eta < 0:
+            raise ValueError("eta must be nonnegative")
+        kc = F.shape[1]
+        G = self.G[:kc]
+        self.eng.gram(F, self.psi, G)
+        self.eng.rowgemm(F, G, self.P, alpha=1.0, beta=float(eta), Y0=self.P, xs=lams)
+
+    @property
+    def sketch_mat(self) -> np.ndarray:
+        return self.P.cpu().numpy()
+
+    def factorize(self):
+        """reconstruct (sketch.py:77-111): shift, core Gram, Cholesky and the
+        triangular solve on the device; the final thin SVD of the n x r
+        factor runs on the host at exit (LAPACK sign conventions)."""
+        eng, rt, n, r = self.eng, self.eng.rt, self.n, self.r
+        sc = rt.zeros(4)
+        eng.dot_into(self.P.view(-1), self.P.view(-1), sc[0:1])
+        norm_p = math.sqrt(float(sc[0].item()))
+        if norm_p == 0.0:
+            u = np.zeros((n, r))
+            u[:r, :r] = np.eye(r)
+            return u, np.zeros(r)
+        shift = math.sqrt(n) * np.finfo(float).eps * norm_p
+        ps = rt.empty(n, r)
+        eng.vec(N.VOP_AXPBY, n * r, x=self.P.view(-1), y=self.psi.view(-1), s0=1.0, s1=shift, out=ps.view(-1))
+        core = rt.empty(r, r)
+        eng.gram(self.psi, ps, core, sym=True)
+        perm = rt.torch.zeros(r, dtype=rt.torch.int32, device=rt.device)
+        rinv = rt.zeros(r, r)
+        info = rt.zeros(3)
+        eng.pivchol(core, -1.0, perm, rinv, info)
+        if int(info[0].item()) == r and float(info[1].item()) > 0.0:
+            half = eng.rowgemm(ps, rinv, rt.empty(n, r))
+        else:  # rank-deficient core: eigenvalue pseudo-inverse (sketch.py:100-108)
+            vals, vecs = rt.empty(r), rt.empty(r, r)
+            eng.small_eigh(core, vals, vecs)
+            w = vals.cpu().numpy()[::-1].copy()
+            qm = vecs.cpu().numpy()[:, ::-1].copy()
+            keep = w > max(w.max(initial=0.0), 0.0) * 1e-14
+            if not np.any(keep):
+                u = np.zeros((n, r))
+                u[:r, :r] = np.eye(r)
+                return u, np.zeros(r)
+            B = rt.upload(qm[:, keep] / np.sqrt(w[keep])[None, :])
+            half = eng.rowgemm(ps, B, rt.empty(n, int(keep.sum())))
+        u, sv, _ = np.linalg.svd(half.cpu().numpy(), full_matrices=False)
+        return u, np.maximum(sv ** 2 - shift, 0.0)
+
+
+class DeviceExplicitStore:
+    """ExplicitStore (bundle.py:104-117) with Xbar on the device."""
+
+    def __init__(self, eng: Engine, n: int):
+        self.eng = eng
+        self.X = eng.rt.zeros(n, n)
+
+    def update(self, eta: float, F, lams) -> None:
+        self.eng.dense_update(self.X, eta, F, lams)
+
+    @property
+    def xbar(self) -> np.ndarray:
+        return self.X.cpu().numpy()
+
+    def factorize(self):
+        x = self.xbar
+        vals, vecs = np.linalg.eigh(0.5 * (x + x.T))
+        vals, vecs = vals[::-1].copy(), vecs[:, ::-1].copy()
+        keep = vals > max(vals.max(initial=0.0), 0.0) * 1e-12
+        if not np.any(keep):
+            return np.eye(x.shape[0], 1), np.zeros(1)
+        return vecs[:, keep], vals[keep]
+
+
+@dataclass
+class BundleModel:
+    basis_dev: object
+    stats: AggregateStats
+    k_c: int
+    k_p: int
+    store: object
+
+    @property
+    def basis(self) -> np.ndarray:
+        return self.basis_dev.cpu().numpy()
+
+    @property
+    def k(self) -> int:
+        return self.basis_dev.shape[1]
+
+
+@dataclass
+class SolverState:
+    y_dev: object
+    nu_dev: object
+    f_y: Optional[float]
+    lam_y: Optional[float]
+    model: BundleModel
+    descent_steps: int = 0
+    null_steps: int = 0
+    iterations: int = 0
+    last_primal: Optional[AggregateStats] = None
+    residuals: Optional[Residuals] = None
+    status: Optional[str] = None
+    scale_x: float = 1.0
+    scale_c: float = 1.0
+    best_rel_infeas: float = np.inf
+    best_rel_subopt: float = np.inf
+
+    @property
+    def y(self) -> np.ndarray:
+        return self.y_dev.cpu().numpy()
+
+    @property
+    def nu(self) -> np.ndarray:
+        return self.nu_dev.cpu().numpy()
+
+
+@dataclass
+class IterationInfo:
+    """bundle.IterationInfo (bundle.py:180-198); m-vectors download lazily."""
+
+    t: int
+    elapsed: float
+    step: str
+    f_y: float
+    f_cand: float
+    model_val: float
+    y_dev: object
+    y_cand_dev: object
+    nu_cand_dev: object
+    residuals: Residuals
+    primal: AggregateStats
+    eta: float
+    lam_cand: float
+    state: SolverState
+    model: BundleModel
+    alt_passes: int = 0
+    lanczos_matvecs: int = 0
+    lanczos_restarts: int = 0
+
+    @property
+    def y(self):
+        return self.y_dev.cpu().numpy()
+
+    @property
+    def y_cand(self):
+        return self.y_cand_dev.cpu().numpy()
+
+    @property
+    def nu_cand(self):
+        return self.nu_cand_dev.cpu().numpy()
+
+
+@dataclass
+class PrimalOutput:
+    factor: np.ndarray
+    lams: np.ndarray
+    dense: Optional[np.ndarray] = None
+
+
+# scalar slots of the device scratch vector
+S_Q22, S_LINETA, S_EQ22, S_ELINETA, S_DNU, S_CQS, S_BYC, S_RES, S_BY, S_MINI, S_CFIP = 0, 1, 2, 3, 4, 6, 8, 10, 12, 14, 16
+
+
+class DeviceSolver:
+    """Holds the uploaded problem and scratch buffers for one solve."""
+
+    def __init__(self, prob, cfg, dprob: Optional[DeviceProblem] = None):
+        self.prob = prob
+        self.cfg = cfg
+        self.dp = dprob or DeviceProblem(prob)
+        self.eng = Engine(self.dp)
+        self.rt = self.dp.rt
+        self.n, self.m = self.dp.n, self.dp.m
+        self.alpha = float(prob.alpha)
+        self.b = self.dp.b
+        self.ineq = self.dp.ineq
+        self.has_ineq = self.dp.has_ineq
+        self.b_norm = float(np.linalg.norm(np.asarray(prob.b, dtype=float)))
+        self.sc = self.rt.zeros(64)
+        self.opts = _ipm_opts(cfg)
+        lz = getattr(cfg, "lanczos", None) or LanczosSettings()
+        self.lz = (int(lz.inner_iters), int(lz.max_restarts), lz.tol)
+        self.seed = int(cfg.seed)
+        self.k_c = min(cfg.k_c, self.n)
+        self.k_p = min(cfg.k_p, self.n - self.k_c)
+        k = self.k_c + self.k_p
+        self.k = k
+        rt = self.rt
+        n, m = self.n, self.m
+        self.tmp_nk = rt.empty(n, max(k, 1))
+        self.tmp_nk2 = rt.empty(n, max(k, 1))
+        self.vecs = rt.empty(n, max(self.k_c, 1))
+        self.wv = rt.empty(m)
+        self.nu_a = rt.empty(m)
+        self.nu_b = rt.empty(m)
+        self.ax = rt.empty(m)
+        self.ycand = rt.empty(m)
+        self.img_b = rt.empty(m)
+        d = k * (k + 1) // 2
+        self.d = d
+        self.Q11 = rt.empty(d, d)
+        self.q12 = rt.empty(d)
+        self.lin_s = rt.empty(d)
+        self.csv = rt.empty(d)
+        self.cq = rt.empty(k, k)
+        self.zq = rt.empty(k, k)
+        sl = self.eng.state_len(k)
+        self.st_q = rt.zeros(sl)
+        self.st_e = rt.zeros(sl)
+        self.res_q = rt.zeros(8)
+        self.res_e = rt.zeros(8)
+        self.s_act = rt.empty(k, k)
+        self.evals = rt.empty(k)
+        self.evecs = rt.empty(k, k)
+        self.lamc = rt.empty(max(self.k_c, 1))
+        self.ident = rt.upload(np.eye(max(k, 1)))
+
+    # ------------------------------------------------------------ helpers
+    def _fetch(self, *tensors):
+        """One synchronising D2H of several small device arrays."""
+        return [t.cpu().numpy() for t in tensors]
+
+    def penalized_lanczos(self, y_dev, which=1):
+        """penalized_obj (bundle.py:212-236) minus the <b,y> term (device dot)."""
+        if which == 1:
+            self.dp.assemble(y_dev)
+        op = DeviceLinOp(self.dp, which)
+        inner, rst, tol = self.lz
+        return lanczos_top(op, self.k_c, inner, rst, tol, self.seed, out=self.vecs)
+
+    def completion(self, basis, k, tag):
+        """_completion_columns (bundle.py:264-282) with host PCG64 vectors."""
+        rt, eng, n = self.rt, self.eng, self.n
+        have = 0 if basis is None else basis.shape[1]
+        out = rt.empty(n, k)
+        if have:
+            eng.rowgemm(basis, self.ident[:have, :have], out[:, :have])
+        attempt = 0
+        coef = rt.empty(k, 1)
+        red = rt.zeros(2)
+        while have < k:
+            g = np.random.default_rng([self.seed & 0xFFFFFFFF, 0x5EED, tag, attempt])
+            v = rt.upload(g.standard_normal(n).reshape(n, 1))
+            if have:
+                cur = out[:, :have]
+                eng.gram(cur, v, coef[:have])
+                eng.rowgemm(cur, coef[:have], v, alpha=-1.0, beta=1.0, Y0=v)
+            eng.dot_into(v.view(-1), v.view(-1), red)
+            nv = math.sqrt(float(red[0].item()))
+            attempt += 1
+            if nv < 1e-10:
+                continue
+            eng.rowgemm(v, self.ident[:1, :1], out[:, have:have + 1], alpha=1.0 / nv)
+            have += 1
+        return out
+
+    def orthonormalize(self, A):
+        """symlin.orthonormalize (symlin.py:148-190): pivot order and drop rule
+        from a pivoted Cholesky of the Gram, then CholQR2.  Falls back to the
+        exact column-pivoted Gram-Schmidt when a selected residual is below
+        1e-6 of the largest column (where a Gram cannot resolve the 1e-12 rule)."""
+        rt, eng = self.rt, self.eng
+        c = A.shape[1]
+        G = rt.empty(c, c)
+        eng.gram(A, A, G)
+        perm = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
+        rinv = rt.zeros(c, c)
+        info = rt.zeros(3)
+        eng.pivchol(G, 1e-12, perm, rinv, info)
+        info_h, perm_h, rinv_h = self._fetch(info, perm, rinv)
+        r = int(info_h[0])
+        if info_h[2] == 0.0:
+            raise EmptyBasisError("all input columns are zero")
+        if r == 0:
+            raise EmptyBasisError("all input columns are numerically dependent")
+        if info_h[1] < 1e-6:
+            return self._gs_exact(A)
+        B = np.zeros((c, r))
+        B[perm_h[:r].astype(np.int64), :] = rinv_h[:r, :r]
+        Y = eng.rowgemm(A, rt.upload(B), rt.empty(self.n, r))
+        G2 = rt.empty(r, r)
+        eng.gram(Y, Y, G2)
+        rinv2 = rt.zeros(r, r)
+        eng.pivchol(G2, -1.0, perm, rinv2, info)
+        Q = eng.rowgemm(Y, rinv2, rt.empty(self.n, r))
+        return Q
+
+    def _gs_exact(self, A):
+        """Column-pivoted two-pass Gram-Schmidt on device primitives."""
+        rt, eng, n = self.rt, self.eng, self.n
+        c = A.shape[1]
+        work = rt.empty(n, c)
+        eng.rowgemm(A, self.ident[:c, :c], work)
+        G = rt.empty(c, c)
+        eng.gram(work, work, G)
+        norms = np.sqrt(np.maximum(np.diag(G.cpu().numpy()), 0.0))
+        thresh = 1e-12 * float(norms.max())
+        alive = list(range(c))
+        basis = rt.empty(n, c)
+        nb = 0
+        coef = rt.empty(c, c)
+        red = rt.zeros(2)
+        while alive:
+            eng.gram(work, work, G)
+            g = G.cpu().numpy()
+            nr = np.sqrt(np.maximum(np.array([g[j, j] for j in alive]), 0.0))
+            pick = int(np.argmax(nr))
+            if nr[pick] <= thresh:
+                break
+            piv = alive.pop(pick)
+            q = rt.empty(n, 1)
+            eng.rowgemm(work[:, piv:piv + 1], self.ident[:1, :1], q)
+            if nb:
+                B = basis[:, :nb]
+                eng.gram(B, q, coef[:nb, :1])
+                eng.rowgemm(B, coef[:nb, :1], q, alpha=-1.0, beta=1.0, Y0=q)
+            eng.dot_into(q.view(-1), q.view(-1), red)
+            nq = math.sqrt(float(red[0].item()))
+            if nq <= thresh:
+                continue
+            eng.rowgemm(q, self.ident[:1, :1], basis[:, nb:nb + 1], alpha=1.0 / nq)
+            qb = basis[:, nb:nb + 1]
+            nb += 1
+            for j in alive:
+                col = work[:, j:j + 1]
+                eng.gram(qb, col, coef[:1, :1])
+                eng.rowgemm(qb, coef[:1, :1], col, alpha=-1.0, beta=1.0, Y0=col)
+        if nb == 0:
+            raise EmptyBasisError("all input columns are numerically dependent")
+        out = rt.empty(n, nb)
+        eng.rowgemm(basis[:, :nb], self.ident[:nb, :nb], out)
+        return out
+
+    # ------------------------------------------------------------ cold start
+    def cold_start(self) -> SolverState:
+        """bundle.cold_start (bundle.py:390-423)."""
+        rt = self.rt
+        sketch_seed = int(np.random.SeedSequence(self.seed).generate_state(2)[0])
+        eig = self.penalized_lanczos(None, which=0)
+        basis = self.completion(eig.eigenvectors_dev, self.k, tag=0)
+        stats = AggregateStats(0.0, 0.0, rt.zeros(self.m))
+        if self.cfg.sketch_rank > 0:
+            store = DeviceSketchStore(self.eng, self.n, min(self.cfg.sketch_rank, self.n), sketch_seed)
+        else:
+            store = DeviceExplicitStore(self.eng, self.n)
+        model = BundleModel(basis, stats, self.k_c, self.k_p, store)
+        return SolverState(rt.zeros(self.m), rt.zeros(self.m), None, None, model,
+                           last_primal=AggregateStats(0.0, 0.0, stats.constr_image_dev),
+                           scale_x=float(self.prob.scale_x), scale_c=float(self.prob.scale_c))
+
+    def state_from_arrays(self, y, nu, f_y, lam_y, basis, trace, cost_ip, image, xbar=None, sketch=None,
+                          descent=0, null=0, last_primal=None) -> SolverState:
+        """Device state from host arrays (a reference SolverState's fields or
+        a loaded USBS state record), e.g. for warm starts and lock-step replay."""
+        rt = self.rt
+        if sketch is not None:
+            sketch_seed = int(np.random.SeedSequence(self.seed).generate_state(2)[0])
+            store = DeviceSketchStore(self.eng, self.n, sketch.shape[1], sketch_seed)
+            store.P.copy_(rt.upload(sketch))
+        elif xbar is not None:
+            store = DeviceExplicitStore(self.eng, self.n)
+            store.X.copy_(rt.upload(xbar))
+        else:
+            store = None
+        stats = AggregateStats(float(trace), float(cost_ip), rt.upload(image))
+        model = BundleModel(rt.upload(basis), stats, self.k_c, self.k_p, store)
+        lp = stats if last_primal is None else AggregateStats(last_primal[0], last_primal[1],
+                                                              rt.upload(last_primal[2]))
+        return SolverState(rt.upload(y), rt.upload(nu), f_y, lam_y, model, descent_steps=int(descent),
+                           null_steps=int(null), last_primal=lp, scale_x=float(self.prob.scale_x),
+                           scale_c=float(self.prob.scale_c))
+
+    # ------------------------------------------------------------ subproblem
+    def alternating_max(self, model: BundleModel, y, nu0, max_passes=50, tol=1e-8):
+        """subqp.alternating_max (subqp.py:552-614) + assemble_quad_coeffs
+        (471-527): compressed Gram, C^T w, IPM and A(V S V^T) on device."""
+        eng, rt, sc = self.eng, self.rt, self.sc
+        a, rho = self.alpha, float(self.cfg.rho)
+        V = model.basis_dev
+        k = V.shape[1]
+        tr = model.stats.trace
+        has_eta = tr > 0.0
+        img = model.stats.constr_image_dev
+        nu = self.nu_a
+        eng.vec(N.VOP_PROJN, self.m, x=nu0, ineq=self.ineq, out=nu)
+        a2 = a * a
+        eng.compressed(V, scale_gram=a2 / rho, gram_out=self.Q11, a=img if has_eta else None,
+                       scale_a=(a2 / (rho * tr)) if has_eta else 0.0, a_out=self.q12 if has_eta else None)
+        if has_eta:
+            eng.dot_into(img, img, sc[S_Q22:S_Q22 + 1], scale=a2 / (rho * tr * tr))
+        else:
+            eng.dot_into(img[:1], img[:1], sc[S_Q22:S_Q22 + 1], scale=0.0)
+        eng.apply(0, V, self.tmp_nk[:, :k], gram=self.cq)  # cost_quad = sym(V^T C V)
+        eng.svec(self.cq, self.csv, scale=a)
+        warm = None
+        passes = 0
+        for passes in range(1, max_passes + 1):
+            eng.vec(N.VOP_W, self.m, x=y, y=nu, b=self.b, s0=rho, out=self.wv)
+            eng.compressed(V, w=self.wv, scale_w=a, w_out=self.lin_s)
+            eng.vec(N.VOP_AXPBY, self.d, x=self.lin_s, y=self.csv, s0=1.0, s1=-1.0, out=self.lin_s)
+            if has_eta:
+                eng.dot_into(img, self.wv, sc[S_LINETA:S_LINETA + 1], scale=a / tr,
+                             shift=-(a / tr) * model.stats.cost_ip)
+            else:
+                eng.dot_into(img[:1], img[:1], sc[S_LINETA:S_LINETA + 1], scale=0.0)
+            eng.ipm(k, has_eta, self.Q11, self.q12 if has_eta else None, self.lin_s, sc[S_Q22:S_Q22 + 2], warm,
+                    self.st_q, self.res_q, self.opts)
+            warm = self.st_q
+            S = self.st_q[:k * k].view(k, k)
+            eng.image(V, S, self.ax, s_scale=a, beta_dev=self.res_q[3:4] if has_eta else None,
+                      beta=(a / tr) if has_eta else 0.0, base=img if has_eta else None)
+            nxt = self.nu_b if nu is self.nu_a else self.nu_a
+            eng.vec(N.VOP_NUNEXT, self.m, x=self.ax, y=y, z=nu, b=self.b, ineq=self.ineq, s0=rho, out=nxt,
+                    red=sc[S_DNU:S_DNU + 2])
+            nu = nxt
+            if not self.has_ineq:
+                break
+            dnu = math.sqrt(max(float(sc[S_DNU].item()), 0.0))
+            if dnu <= tol * (1.0 + self.b_norm):
+                break
+        eng.dot_into(self.cq.view(-1), self.st_q[:k * k], sc[S_CQS:S_CQS + 1], scale=a)
+        return nu, passes, has_eta
+
+    # ------------------------------------------------------------ model update
+    def model_update(self, model: BundleModel, eta, new_vecs, tag):
+        """bundle.model_update (bundle.py:285-341) on device; returns the new
+        model with trace/cost statistics still pending (finalised at the
+        residual sync)."""
+        eng, rt = self.eng, self.rt
+        kp, kc = model.k_p, model.k_c
+        V = model.basis_dev
+        k = V.shape[1]
+        eng.small_eigh(self.s_act, self.evals, self.evecs)
+        eng.vec(N.VOP_RELU, kc, x=self.evals[kp:], out=self.lamc[:kc])
+        lamc = self.lamc[:kc]
+        F = self.tmp_nk[:, :kc]
+        eng.rowgemm(V, self.evecs[:, kp:], F)
+        CF = self.tmp_nk2[:, :kc]
+        eng.apply(0, F, CF)
+        eng.wcoldot(F, CF, lamc, self.sc[S_CFIP:S_CFIP + 1])
+        img_new = self.img_b
+        eng.image(F, lamc, img_new, s_is_diag=True, beta=eta, base=model.stats.constr_image_dev)
+        self.img_b = model.stats.constr_image_dev  # ping-pong
+        if model.store is not None:
+            model.store.update(eta, F, lamc)
+        if kp == 0:
+            new_basis = rt.empty(self.n, kc)
+            eng.rowgemm(new_vecs, self.ident[:kc, :kc], new_basis)
+        else:
+            cand = rt.empty(self.n, kp + kc)
+            eng.rowgemm(V, self.evecs[:, :kp], cand[:, :kp])
+            eng.rowgemm(new_vecs, self.ident[:kc, :kc], cand[:, kp:])
+            try:
+                new_basis = self.orthonormalize(cand)
+            except EmptyBasisError:
+                new_basis = None
+        if new_basis is None or new_basis.shape[1] < k:
+            new_basis = self.completion(new_basis, k, tag)
+        pending = (eta, model.stats.trace, model.stats.cost_ip)
+        stats = AggregateStats(float("nan"), float("nan"), img_new)
+        return BundleModel(new_basis, stats, kc, kp, model.store), pending
+
+    # ------------------------------------------------------------ outer loop
+    def solve(self, init: Optional[SolverState] = None, callback: Optional[Callable] = None):
+        """bundle.solve (bundle.py:426-529)."""
+        cfg, rt, eng, sc = self.cfg, self.rt, self.eng, self.sc
+        state = init if init is not None else self.cold_start()
+        model = state.model
+        if model.basis_dev.shape[0] != self.n or state.y_dev.shape[0] != self.m:
+            raise ValueError("initial state does not match the problem dimensions")
+        t_start = time.monotonic()
+        y = state.y_dev.clone()  # never overwrite the caller's buffers
+        if state.f_y is None or state.lam_y is None:
+            if self.has_ineq:
+                eng.vec(N.VOP_MINI, self.m, x=y, ineq=self.ineq, red=sc[S_MINI:S_MINI + 2])
+                if float(sc[S_MINI + 1].item()) > 0.0:
+                    raise ValueError("initial dual point violates the sign constraints")
+            eig = self.penalized_lanczos(y)
+            eng.dot_into(self.b, y, sc[S_BY:S_BY + 1])
+            lam_y = float(eig.eigenvalues[0])
+            f_y = self.alpha * max(lam_y, 0.0) + float(sc[S_BY].item())
+        else:
+            f_y, lam_y = state.f_y, state.lam_y
+        primal = state.last_primal if state.last_primal is not None else model.stats
+        residuals = self.residuals(y, f_y, lam_y, primal)
+        state.f_y, state.lam_y, state.residuals = f_y, lam_y, residuals
+        status = "converged" if residuals.converged(cfg.eps, cfg.linf_check) else None
+        t = 0
+        inner_nu = rt.empty(self.m)
+        inner_nu.copy_(state.nu_dev)
+        y_buf = rt.empty(self.m)
+        a = self.alpha
+        while status is None:
+            if t >= cfg.max_iters or (cfg.max_time is not None and time.monotonic() - t_start > cfg.max_time):
+                status = "budget"
+                break
+            nu, passes, has_eta = self.alternating_max(model, y, inner_nu)
+            inner_nu, nu_keep = nu, nu
+            k = model.k
+            eng.vec(N.VOP_CAND, self.m, x=self.ax, y=y, z=nu, b=self.b, ineq=self.ineq, s0=float(cfg.rho),
+                    out=self.ycand)
+            if self.has_ineq:
+                eng.vec(N.VOP_MINI, self.m, x=self.ycand, ineq=self.ineq, red=sc[S_MINI:S_MINI + 2])
+            eig = self.penalized_lanczos(self.ycand)
+            lam_c = float(eig.eigenvalues[0])
+            # ipm_eval(assemble_eval_coeffs(prob, model, y_cand)) (subqp.py:455-468)
+            tr = model.stats.trace
+            eng.apply(1, model.basis_dev, self.tmp_nk2[:, :k], gram=self.zq)
+            eng.svec(self.zq, self.lin_s, scale=-a)
+            eng.dot_into(self.ycand[:1], self.ycand[:1], sc[S_EQ22:S_EQ22 + 1], scale=0.0)
+            if tr > 0.0:
+                eng.dot_into(self.ycand, model.stats.constr_image_dev, sc[S_ELINETA:S_ELINETA + 1],
+                             scale=a / tr, shift=-(a / tr) * model.stats.cost_ip)
+            else:
+                eng.dot_into(self.ycand[:1], self.ycand[:1], sc[S_ELINETA:S_ELINETA + 1], scale=0.0)
+            eng.ipm(k, tr > 0.0, None, None, self.lin_s, sc[S_EQ22:S_EQ22 + 2], None, self.st_e, self.res_e,
+                    self.opts)
+            eng.dot_into(self.b, self.ycand, sc[S_BYC:S_BYC + 1])
+            # s_act = alpha S (original units) for model_update
+            S = self.st_q[:k * k].view(k, k)
+            eng.vec(N.VOP_AXPBY, k * k, x=S.reshape(-1), s0=a, out=self.s_act.view(-1))
+            sc_h, rq, re_, sdiag = self._fetch(sc[:18], self.res_q, self.res_e, S.diagonal())
+            if self.has_ineq and sc_h[S_MINI + 1] > 0.0:
+                raise ValueError("candidate dual point violates the sign constraints")
+            eta_act = (a * float(rq[3]) / tr) if has_eta else 0.0
+            c_x = eta_act * model.stats.cost_ip + float(sc_h[S_CQS])
+            tr_x = eta_act * tr + float(np.sum(a * sdiag))
+            b_yc = float(sc_h[S_BYC])
+            f_cand = a * max(lam_c, 0.0) + b_yc
+            model_val = b_yc - float(re_[0])
+            accept = cfg.beta * (f_y - model_val) <= f_y - f_cand
+            if accept:
+                y_buf.copy_(self.ycand)
+                y, y_buf = y_buf, y
+                f_y, lam_y = f_cand, lam_c
+                state.nu_dev = nu_keep.clone()
+                state.descent_steps += 1
+            else:
+                state.null_steps += 1
+            step = "descent" if accept else "null"
+            model, pending = self.model_update(model, eta_act, eig.eigenvectors_dev, tag=t + 1)
+            primal = AggregateStats(tr_x, c_x, self.ax)
+            residuals = self.residuals(y, f_y, lam_y, primal, pending=pending, model=model)
+            state.y_dev, state.f_y, state.lam_y, state.model = y, f_y, lam_y, model
+            state.last_primal, state.residuals, state.iterations = primal, residuals, t + 1
+            state.best_rel_infeas = min(state.best_rel_infeas, residuals.rel_infeas)
+            state.best_rel_subopt = min(state.best_rel_subopt, residuals.rel_subopt)
+            if callback is not None:
+                callback(IterationInfo(t, time.monotonic() - t_start, step, f_y, f_cand, model_val, y, self.ycand,
+                                       nu_keep, residuals, primal, eta_act, lam_c, state, model, passes,
+                                       eig.matvecs, eig.restarts))
+            t += 1
+            if residuals.converged(cfg.eps, cfg.linf_check):
+                status = "converged"
+        state.status = status
+        state.last_primal = AggregateStats(state.last_primal.trace, state.last_primal.cost_ip,
+                                           state.last_primal.constr_image_dev.clone())
+        return state, self.primal_output(model)
+
+    def residuals(self, y, f_y, lam_y, primal, pending=None, model=None) -> Residuals:
+        """compute_residuals (bundle.py:344-372); also finalises the pending
+        trace / cost statistics of a model update in the same sync."""
+        eng, sc = self.eng, self.sc
+        eng.vec(N.VOP_RESID, self.m, x=primal.constr_image_dev, b=self.b, ineq=self.ineq,
+                red=sc[S_RES:S_RES + 2])
+        eng.dot_into(self.b, y, sc[S_BY:S_BY + 1])
+        if pending is not None:
+            sc_h, lamc = self._fetch(sc[:18], self.lamc[:model.k_c])
+            eta, tr_old, cip_old = pending
+            model.stats.trace = eta * tr_old + float(lamc.sum())
+            model.stats.cost_ip = eta * cip_old + float(sc_h[S_CFIP])
+        else:
+            (sc_h,) = self._fetch(sc[:18])
+        c_x = primal.cost_ip
+        rel_infeas = math.sqrt(max(float(sc_h[S_RES]), 0.0)) / (1.0 + self.b_norm)
+        linf = float(sc_h[S_RES + 1]) if self.m else 0.0
+        return Residuals((c_x - f_y) / (1.0 + abs(c_x)), rel_infeas, linf, abs(float(sc_h[S_BY]) - c_x), lam_y)
+
+    def primal_output(self, model: BundleModel) -> PrimalOutput:
+        """bundle.primal_output (bundle.py:532-538)."""
+        if model.store is None:
+            return PrimalOutput(np.eye(self.n, 1), np.zeros(1))
+        factor, lams = model.store.factorize()
+        dense = model.store.xbar if isinstance(model.store, DeviceExplicitStore) else None
+        return PrimalOutput(factor, lams, dense)
+
+
+def solve(prob, cfg, init: Optional[SolverState] = None, callback: Optional[Callable] = None):
+    """Drop-in for specbundle.solve (bundle.py:426-529): same arguments and
+    return value (SolverState, PrimalOutput); arrays of the state live on the
+    GPU and convert to numpy on attribute access."""
+    return DeviceSolver(prob, cfg).solve(init=init, callback=callback)

@@ -60,6 +60,7 @@ def test_op_apply_matches_oracle(name, k):
     rng = np.random.default_rng(1234)
     y = rng.standard_normal(p.m) * 1e-3
     v, _ = np.linalg.qr(rng.standard_normal((p.n, k)))
+    k = v.shape[1]
     dp = runtime.DeviceProblem(p)
     rt = dp.rt
     z = (p.cost - O.adjoint_csr(p.constraints, y, p.n)).tocsr()

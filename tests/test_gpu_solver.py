@@ -1,0 +1,222 @@
+"""GPU parity of the bookkeeping kernels, the device IPM and the device outer
+loop against the golden fixtures (recorded from the reference) and the CPU
+oracle.  Tolerances follow SURVEY 7 / BASELINE.md: kernel parity at rounding
+level, lock-step iteration at 1e-6 relative, free-running at solver
+tolerance."""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, cuda_ok
+from helpers import TRAJ_CFG, load_npz, random_graph, random_qap, traj_problem
+from oracle import usbs_cpu as O
+from paper_2312_11801_b200 import instances as inst
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+
+def mods():
+    from paper_2312_11801_b200 import engine, runtime, solver, subproblem
+    return engine, runtime, solver, subproblem
+
+
+# ------------------------------------------------------------------ IPM
+
+def test_ipm_quad_frozen_projected_gradient_values():
+    """The reference's frozen 1e6-step PG oracle (pkg/tests/data_quad_oracle.json)."""
+    _, _, _, sp = mods()
+    g = json.loads((GOLDEN / "quad_oracle.json").read_text())
+    for s, want in g["values"].items():
+        c = g["coeffs"][s]
+        q = O.Coeffs(np.array(c["quad_ss"]), np.array(c["quad_s_eta"]), c["quad_eta"], np.array(c["lin_s"]),
+                     c["lin_eta"], True, 3)
+        r = sp.ipm_quad(q)
+        assert r.value == pytest.approx(want, abs=1e-5), s
+        assert r.value == pytest.approx(g["ipm_value"][s], abs=1e-9), s
+        assert r.exact
+
+
+def test_ipm_matches_reference_golden():
+    _, _, _, sp = mods()
+    z = load_npz("ipm.npz")
+    for seed in range(4):
+        pre = f"quad{seed}"
+        qe, le, he, k = z[pre + "/scal"]
+        q = O.Coeffs(z[pre + "/Q"], z[pre + "/q12"], float(qe), z[pre + "/h"], float(le), bool(he), int(k))
+        r = sp.ipm_quad(q)
+        eta_ref, val_ref, it_ref, ex_ref = z[pre + "/out"]
+        assert r.value == pytest.approx(val_ref, abs=1e-9 * (1 + abs(val_ref)))
+        np.testing.assert_allclose(r.s_opt, z[pre + "/S"], atol=1e-6)
+        assert r.eta_opt == pytest.approx(eta_ref, abs=1e-6)
+        assert r.exact == bool(ex_ref)
+        assert abs(r.newton_iters - int(it_ref)) <= 2
+        e = sp.ipm_eval(O.linear_coeffs(q.lin_s, q.lin_eta, q.has_eta, q.k))
+        ev = z[pre + "/evalout"]
+        assert e.value == pytest.approx(ev[1], abs=1e-9 * (1 + abs(ev[1])))
+        np.testing.assert_allclose(e.s_opt, z[pre + "/evalS"], atol=1e-6)
+
+
+@pytest.mark.parametrize("k", [11, 20])
+def test_ipm_large_k_vs_oracle(k):
+    """d = 66 and d = 210 (the BASELINE bundle sizes), warm start included."""
+    _, _, _, sp = mods()
+    rng = np.random.default_rng(k)
+    d = k * (k + 1) // 2
+    a = rng.standard_normal((d + 5, d))
+    zz = rng.standard_normal(d + 5)
+    q = O.Coeffs(a.T @ a / (d + 5), a.T @ zz / (d + 5), float(zz @ zz / (d + 5)), rng.standard_normal(d),
+                 float(rng.standard_normal()), True, k)
+    ro = O.ipm(q)
+    r = sp.ipm_quad(q)
+    assert r.value == pytest.approx(ro.value, abs=1e-8 * (1 + abs(ro.value)))
+    np.testing.assert_allclose(r.s_opt, ro.s_opt, atol=1e-6)
+    # warm restart on perturbed linear term
+    q2 = O.Coeffs(q.quad_ss, q.quad_s_eta, q.quad_eta, q.lin_s + 0.01 * rng.standard_normal(d), q.lin_eta, True, k)
+    ro2 = O.ipm(q2, warm=ro.state)
+    r2 = sp.ipm_quad(q2, warm=r.state)
+    assert r2.value == pytest.approx(ro2.value, abs=1e-8 * (1 + abs(ro2.value)))
+
+
+# ------------------------------------------------------------------ constraint kernels
+
+@pytest.mark.parametrize("tag", ["mc", "qap"])
+def test_constraint_kernels_vs_reference(tag):
+    engine, runtime, solver, _ = mods()
+    z = load_npz("cons.npz")
+    p = inst.maxcut_problem(random_graph(12, 0.4, 0)) if tag == "mc" else inst.qap_problem(random_qap(3, 1))
+    y, v, s, lam = z[f"{tag}/y"], z[f"{tag}/V"], z[f"{tag}/S"], z[f"{tag}/lam"]
+    dp = runtime.DeviceProblem(p)
+    eng = engine.Engine(dp)
+    rt = dp.rt
+    V, S = rt.upload(v), rt.upload(s)
+    out = rt.empty(p.m)
+    eng.image(V, S, out)
+    np.testing.assert_allclose(out.cpu().numpy(), z[f"{tag}/img_lowrank"], rtol=1e-12, atol=1e-14)
+    eng.image(V, rt.upload(lam), out, s_is_diag=True)
+    np.testing.assert_allclose(out.cpu().numpy(), z[f"{tag}/img_factor"], rtol=1e-12, atol=1e-14)
+    comp = z[f"{tag}/compressed"]
+    d = comp.shape[1]
+    G, A, W = rt.empty(d, d), rt.empty(d), rt.empty(d)
+    yv = rt.upload(y)
+    eng.compressed(V, scale_gram=2.0, gram_out=G, a=yv, scale_a=3.0, a_out=A, w=yv, scale_w=-1.0, w_out=W)
+    np.testing.assert_allclose(G.cpu().numpy(), 2.0 * comp.T @ comp, rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(A.cpu().numpy(), 3.0 * comp.T @ y, rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(W.cpu().numpy(), -comp.T @ y, rtol=1e-11, atol=1e-13)
+
+
+@pytest.mark.parametrize("name", ["C1", "C5s", "qap20"])
+def test_compressed_gram_at_scale(name):
+    engine, runtime, solver, _ = mods()
+    if name == "C1":
+        p, k = inst.baseline_config("C1").problem, 11
+    elif name == "C5s":
+        p, k = inst.baseline_config("C5", small=True).problem, 20
+    else:
+        p, k = inst.qap_problem(random_qap(5, 3)), 20
+    rng = np.random.default_rng(5)
+    v, _ = np.linalg.qr(rng.standard_normal((p.n, k)))
+    w = rng.standard_normal(p.m)
+    comp = O.compressed(p.constraints, v)
+    dp = runtime.DeviceProblem(p)
+    eng = engine.Engine(dp)
+    rt = dp.rt
+    d = k * (k + 1) // 2
+    G, W = rt.empty(d, d), rt.empty(d)
+    eng.compressed(rt.upload(v), scale_gram=1.0, gram_out=G, w=rt.upload(w), scale_w=1.0, w_out=W)
+    ref = comp.T @ comp
+    np.testing.assert_allclose(G.cpu().numpy(), ref, atol=1e-12 * np.abs(ref).max())
+    rw = comp.T @ w
+    np.testing.assert_allclose(W.cpu().numpy(), rw, atol=1e-12 * np.abs(rw).max() * np.sqrt(p.m))
+
+
+def test_sketch_update_and_reconstruct_vs_reference():
+    engine, runtime, solver, _ = mods()
+    z = load_npz("sketch.npz")
+    p = inst.maxcut_problem(random_graph(50, 0.2, 1))
+    dp = runtime.DeviceProblem(p)
+    eng = engine.Engine(dp)
+    rt = dp.rt
+    st = solver.DeviceSketchStore(eng, 50, 6, int(z["seed"][0]))
+    np.testing.assert_array_equal(st.psi.cpu().numpy(), z["psi"])
+    for t in range(3):
+        st.update(float(z[f"step{t}/eta"][0]), rt.upload(z[f"step{t}/F"]), rt.upload(z[f"step{t}/lam"]))
+        np.testing.assert_allclose(st.P.cpu().numpy(), z[f"step{t}/P"], rtol=1e-12, atol=1e-14)
+    u, lam = st.factorize()
+    np.testing.assert_allclose(lam, z["lams"], rtol=1e-8, atol=1e-12)
+    ref_u = z["U"]
+    keep = z["lams"] > 1e-10
+    pu = u[:, keep] @ u[:, keep].T
+    pr = ref_u[:, keep] @ ref_u[:, keep].T
+    assert np.linalg.norm(pu - pr) <= 1e-6
+
+
+def test_orthonormalize_span_and_drops():
+    engine, runtime, solver, _ = mods()
+    p = inst.maxcut_problem(random_graph(200, 0.05, 2))
+    cfg = solver.SolverConfig()
+    ds = solver.DeviceSolver(p, cfg)
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((200, 6))
+    a[:, 4] = a[:, 0] + 1e-3 * rng.standard_normal(200)   # near-dependent but kept
+    a[:, 5] = 2.0 * a[:, 1]                                # exactly dependent: dropped
+    q = ds.orthonormalize(ds.rt.upload(a)).cpu().numpy()
+    ref = O.gs_pivoted(a)
+    assert q.shape == ref.shape
+    np.testing.assert_allclose(q.T @ q, np.eye(q.shape[1]), atol=1e-12)
+    assert np.linalg.norm(q @ q.T - ref @ ref.T) <= 1e-9
+
+
+# ------------------------------------------------------------------ outer loop
+
+def test_lockstep_c1_iteration():
+    """Inject the reference state at t=10 (golden) and compare the next
+    iteration: f_cand, model value, candidate dual, primal image and
+    residuals at 1e-6 relative, the step decision exactly."""
+    engine, runtime, solver, _ = mods()
+    z = load_npz("lockstep_c1.npz")
+    p = inst.baseline_config("C1").problem
+    cfg = solver.SolverConfig(rho=0.01, beta=0.25, k_c=10, k_p=1, sketch_rank=0, max_iters=1, seed=0)
+    ds = solver.DeviceSolver(p, cfg)
+    st = ds.state_from_arrays(z["y"], z["nu"], float(z["f_y"]), float(z["lam_y"]), z["basis"], float(z["trace"]),
+                              float(z["cost_ip"]), z["image"], xbar=z["xbar"], descent=int(z["descent"]),
+                              null=int(z["null"]))
+    rec = []
+    ds.solve(init=st, callback=rec.append)
+    r = rec[0]
+    rel = lambda a, b: abs(a - b) / max(1e-300, abs(b))  # noqa: E731
+    assert rel(r.f_cand, float(z["n_f_cand"])) <= 1e-6
+    assert rel(r.model_val, float(z["n_model_val"])) <= 1e-6
+    assert (1 if r.step == "descent" else 0) == int(z["n_step"])
+    yc = z["n_y_cand"]
+    assert np.linalg.norm(r.y_cand - yc) <= 1e-6 * np.linalg.norm(yc)
+    im = z["n_image"]
+    assert np.linalg.norm(r.primal.constr_image - im) <= 1e-6 * np.linalg.norm(im)
+    assert rel(r.primal.trace, float(z["n_trace"])) <= 1e-6
+    assert rel(r.primal.cost_ip, float(z["n_cost_ip"])) <= 1e-6
+    assert rel(r.residuals.rel_infeas, float(z["n_rel_infeas"])) <= 1e-6
+    assert rel(r.lam_cand, float(z["n_lam_cand"])) <= 1e-8
+
+
+@pytest.mark.parametrize("name", list(TRAJ_CFG))
+def test_trajectory_vs_reference(name):
+    """Free-running device solve vs the reference trajectory: the first
+    iterations agree tightly (before chaos amplifies rounding), the rest at
+    solver tolerance."""
+    engine, runtime, solver, _ = mods()
+    z = load_npz(f"traj_{name}.npz")
+    p = traj_problem(name)
+    kw = dict(TRAJ_CFG[name])
+    cfg = solver.SolverConfig(**kw)
+    rec = []
+    st, out = solver.solve(p, cfg, callback=rec.append)
+    fy = np.array([r.f_y for r in rec])
+    steps = np.array([1 if r.step == "descent" else 0 for r in rec])
+    n0 = min(4, len(fy))
+    np.testing.assert_allclose(fy[:n0], z["f_y"][:n0], rtol=1e-7)
+    np.testing.assert_array_equal(steps[:n0], z["step"][:n0])
+    # same iteration budget, objective within solver tolerance at the end
+    assert len(fy) == len(z["f_y"])
+    assert abs(fy[-1] - z["f_y"][-1]) <= 5e-3 * (1 + abs(z["f_y"][-1]))
