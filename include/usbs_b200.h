@@ -110,6 +110,11 @@ usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int which, int k_c,
                              int* converged, int* restarts, double* ritz_hist, int* n_hist,
                              int* matvecs);
 
+/* Phase timers of the Lanczos kernel (ns, accumulated while the environment
+ * variable USBS_LZ_PROF is set): phase A, grid barriers, phase B, phase C,
+ * end of cycle, Rayleigh-Ritz, restart.  reset != 0 zeroes them. */
+usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* out_host, int reset);
+
 /* ---- K3: small symmetric eigendecomposition ----------------------------- */
 /* small_eigh (symlin.py:193-198): symmetrise, eigendecompose, descending.
  * k <= 64; a_dev, vals_dev (k), vecs_dev (k x k, columns = eigenvectors). */

@@ -45,6 +45,7 @@ PROTOS = {
     "usbs_lanczos_top": (_i32, [_p, _p, _i32, _i32, _i32, _i32, C.c_double, _p, RNG_FILL, _p,
                                  _pd, _p, _i64, _pd, _pi, _pi, _pd, _pi, _pi]),
     "usbs_small_eigh": (_i32, [_p, _i32, _p, _p, _p]),
+    "usbs_lanczos_profile": (_i32, [_p, C.POINTER(C.c_uint64), _i32]),
     "usbs_ipm_solve": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "usbs_ipm_state_len": (_i32, [_i32]),
     "usbs_cons_image": (_i32, [_p, _p, _p, _i64, _i32, _p, _i32, C.c_double, _p, C.c_double, _p, _p]),

@@ -340,78 +340,100 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
               sm.f1[p] + sm.rd[p];
         sm.rhs[p] = r;
       }
-      // M (packed lower): Q11 + E + low-rank
-      const int np = d * (d + 1) / 2;
-      for (int x = tid; x < np; x += nth) {
-        int p = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
-        while (p * (p + 1) / 2 > x) --p;
-        while ((p + 1) * (p + 2) / 2 <= x) ++p;
-        const int q = x - p * (p + 1) / 2;
-        const int i = sm.pi[p], j = sm.pj[p], kq = sm.pi[q], l = sm.pj[q];
-        const double wp = (i == j) ? 1.0 : SQ2, wq = (kq == l) ? 1.0 : SQ2;
+      // M (packed lower): Q11 + E + low-rank; warp per row p, lanes over q <= p
+      {
+        const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
         const double* Hm = sm.H;
         const double* Gm = sm.T;
-        double e = Hm[i * k + kq] * Gm[l * k + j] + Hm[i * k + l] * Gm[kq * k + j] +
-                   Gm[i * k + kq] * Hm[l * k + j] + Gm[i * k + l] * Hm[kq * k + j];
-        e *= (wp * wq) * 0.25;
-        double v = (a.Q11 ? a.Q11[(int64_t)p * d + q] : 0.0) + e;
-        if (!has_eta) v += sm.vI[p] * sm.vI[q] / kappa1;
-        else
-          v -= (sm.g[p] * (kappa1 * sm.g[q] + sm.vI[q]) + sm.vI[p] * (sm.g[q] - kappa2 * sm.vI[q])) / cden;
-        Mp[x] = v;
+        for (int p = wid; p < d; p += nwp) {
+          const int i = sm.pi[p], j = sm.pj[p];
+          const double wp = (i == j) ? 1.0 : SQ2;
+          const double gp = sm.g[p], vp = sm.vI[p];
+          const int64_t row = (int64_t)p * d;
+          const int base = p * (p + 1) / 2;
+          for (int q = lane; q <= p; q += 32) {
+            const int kq = sm.pi[q], l = sm.pj[q];
+            const double wq = (kq == l) ? 1.0 : SQ2;
+            double e = Hm[i * k + kq] * Gm[l * k + j] + Hm[i * k + l] * Gm[kq * k + j] +
+                       Gm[i * k + kq] * Hm[l * k + j] + Gm[i * k + l] * Hm[kq * k + j];
+            e *= (wp * wq) * 0.25;
+            double v = (a.Q11 ? a.Q11[row + q] : 0.0) + e;
+            if (!has_eta) v += vp * sm.vI[q] / kappa1;
+            else v -= (gp * (kappa1 * sm.g[q] + sm.vI[q]) + vp * (sm.g[q] - kappa2 * sm.vI[q])) / cden;
+            Mp[base + q] = v;
+          }
+        }
       }
       __syncthreads();
-      // Cholesky of M, right-looking, one barrier per column; column j is
-      // scaled lazily during column j+1 (nobody reads it then)
-      for (int j = 0; j < d; ++j) {
-        if (j > 0) {
-          const double rsp = sm.sc[0];
-          for (int i = j + tid; i < d; i += nth) Mp[pidx(i, j - 1)] *= rsp;  // i >= j > j-1
-          if (tid == 0) Mp[pidx(j - 1, j - 1)] = sm.sc[1];
-        }
-        const double piv = Mp[pidx(j, j)];
-        __syncthreads();  // everyone read piv / finished scaling before sc is rewritten
-        if (!(piv > 0.0)) { fail = 1; break; }
-        const double ljj = sqrt(piv), rs = 1.0 / ljj;
-        // trailing update over rows i > j, cols c in (j, i]
-        const int m1 = d - j - 1;
-        const int tri = m1 * (m1 + 1) / 2;
-        for (int x = tid; x < tri; x += nth) {
-          int r = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
-          while (r * (r + 1) / 2 > x) --r;
-          while ((r + 1) * (r + 2) / 2 <= x) ++r;
-          const int c = x - r * (r + 1) / 2;
-          const int i = j + 1 + r, cc2 = j + 1 + c;
-          Mp[pidx(i, cc2)] -= (Mp[pidx(i, j)] * rs) * (Mp[pidx(cc2, j)] * rs);
-        }
-        if (tid == 0) { sm.sc[0] = rs; sm.sc[1] = ljj; }
-        __syncthreads();
-        if (j == d - 1) {
-          if (tid == 0) Mp[pidx(j, j)] = ljj;
+      // Cholesky of M (right-looking, potrf semantics).  Column j is scaled
+      // into a contiguous buffer (colj) so the trailing update runs warp per
+      // row over contiguous packed storage; rdiag keeps 1 / L_jj.
+      double* colj = sm.tmp;
+      double* rdiag = sm.f1;  // f1 is dead once rhs is formed
+      {
+        const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
+        for (int j = 0; j < d; ++j) {
+          const double piv = Mp[pidx(j, j)];
+          if (!(piv > 0.0)) { fail = 1; break; }  // uniform: every thread read the same value
+          const double ljj = sqrt(piv), rs = 1.0 / ljj;
+          for (int i = j + 1 + tid; i < d; i += nth) {
+            const double c = Mp[pidx(i, j)] * rs;
+            colj[i] = c;
+            Mp[pidx(i, j)] = c;
+          }
+          if (tid == 0) { Mp[pidx(j, j)] = ljj; rdiag[j] = rs; }
+          __syncthreads();
+          for (int i = j + 1 + wid; i < d; i += nwp) {
+            const double li = colj[i];
+            const int base = i * (i + 1) / 2;
+            for (int c = j + 1 + lane; c <= i; c += 32) Mp[base + c] -= li * colj[c];
+          }
           __syncthreads();
         }
       }
       if (!fail) {
-        // forward / backward substitution (warp 0)
-        if (tid < 32) {
-          const int lane = tid;
-          for (int j = 0; j < d; ++j) {
-            __syncwarp();
-            const double yj = sm.rhs[j] / Mp[pidx(j, j)];
-            __syncwarp();
-            if (lane == 0) sm.rhs[j] = yj;
-            for (int i = j + 1 + lane; i < d; i += 32) sm.rhs[i] -= Mp[pidx(i, j)] * yj;
+        // blocked triangular solves: the 32-row diagonal triangles by warp 0
+        // with shuffles, the off-diagonal updates by the whole block
+        const int lane = tid & 31;
+        for (int J = 0; J < d; J += 32) {  // forward: L y = rhs
+          const int JB = min(32, d - J);
+          if (tid < 32) {
+            double x = lane < JB ? sm.rhs[J + lane] : 0.0;
+            for (int jj = 0; jj < JB; ++jj) {
+              const double yj = __shfl_sync(0xffffffffu, x, jj) * rdiag[J + jj];
+              if (lane == jj) x = yj;
+              else if (lane > jj && lane < JB) x -= Mp[pidx(J + lane, J + jj)] * yj;
+            }
+            if (lane < JB) sm.rhs[J + lane] = x;
           }
-          __syncwarp();
-          for (int j = d - 1; j >= 0; --j) {
-            __syncwarp();
-            const double xj = sm.rhs[j] / Mp[pidx(j, j)];
-            __syncwarp();
-            if (lane == 0) sm.ds[j] = xj;
-            for (int i = lane; i < j; i += 32) sm.rhs[i] -= Mp[pidx(j, i)] * xj;
+          __syncthreads();
+          for (int i = J + JB + tid; i < d; i += nth) {
+            const int base = i * (i + 1) / 2 + J;
+            double s = 0.0;
+            for (int jj = 0; jj < JB; ++jj) s = fma(Mp[base + jj], sm.rhs[J + jj], s);
+            sm.rhs[i] -= s;
           }
+          __syncthreads();
         }
-        __syncthreads();
+        for (int Jend = d; Jend > 0; Jend -= 32) {  // backward: L^T x = y
+          const int J = max(0, Jend - 32), JB = Jend - J;
+          if (tid < 32) {
+            double x = lane < JB ? sm.rhs[J + lane] : 0.0;
+            for (int jj = JB - 1; jj >= 0; --jj) {
+              const double xj = __shfl_sync(0xffffffffu, x, jj) * rdiag[J + jj];
+              if (lane == jj) x = xj;
+              else if (lane < jj) x -= Mp[pidx(J + jj, J + lane)] * xj;
+            }
+            if (lane < JB) sm.ds[J + lane] = x;
+          }
+          __syncthreads();
+          for (int i = tid; i < J; i += nth) {
+            double s = 0.0;
+            for (int jj = 0; jj < JB; ++jj) s = fma(Mp[pidx(J + jj, i)], sm.ds[J + jj], s);
+            sm.rhs[i] -= s;
+          }
+          __syncthreads();
+        }
         // E ds = svec((H D G + G D H)/2), D = smat(ds), G = T
         blk_smat(sm.ds, k, d, sm, sm.W1);
         __syncthreads();

@@ -16,6 +16,7 @@ enum WsSlot {
   WS_LZ_FLAGS = 15,
   WS_LZ_OUT = 16,
   WS_LZ_TMP = 17,
+  WS_LZ_PROF = 18,
   WS_SMALL = 20,
   WS_RED = 21,
   WS_IPM = 30,

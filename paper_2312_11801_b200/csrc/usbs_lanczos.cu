@@ -78,7 +78,25 @@ struct LzArgs {
   int first_from_q;  // 1: q_{j0} is materialised in Q (start/restart/reseed)
   double* vecs_out;  // n x k_c row-major (written when done)
   int64_t ldvecs;
+  unsigned long long* prof;  // optional phase timer accumulators (ns), block 0
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// phase timers (block 0, thread 0): 0 phase A work, 1 grid barriers,
+// 2 phase B work, 3 phase C work, 4 end-of-cycle, 5 Rayleigh-Ritz, 6 restart
+#define LZ_MARK(slot)                                   \
+  do {                                                  \
+    if (a.prof && b == 0 && tid == 0) {                 \
+      unsigned long long _t = gtimer();                 \
+      lz_acc[slot] += _t - lz_last;                     \
+      lz_last = _t;                                     \
+    }                                                   \
+  } while (0)
 
 template <int LG>
 __device__ __forceinline__ double group_sum(double v) {
@@ -144,6 +162,18 @@ __device__ __forceinline__ void column_reduce(const LzArgs& a, int j, int r0, in
   __syncthreads();
 }
 
+// out[t] = sum_{b < G} P[b*64 + t] for t < cols: one warp per column, lanes
+// stride over blocks (a few independent L2 loads each), fixed-order shuffles
+__device__ __forceinline__ void cross_block_sum(const double* P, int G, int cols, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = warp; t < cols; t += nw) {
+    double s = 0.0;
+    for (int bb = lane; bb < G; bb += 32) s += P[(int64_t)bb * 64 + t];
+    s = warp_sum(s);
+    if (lane == 0) out[t] = s;
+  }
+}
+
 template <int LG, int NH>
 __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -180,6 +210,8 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   bool from_q = a.first_from_q != 0;
   bool pending = false;  // w''_{m-1} waits in W[wb^1] to become q_m
   int converged = 0;
+  unsigned long long lz_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long lz_last = (a.prof && b == 0 && tid == 0) ? gtimer() : 0ull;
 
   for (; cycle <= a.max_restarts; ++cycle) {
     for (int j = jstart; j < m; ++j) {
@@ -239,7 +271,9 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.flags[F_NONFINITE], 1);
         for (int t = tid; t <= j; t += nth) a.P1[(int64_t)b * 64 + t] = red[t];
       }
+      LZ_MARK(0);
       grid.sync();
+      LZ_MARK(1);
       // ------------------------------------------------------------ phase B
       if (*(volatile int*)&a.flags[F_NONFINITE]) {
         if (b == 0 && tid == 0) {
@@ -248,11 +282,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         }
         return;
       }
-      for (int t = tid; t <= j; t += nth) {
-        double s = 0.0;
-        for (int bb = 0; bb < G; ++bb) s += a.P1[(int64_t)bb * 64 + t];
-        cvec[t] = s;
-      }
+      cross_block_sum(a.P1, G, j + 1, cvec);
       __syncthreads();
       column_reduce<NH>(a, j, r0, r1, wred, red, [&](int i, double (&q)[NH][32]) {
         double s = 0.0;
@@ -266,13 +296,11 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         return w;
       });
       for (int t = tid; t <= j; t += nth) a.P2[(int64_t)b * 64 + t] = red[t];
+      LZ_MARK(2);
       grid.sync();
+      LZ_MARK(1);
       // ------------------------------------------------------------ phase C
-      for (int t = tid; t <= j; t += nth) {
-        double s = 0.0;
-        for (int bb = 0; bb < G; ++bb) s += a.P2[(int64_t)bb * 64 + t];
-        c2vec[t] = s;
-      }
+      cross_block_sum(a.P2, G, j + 1, c2vec);
       __syncthreads();
       {
         double ss = 0.0;
@@ -299,11 +327,14 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         for (int t = 0; t <= j; ++t) mx = fmax(mx, fabs(cvec[t]));
         misc[0] = fmax(1.0, mx);
       }
+      LZ_MARK(3);
       grid.sync();
-      if (tid == 0) {
+      LZ_MARK(1);
+      if (tid < 32) {
         double s = 0.0;
-        for (int bb = 0; bb < G; ++bb) s += a.P3[bb];
-        misc[1] = sqrt(s);
+        for (int bb = tid; bb < G; bb += 32) s += a.P3[bb];
+        s = warp_sum(s);
+        if (tid == 0) misc[1] = sqrt(s);
       }
       __syncthreads();
       beta = misc[1];
@@ -337,10 +368,13 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       pending = false;
     }
     grid.sync();
+    LZ_MARK(4);
     // Rayleigh-Ritz (every block, identical)
     for (int x = tid; x < m * m; x += nth) js.A[x] = a.H[(x / m) * M1 + (x % m)];
     __syncthreads();
-    jacobi_eigh(m, js, thetaS, Ys, m);
+    const int sweeps = jacobi_eigh(m, js, thetaS, Ys, m);
+    LZ_MARK(5);
+    if (a.prof && b == 0 && tid == 0) lz_acc[7] += sweeps;
     const double beta_last = a.H[m * M1 + (m - 1)];
     if (tid == 0) {
       bool ok = true;
@@ -387,8 +421,11 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       for (int u = tid; u < ell; u += nth) a.H[u * M1 + u] = thetaS[u];
       __syncthreads();
     }
+    LZ_MARK(6);
   }
   // ---------------------------------------------------------------- output
+  if (a.prof && b == 0 && tid == 0)
+    for (int s = 0; s < 8; ++s) a.prof[s] += lz_acc[s];
   for (int i = r0 + tid; i < r1; i += nth) {
     double qrow[64];
     for (int t = 0; t < m; ++t) qrow[t] = a.Q[(int64_t)t * a.ldq + i];
@@ -555,6 +592,17 @@ static void lz_dispatch(usbs_ctx* ctx, LzArgs& a, int G, int LG, size_t smem) {
 
 using namespace usbs;
 
+// Phase timers accumulated by k_lanczos when USBS_LZ_PROF is set (ns):
+// [phase A, grid barriers, phase B, phase C, end of cycle, Rayleigh-Ritz, restart, -]
+extern "C" usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* out, int reset) {
+  USBS_API_BEGIN
+  auto* p = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 8 * sizeof(unsigned long long));
+  USBS_CUDA(cudaMemcpyAsync(out, p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  USBS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  USBS_API_END
+}
+
 extern "C" usbs_status usbs_small_eigh(usbs_ctx* ctx, int k, const double* a, double* vals, double* vecs) {
   USBS_API_BEGIN
   if (k < 1 || k > 64) fail(USBS_ERR_SHAPE, "small_eigh supports 1 <= k <= 64");
@@ -634,6 +682,15 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   a.vecs_out = vecs_dev; a.ldvecs = ldvecs;
   a.cycle0 = 0; a.ell0 = 0; a.j0 = 0; a.restarts0 = 0; a.nhist0 = 0; a.matvecs0 = 0; a.wbuf0 = 0;
   a.beta_prev = 1.0; a.first_from_q = 1;
+  a.prof = nullptr;
+  if (getenv("USBS_LZ_PROF")) {
+    static bool zeroed = false;
+    a.prof = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 8 * sizeof(unsigned long long));
+    if (!zeroed) {
+      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 8 * sizeof(unsigned long long), st));
+      zeroed = true;
+    }
+  }
 
   const int nw = (NH == 1 ? 512 : 256) / 32;
   size_t smem = (size_t)(nw * 32 * NH + 64 * 3 + 8 + 64 + m * m + 4 * m * m + 64 * 2 + 32) * sizeof(double) +

@@ -347,6 +347,7 @@ class DeviceSolver:
         self.evecs = rt.empty(k, k)
         self.lamc = rt.empty(max(self.k_c, 1))
         self.ident = rt.upload(np.eye(max(k, 1)))
+        self.lz_probe = None  # list -> (start, end, restarts, matvecs) per Lanczos call
 
     # ------------------------------------------------------------ helpers
     def _fetch(self, *tensors):
@@ -359,7 +360,16 @@ class DeviceSolver:
             self.dp.assemble(y_dev)
         op = DeviceLinOp(self.dp, which)
         inner, rst, tol = self.lz
-        return lanczos_top(op, self.k_c, inner, rst, tol, self.seed, out=self.vecs)
+        probe = self.lz_probe
+        if probe is not None:  # bench: CUDA events on the launching stream around the kernel
+            ev0 = self.rt.torch.cuda.Event(enable_timing=True)
+            ev1 = self.rt.torch.cuda.Event(enable_timing=True)
+            ev0.record(self.rt.stream)
+        res = lanczos_top(op, self.k_c, inner, rst, tol, self.seed, out=self.vecs)
+        if probe is not None:
+            ev1.record(self.rt.stream)
+            probe.append((ev0, ev1, res.restarts, res.matvecs))
+        return res
 
     def completion(self, basis, k, tag):
         """_completion_columns (bundle.py:264-282) with host PCG64 vectors."""
@@ -445,8 +455,9 @@ class DeviceSolver:
             eng.rowgemm(work[:, piv:piv + 1], self.ident[:1, :1], q)
             if nb:
                 B = basis[:, :nb]
-                eng.gram(B, q, coef[:nb, :1])
-                eng.rowgemm(B, coef[:nb, :1], q, alpha=-1.0, beta=1.0, Y0=q)
+                cv = coef.view(-1)[:nb].view(nb, 1)  # gram writes a contiguous block
+                eng.gram(B, q, cv)
+                eng.rowgemm(B, cv, q, alpha=-1.0, beta=1.0, Y0=q)
             eng.dot_into(q.view(-1), q.view(-1), red)
             nq = math.sqrt(float(red[0].item()))
             if nq <= thresh:

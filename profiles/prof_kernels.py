@@ -1,0 +1,110 @@
+"""Small driver for ncu captures of individual kernels (not a benchmark).
+
+    python profiles/prof_kernels.py lanczos   # k_lanczos on C2 slack operator
+    python profiles/prof_kernels.py ipm       # k_ipm (d = 66) on a C2-like subproblem
+    python profiles/prof_kernels.py spmm      # K1 on C4 (n = 1e6), k = 1 and 11
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main(which):
+    import torch
+
+    from paper_2312_11801_b200 import eigen, instances as inst, subproblem
+    from paper_2312_11801_b200.runtime import DeviceProblem
+
+    if which == "lanczos":
+        p = inst.baseline_config("C2").problem
+        dp = DeviceProblem(p)
+        y = np.random.default_rng(1234).standard_normal(p.m) * 1e-3
+        import ctypes as C
+        import os
+        import time
+        for _ in range(4):
+            r = eigen.lanczos_top(eigen.dual_slack_operator(dp, y), 10, seed=0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = 10
+        for _ in range(reps):
+            r = eigen.lanczos_top(eigen.dual_slack_operator(dp, y), 10, seed=0)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / reps
+        print("lanczos", r.eigenvalues[0], r.restarts, r.matvecs, f"{dt * 1e3:.3f} ms/call",
+              f"{dt / r.matvecs * 1e6:.2f} us/step", "blocks", dp.info().lanczos_blocks)
+        if os.environ.get("USBS_LZ_PROF"):
+            out = (C.c_uint64 * 8)()
+            dp.rt.lib.usbs_lanczos_profile(dp.rt.h, out, 1)
+            names = ["phaseA", "barriers", "phaseB", "phaseC", "endcycle", "rayleigh_ritz", "restart", "-"]
+            tot = sum(out[:7])
+            for nm, v in zip(names, out[:7]):
+                print(f"  {nm:14s} {v / 1e6 / (reps + 4):8.3f} ms/call  {100 * v / max(tot, 1):5.1f}%")
+            print(f"  jacobi sweeps per Rayleigh-Ritz: {out[7] / ((reps + 4) * (r.restarts + 1)):.1f}")
+        if os.environ.get("USBS_LZ_SWEEP"):
+            for g in (8, 16, 32, 64, 148):
+                os.environ["USBS_LZ_BLOCKS"] = str(g)
+                dpg = DeviceProblem(p)
+                eigen.lanczos_top(eigen.dual_slack_operator(dpg, y), 10, seed=0)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for _ in range(5):
+                    r = eigen.lanczos_top(eigen.dual_slack_operator(dpg, y), 10, seed=0)
+                torch.cuda.synchronize()
+                dt = (time.perf_counter() - t0) / 5
+                print(f"  G={g:4d}: {dt * 1e3:.3f} ms/call")
+    elif which == "ipm":
+        rng = np.random.default_rng(11)
+        k = 11
+        d = k * (k + 1) // 2
+        a = rng.standard_normal((d + 5, d))
+        z = rng.standard_normal(d + 5)
+
+        class Q:
+            pass
+
+        q = Q()
+        q.quad_ss, q.quad_s_eta, q.quad_eta = a.T @ a / (d + 5), a.T @ z / (d + 5), float(z @ z / (d + 5))
+        q.lin_s, q.lin_eta, q.has_eta, q.k = rng.standard_normal(d), float(rng.standard_normal()), True, k
+        import time
+        for _ in range(4):
+            r = subproblem.ipm_quad(q)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(10):
+            r = subproblem.ipm_quad(q)
+        dt = (time.perf_counter() - t0) / 10
+        print("ipm d=66", r.value, r.newton_iters, f"{dt * 1e3:.3f} ms/solve (incl. host copies)")
+        k = 20
+        d = k * (k + 1) // 2
+        a = rng.standard_normal((d + 5, d))
+        z = rng.standard_normal(d + 5)
+        q.quad_ss, q.quad_s_eta, q.quad_eta = a.T @ a / (d + 5), a.T @ z / (d + 5), float(z @ z / (d + 5))
+        q.lin_s, q.lin_eta, q.k = rng.standard_normal(d), float(rng.standard_normal()), k
+        r = subproblem.ipm_quad(q)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            r = subproblem.ipm_quad(q)
+        dt = (time.perf_counter() - t0) / 3
+        print("ipm d=210", r.value, r.newton_iters, f"{dt * 1e3:.3f} ms/solve (incl. host copies)")
+    elif which == "spmm":
+        p = inst.baseline_config("C4").problem
+        dp = DeviceProblem(p)
+        dp.assemble(dp.rt.upload(np.random.default_rng(1).standard_normal(p.m) * 1e-3))
+        for k in (1, 11):
+            V = dp.rt.upload(np.random.default_rng(2).standard_normal((p.n, k)))
+            for _ in range(3):
+                dp.apply(1, V)
+        torch.cuda.synchronize()
+        print("spmm done")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "lanczos")
