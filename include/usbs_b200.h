@@ -136,6 +136,9 @@ usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const double* Q11_
                            const double* warm_state_dev, double* state_out_dev, double* result_dev,
                            const double* opts);
 int usbs_ipm_state_len(int k);
+/* Phase timers of the IPM kernel (ns, 10 slots, accumulated while the
+ * environment variable USBS_IPM_PROF is set); reset != 0 zeroes them. */
+usbs_status usbs_ipm_profile(usbs_ctx* ctx, unsigned long long* out_host, int reset);
 
 /* ---- K5: constraint image A(V S V^T) ------------------------------------
  * out = beta * base + A(V S V^T); S k x k (s_is_diag = 0) or its diagonal

@@ -41,7 +41,20 @@ struct IpmArgs {
   double* result;      // [value, newton_iters, exact, eta_opt, failures]
   double* gM;          // global scratch for M when d > SMEM_D
   IpmOpts o;
+  unsigned long long* prof;  // optional phase timers (ns), thread 0
 };
+
+// phase timers: 0 stationarity/exit test, 1 S^-1, 2 rd/rhs, 3 M build,
+// 4 Cholesky, 5 solves, 6 E ds / scalar directions, 7 line search, 8 update
+#define IPM_MARK(slot)                                             \
+  do {                                                             \
+    if (a.prof && tid == 0) {                                      \
+      unsigned long long _t;                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));       \
+      ipm_acc[slot] += _t - ipm_last;                              \
+      ipm_last = _t;                                               \
+    }                                                              \
+  } while (0)
 
 // state layout: S (k*k), T (k*k), eta, zeta, omega, mu, has_eta, k, valid
 __host__ __device__ inline int state_len(int k) { return 2 * k * k + 7; }
@@ -85,8 +98,8 @@ __device__ void warp_chol(double* W, int k, int* flg, int slot) {
     for (int j = 0; j < k; ++j) {
       double piv = W[j * k + j];
       if (!(piv > 0.0)) { ok = 0; break; }
-      double ljj = sqrt(piv);
-      double r = 1.0 / ljj;
+      const double r = rsqrt(piv);
+      const double ljj = piv * r;
       __syncwarp();
       if (lane == 0) W[j * k + j] = ljj;
       if (lane > j && lane < k) W[lane * k + j] *= r;
@@ -262,6 +275,9 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   const double coeff_scale = 1.0 + fmax(fmax(fmax(hmax, fabs(h2)), qmax), fmax(gmax, fabs(q22e)));
 
   int exact = 0, failures = 0, it = 0;
+  unsigned long long ipm_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ipm_last = 0;
+  if (a.prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ipm_last));
   const double SQ2 = 1.4142135623730951;
   for (it = 1; it <= a.o.max_newton; ++it) {
     // ---- stationarity (subqp.py:210-219)
@@ -286,6 +302,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       it -= 1;
       break;
     }
+    IPM_MARK(0);
     // ---- newton_direction (subqp.py:222-265)
     int fail = 0;
     // H = S^-1 via Cholesky: S = L L^T, Linv by forward substitution, H = Linv^T Linv
@@ -295,12 +312,14 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     if (!sm.flg[2]) fail = 1;
     if (!fail) {
       // X1 = L^-1 (lower): column c solved by thread c
+      for (int r = tid; r < k; r += nth) sm.rd[r] = 1.0 / sm.W1[r * k + r];  // rd is free until rd is formed
+      __syncthreads();
       for (int c = tid; c < k; c += nth) {
-        for (int r = 0; r < k; ++r) sm.X1[r * k + c] = 0.0;
+        for (int r = 0; r < c; ++r) sm.X1[r * k + c] = 0.0;
         for (int r = c; r < k; ++r) {
           double s = (r == c) ? 1.0 : 0.0;
           for (int u = c; u < r; ++u) s -= sm.W1[r * k + u] * sm.X1[u * k + c];
-          sm.X1[r * k + c] = s / sm.W1[r * k + r];
+          sm.X1[r * k + c] = s * sm.rd[r];
         }
       }
       __syncthreads();
@@ -320,6 +339,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       const double sigma = 1.0 - tr - eta;
       const double rc = mu / omega - sigma;
       const double kappa1 = sigma / omega;
+      IPM_MARK(1);
       // rd = mu svec(H) - t
       blk_svec(sm.H, k, d, sm, sm.rd);
       __syncthreads();
@@ -340,6 +360,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
               sm.f1[p] + sm.rd[p];
         sm.rhs[p] = r;
       }
+      IPM_MARK(2);
       // M (packed lower): Q11 + E + low-rank; warp per row p, lanes over q <= p
       {
         const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
@@ -365,32 +386,87 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
         }
       }
       __syncthreads();
-      // Cholesky of M (right-looking, potrf semantics).  Column j is scaled
-      // into a contiguous buffer (colj) so the trailing update runs warp per
-      // row over contiguous packed storage; rdiag keeps 1 / L_jj.
-      double* colj = sm.tmp;
+      IPM_MARK(3);
+      // Blocked Cholesky of M (potrf semantics: fails on a pivot <= 0 or NaN).
+      // Panels of CB columns are factorised by warp 0 (lanes over rows,
+      // __syncwarp only); the trailing update is a SYRK over 4x4 register
+      // tiles by the whole block.  rdiag keeps 1 / L_jj for the solves.
       double* rdiag = sm.f1;  // f1 is dead once rhs is formed
       {
-        const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
-        for (int j = 0; j < d; ++j) {
-          const double piv = Mp[pidx(j, j)];
-          if (!(piv > 0.0)) { fail = 1; break; }  // uniform: every thread read the same value
-          const double ljj = sqrt(piv), rs = 1.0 / ljj;
-          for (int i = j + 1 + tid; i < d; i += nth) {
-            const double c = Mp[pidx(i, j)] * rs;
-            colj[i] = c;
-            Mp[pidx(i, j)] = c;
+        constexpr int CB = 16;
+        for (int J = 0; J < d && !fail; J += CB) {
+          const int JB = min(CB, d - J);
+          if (tid < 32) {
+            const int lane = tid;
+            int ok = 1;
+            for (int jj = 0; jj < JB; ++jj) {
+              const int c = J + jj;
+              __syncwarp();
+              const double piv = Mp[pidx(c, c)];
+              if (!(piv > 0.0)) { ok = 0; break; }
+              const double r = rsqrt(piv);
+              __syncwarp();
+              if (lane == 0) { Mp[pidx(c, c)] = piv * r; rdiag[c] = r; }
+              for (int i = c + 1 + lane; i < d; i += 32) Mp[pidx(i, c)] *= r;
+              __syncwarp();
+              const int cmax = J + JB - 1;
+              if (c < cmax)
+                for (int i = c + 1 + lane; i < d; i += 32) {
+                  const int bi = i * (i + 1) / 2;
+                  const double li = Mp[bi + c];
+                  const int cend = min(i, cmax);
+                  for (int c2 = c + 1; c2 <= cend; ++c2) Mp[bi + c2] -= li * Mp[pidx(c2, c)];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) sm.flg[5] = ok;
           }
-          if (tid == 0) { Mp[pidx(j, j)] = ljj; rdiag[j] = rs; }
           __syncthreads();
-          for (int i = j + 1 + wid; i < d; i += nwp) {
-            const double li = colj[i];
-            const int base = i * (i + 1) / 2;
-            for (int c = j + 1 + lane; c <= i; c += 32) Mp[base + c] -= li * colj[c];
+          if (!sm.flg[5]) { fail = 1; break; }
+          // trailing SYRK: rows/cols >= J + JB
+          const int T0 = J + JB, T = d - T0;
+          if (T > 0) {
+            const int nt = (T + 3) / 4, ntiles = nt * (nt + 1) / 2;
+            for (int x = tid; x < ntiles; x += nth) {
+              int R = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+              while (R * (R + 1) / 2 > x) --R;
+              while ((R + 1) * (R + 2) / 2 <= x) ++R;
+              const int Cc = x - R * (R + 1) / 2;
+              const int i0 = T0 + 4 * R, c0 = T0 + 4 * Cc;
+              double acc[4][4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+              int bi[4], bc[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int ii = min(i0 + u, d - 1), cc2 = min(c0 + u, d - 1);
+                bi[u] = ii * (ii + 1) / 2 + J;
+                bc[u] = cc2 * (cc2 + 1) / 2 + J;
+              }
+              for (int t = 0; t < JB; ++t) {
+                double li[4], lc[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { li[u] = Mp[bi[u] + t]; lc[u] = Mp[bc[u] + t]; }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                  for (int v = 0; v < 4; ++v) acc[u][v] = fma(li[u], lc[v], acc[u][v]);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                  const int ii = i0 + u, cc2 = c0 + v;
+                  if (ii < d && cc2 <= ii) Mp[pidx(ii, cc2)] -= acc[u][v];
+                }
+            }
           }
           __syncthreads();
         }
       }
+      IPM_MARK(4);
       if (!fail) {
         // blocked triangular solves: the 32-row diagonal triangles by warp 0
         // with shuffles, the off-diagonal updates by the whole block
@@ -434,6 +510,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           }
           __syncthreads();
         }
+        IPM_MARK(5);
         // E ds = svec((H D G + G D H)/2), D = smat(ds), G = T
         blk_smat(sm.ds, k, d, sm, sm.W1);
         __syncthreads();
@@ -460,6 +537,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           domega = -f2 + re - gds - kappa2 * deta;
         }
         __syncthreads();
+        IPM_MARK(6);
         // ---- line_search_feasible (subqp.py:294-343)
         int finite = 1;
         for (int p = tid; p < d; p += nth)
@@ -505,6 +583,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           if (!found) {
             fail = 1;
           } else {
+            IPM_MARK(7);
             // ---- step + barrier_update (subqp.py:415-422, 346-350)
             failures = 0;
             for (int x = tid; x < kk; x += nth) {
@@ -520,6 +599,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
             const double gamma = delta <= 0.2 ? 1.0 : 0.5 - 0.4 * delta * delta;
             const double est = blk_compl(sm, k, eta, zeta, omega, has_eta) / (2.0 * pairs);
             mu = fmin(mu, gamma * est);
+            IPM_MARK(8);
             continue;
           }
         }
@@ -532,6 +612,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     mu = fmax(mu * 10.0, 10.0 * a.o.mu_tol);
   }
   if (it > a.o.max_newton) it = a.o.max_newton;
+  if (a.prof && tid == 0)
+    for (int s = 0; s < 10; ++s) a.prof[s] += ipm_acc[s];
   // ---- objective (subqp.py:200-207) and outputs
   blk_svec(sm.S, k, d, sm, sm.s);
   __syncthreads();
@@ -603,6 +685,15 @@ extern "C" usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const d
   a.state = state_out;
   a.result = result;
   a.gM = a.d > SMEM_D ? (double*)ctx->ws.get(WS_IPM, (size_t)a.d * (a.d + 1) / 2 * sizeof(double)) : nullptr;
+  a.prof = nullptr;
+  if (getenv("USBS_IPM_PROF")) {
+    static bool zeroed = false;
+    a.prof = (unsigned long long*)ctx->ws.get(WS_IPM + 1, 16 * sizeof(unsigned long long));
+    if (!zeroed) {
+      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 16 * sizeof(unsigned long long), ctx->stream));
+      zeroed = true;
+    }
+  }
   // IpmOptions defaults (subqp.py:150-162) unless given:
   // [mu_tol, kkt_tol, max_newton, step_frac, backtrack, min_step, max_step_failures, warm_blend]
   double o[8] = {1e-11, 1e-6, 100, 0.99, 0.8, 1e-12, 6, 0.2};
@@ -615,3 +706,13 @@ extern "C" usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const d
 }
 
 extern "C" int usbs_ipm_state_len(int k) { return state_len(k); }
+
+// Phase timers of k_ipm (ns) accumulated while USBS_IPM_PROF is set.
+extern "C" usbs_status usbs_ipm_profile(usbs_ctx* ctx, unsigned long long* out, int reset) {
+  USBS_API_BEGIN
+  auto* p = (unsigned long long*)ctx->ws.get(WS_IPM + 1, 16 * sizeof(unsigned long long));
+  USBS_CUDA(cudaMemcpyAsync(out, p, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  USBS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 16 * sizeof(unsigned long long), ctx->stream));
+  USBS_API_END
+}

@@ -32,6 +32,7 @@
 
 #include "usbs_common.cuh"
 #include "usbs_jacobi.cuh"
+#include "usbs_tridiag.cuh"
 #include "usbs_kernels.cuh"
 
 namespace cg = cooperative_groups;
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   js.red = js.cmate + 64;
   js.mate = (int*)(js.red + 32);
   js.flag = js.mate + 64;
+  js.ptab = (unsigned char*)(js.flag + 4);
 
   int cycle = a.cycle0, ell = a.ell0, jstart = a.j0, restarts = a.restarts0, nhist = a.nhist0;
   int matvecs = a.matvecs0, wb = a.wbuf0;
@@ -372,9 +374,25 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
     // Rayleigh-Ritz (every block, identical)
     for (int x = tid; x < m * m; x += nth) js.A[x] = a.H[(x / m) * M1 + (x % m)];
     __syncthreads();
-    const int sweeps = jacobi_eigh(m, js, thetaS, Ys, m);
+    // only the nw leading Ritz pairs are used: theta/Y[:, :ell] for the
+    // restart, theta/Y[:, :k_c] for the output and the residual test
+    const int ell_next = max(1, min(a.k_c + 3, m - 2));
+    const int nwant = min(m, max(ell_next, a.k_c));
+    {
+      TriSmem ts;
+      ts.A = js.A;
+      ts.Q = js.V;
+      ts.Z = js.A2;
+      ts.v = (double*)(js.ptab + JAC_PTAB_BYTES);
+      ts.p = ts.v + 64;
+      ts.dd = ts.p + 64;
+      ts.ee = ts.dd + 64;
+      ts.lam = ts.ee + 64;
+      ts.red = ts.lam + 64;
+      ts.iw = (int*)(ts.red + 64);
+      rr_topk(m, nwant, cycle == 0 ? 1 : 0, ts, thetaS, Ys, m, (a.prof && b == 0) ? a.prof + 8 : nullptr);
+    }
     LZ_MARK(5);
-    if (a.prof && b == 0 && tid == 0) lz_acc[7] += sweeps;
     const double beta_last = a.H[m * M1 + (m - 1)];
     if (tid == 0) {
       bool ok = true;
@@ -387,11 +405,10 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
     }
     __syncthreads();
     if (b == 0) {
-      for (int u = tid; u < m; u += nth) {
+      for (int u = tid; u < nwant; u += nth) {
         a.theta[u] = thetaS[u];
         a.res[u] = fabs(beta_last * Ys[(m - 1) * m + u]);
       }
-      for (int x = tid; x < m * m; x += nth) a.Y[x] = Ys[x];
       if (tid == 0) a.hist[nhist] = thetaS[0];
     }
     ++nhist;
@@ -502,6 +519,7 @@ __global__ void k_dense_eigh(int n, const int* __restrict__ rowptr, const int* _
   js.red = js.cmate + 64;
   js.mate = (int*)(js.red + 32);
   js.flag = js.mate + 64;
+  js.ptab = (unsigned char*)(js.flag + 4);
   for (int x = threadIdx.x; x < n * n; x += blockDim.x) js.A[x] = 0.0;
   __syncthreads();
   int bad = 0;
@@ -539,6 +557,7 @@ __global__ void k_small_eigh(int k, const double* __restrict__ a, double* vals_o
   js.red = js.cmate + 64;
   js.mate = (int*)(js.red + 32);
   js.flag = js.mate + 64;
+  js.ptab = (unsigned char*)(js.flag + 4);
   for (int x = threadIdx.x; x < k * k; x += blockDim.x) js.A[x] = a[x];
   __syncthreads();
   jacobi_eigh(k, js, vals, vecs, k);
@@ -547,7 +566,7 @@ __global__ void k_small_eigh(int k, const double* __restrict__ a, double* vals_o
 }
 
 static size_t eigh_smem(int n) {
-  return (size_t)(5 * n * n + 64 * 3 + 32) * sizeof(double) + 65 * sizeof(int) + 64;
+  return (size_t)(5 * n * n + 64 * 3 + 32) * sizeof(double) + 68 * sizeof(int) + JAC_PTAB_BYTES + 64;
 }
 
 void launch_small_eigh(usbs_ctx* ctx, int k, const double* a, double* vals, double* vecs) {
@@ -596,10 +615,10 @@ using namespace usbs;
 // [phase A, grid barriers, phase B, phase C, end of cycle, Rayleigh-Ritz, restart, -]
 extern "C" usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* out, int reset) {
   USBS_API_BEGIN
-  auto* p = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 8 * sizeof(unsigned long long));
-  USBS_CUDA(cudaMemcpyAsync(out, p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  auto* p = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 16 * sizeof(unsigned long long));
+  USBS_CUDA(cudaMemcpyAsync(out, p, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   USBS_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 16 * sizeof(unsigned long long), ctx->stream));
   USBS_API_END
 }
 
@@ -685,16 +704,16 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   a.prof = nullptr;
   if (getenv("USBS_LZ_PROF")) {
     static bool zeroed = false;
-    a.prof = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 8 * sizeof(unsigned long long));
+    a.prof = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 16 * sizeof(unsigned long long));
     if (!zeroed) {
-      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 8 * sizeof(unsigned long long), st));
+      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 16 * sizeof(unsigned long long), st));
       zeroed = true;
     }
   }
 
   const int nw = (NH == 1 ? 512 : 256) / 32;
   size_t smem = (size_t)(nw * 32 * NH + 64 * 3 + 8 + 64 + m * m + 4 * m * m + 64 * 2 + 32) * sizeof(double) +
-                65 * sizeof(int) + 64;
+                68 * sizeof(int) + JAC_PTAB_BYTES + (6 * 64) * sizeof(double) + 64 * sizeof(int) + 64;
   int64_t ctr = 0;
   int* hf = ctx->pinned_i;
   for (;;) {

@@ -40,13 +40,15 @@ def main(which):
         print("lanczos", r.eigenvalues[0], r.restarts, r.matvecs, f"{dt * 1e3:.3f} ms/call",
               f"{dt / r.matvecs * 1e6:.2f} us/step", "blocks", dp.info().lanczos_blocks)
         if os.environ.get("USBS_LZ_PROF"):
-            out = (C.c_uint64 * 8)()
+            out = (C.c_uint64 * 12)()
             dp.rt.lib.usbs_lanczos_profile(dp.rt.h, out, 1)
             names = ["phaseA", "barriers", "phaseB", "phaseC", "endcycle", "rayleigh_ritz", "restart", "-"]
             tot = sum(out[:7])
             for nm, v in zip(names, out[:7]):
                 print(f"  {nm:14s} {v / 1e6 / (reps + 4):8.3f} ms/call  {100 * v / max(tot, 1):5.1f}%")
-            print(f"  jacobi sweeps per Rayleigh-Ritz: {out[7] / ((reps + 4) * (r.restarts + 1)):.1f}")
+            nrr = (reps + 4) * (r.restarts + 1)
+            for nm, v in zip(["householder", "bisection", "inverse-it", "QZ"], out[8:12]):
+                print(f"    rr {nm:12s} {v / 1e3 / nrr:8.2f} us per Rayleigh-Ritz")
         if os.environ.get("USBS_LZ_SWEEP"):
             for g in (8, 16, 32, 64, 148):
                 os.environ["USBS_LZ_BLOCKS"] = str(g)
@@ -81,6 +83,18 @@ def main(which):
             r = subproblem.ipm_quad(q)
         dt = (time.perf_counter() - t0) / 10
         print("ipm d=66", r.value, r.newton_iters, f"{dt * 1e3:.3f} ms/solve (incl. host copies)")
+        import ctypes as C
+        import os
+        if os.environ.get("USBS_IPM_PROF"):
+            from paper_2312_11801_b200.runtime import runtime
+            rt = runtime()
+            out = (C.c_uint64 * 10)()
+            rt.lib.usbs_ipm_profile(rt.h, out, 1)
+            names = ["stationarity", "S^-1", "rd/rhs", "M build", "Cholesky", "solves", "Eds/dirs", "line search",
+                     "update"]
+            tot = sum(out[:9])
+            for nm, v in zip(names, out[:9]):
+                print(f"  {nm:14s} {v / 1e3 / (14 * 14):8.2f} us/newton  {100 * v / max(tot, 1):5.1f}%")
         k = 20
         d = k * (k + 1) // 2
         a = rng.standard_normal((d + 5, d))
