@@ -92,6 +92,21 @@ struct usbs_problem {
   int* it_beg = nullptr;
   int* it_end = nullptr;
   int* it_slot = nullptr;  // -1: whole row, else index into the split-partial scratch
+  // SpMV hybrid: rows with 32 < nnz <= 1024 (warp per row), > 1024 (block per row)
+  int n_long_rows = 0, n_huge_rows = 0;
+  int* long_rows = nullptr;
+  int* huge_rows = nullptr;
+  int n_hseg = 0;  // 256-nnz segments of the huge rows
+  int* hseg_beg = nullptr;
+  int* hseg_end = nullptr;
+  int* hrow_first = nullptr;
+  int* hrow_count = nullptr;
+  // the subset of items that belong to rows longer than 32
+  int n_long_items = 0;
+  int* lit_row = nullptr;
+  int* lit_beg = nullptr;
+  int* lit_end = nullptr;
+  int* lit_slot = nullptr;
   int n_split_items = 0;
   int n_split_rows = 0;
   int* sr_row = nullptr;    // split rows

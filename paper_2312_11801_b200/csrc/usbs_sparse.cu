@@ -95,6 +95,174 @@ __global__ void __launch_bounds__(256) k_spmm(int n_items, const int* __restrict
   }
 }
 
+// SpMV (k = 1): groups of 4 lanes per row segment, each lane keeps 4
+// independent nonzeros in flight (16 per group per iteration), so a warp has
+// 8 segments and up to 128 gathers outstanding.  Read-only data via the
+// non-coherent path.  Segment partials of split rows go to `partial`.
+__global__ void __launch_bounds__(256) k_spmv4(int n_items, const int* __restrict__ it_row,
+                                               const int* __restrict__ it_beg, const int* __restrict__ it_end,
+                                               const int* __restrict__ it_slot, const int* __restrict__ col,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               int64_t ldx, double* __restrict__ y, int64_t ldy,
+                                               double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int warps_total = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int base = gw * 8; base < n_items; base += warps_total * 8) {
+    const int it = base + g;
+    const bool ok = it < n_items;
+    double acc = 0.0;
+    if (ok) {
+      const int b = __ldg(it_beg + it), e = __ldg(it_end + it);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int z = b + t;
+      for (; z + 12 < e; z += 16) {
+        const int j0 = __ldg(col + z), j1 = __ldg(col + z + 4), j2 = __ldg(col + z + 8), j3 = __ldg(col + z + 12);
+        const double v0 = __ldg(val + z), v1 = __ldg(val + z + 4), v2 = __ldg(val + z + 8), v3 = __ldg(val + z + 12);
+        a0 = fma(v0, __ldg(x + (int64_t)j0 * ldx), a0);
+        a1 = fma(v1, __ldg(x + (int64_t)j1 * ldx), a1);
+        a2 = fma(v2, __ldg(x + (int64_t)j2 * ldx), a2);
+        a3 = fma(v3, __ldg(x + (int64_t)j3 * ldx), a3);
+      }
+      for (; z < e; z += 4) a0 = fma(__ldg(val + z), __ldg(x + (int64_t)__ldg(col + z) * ldx), a0);
+      acc = (a0 + a1) + (a2 + a3);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (ok && t == 0) {
+      const int sl = __ldg(it_slot + it);
+      if (sl < 0) y[(int64_t)__ldg(it_row + it) * ldy] = acc;
+      else partial[sl] = acc;
+    }
+  }
+}
+
+// SpMV over the short rows (nnz <= SHORT_ROW): one thread per row, four
+// independent nonzeros in flight per thread; the warp's rows are contiguous
+// so its col/val loads stream through L1.  Long rows are skipped here and
+// handled by k_spmv4 over their segment list.
+constexpr int SHORT_ROW = 32;
+__global__ void __launch_bounds__(256) k_spmv_short(int64_t n, const int* __restrict__ rowptr,
+                                                    const int* __restrict__ col, const double* __restrict__ val,
+                                                    const double* __restrict__ x, int64_t ldx, double* __restrict__ y,
+                                                    int64_t ldy) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = __ldg(rowptr + i), e = __ldg(rowptr + i + 1);
+    if (e - b > SHORT_ROW) continue;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int z = b;
+    for (; z + 3 < e; z += 4) {
+      const int j0 = __ldg(col + z), j1 = __ldg(col + z + 1), j2 = __ldg(col + z + 2), j3 = __ldg(col + z + 3);
+      a0 = fma(__ldg(val + z), __ldg(x + (int64_t)j0 * ldx), a0);
+      a1 = fma(__ldg(val + z + 1), __ldg(x + (int64_t)j1 * ldx), a1);
+      a2 = fma(__ldg(val + z + 2), __ldg(x + (int64_t)j2 * ldx), a2);
+      a3 = fma(__ldg(val + z + 3), __ldg(x + (int64_t)j3 * ldx), a3);
+    }
+    for (; z < e; ++z) a0 = fma(__ldg(val + z), __ldg(x + (int64_t)__ldg(col + z) * ldx), a0);
+    y[i * ldy] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+// SpMV over long rows (SHORT_ROW < nnz <= 1024): one warp per row, lanes
+// stride over the nonzeros (coalesced col/val), fixed-order warp reduction.
+__global__ void __launch_bounds__(256) k_spmv_long(int nrows, const int* __restrict__ rows,
+                                                   const int* __restrict__ rowptr, const int* __restrict__ col,
+                                                   const double* __restrict__ val, const double* __restrict__ x,
+                                                   int64_t ldx, double* __restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int warps_total = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows; w += warps_total) {
+    const int r = __ldg(rows + w);
+    const int b = __ldg(rowptr + r), e = __ldg(rowptr + r + 1);  // e - b <= 256
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int z = b + lane + 32 * u;
+      a[u] = (z < e) ? __ldg(val + z) * __ldg(x + (int64_t)__ldg(col + z) * ldx) : 0.0;
+    }
+    const double s = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
+    if (lane == 0) y[(int64_t)r * ldy] = s;
+  }
+}
+
+// SpMV over 256-nnz segments of huge rows (nnz > 1024): one warp per segment
+// into a partial; k_spmv_hcombine sums each row's partials with one warp in a
+// fixed order (deterministic, no atomics).
+__global__ void __launch_bounds__(256) k_spmv_hseg(int nseg, const int* __restrict__ sbeg,
+                                                   const int* __restrict__ send, const int* __restrict__ col,
+                                                   const double* __restrict__ val, const double* __restrict__ x,
+                                                   int64_t ldx, double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const int warps_total = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nseg; w += warps_total) {
+    const int b = __ldg(sbeg + w), e = __ldg(send + w);
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int z = b + lane + 32 * u;
+      a[u] = (z < e) ? __ldg(val + z) * __ldg(x + (int64_t)__ldg(col + z) * ldx) : 0.0;
+    }
+    const double s = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
+    if (lane == 0) partial[w] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spmv_hcombine(int nrows, const int* __restrict__ rows,
+                                                       const int* __restrict__ first, const int* __restrict__ count,
+                                                       const double* __restrict__ partial, double* __restrict__ y,
+                                                       int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int warps_total = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows; w += warps_total) {
+    const int f = __ldg(first + w), c = __ldg(count + w);
+    double s = 0.0;
+    for (int u = lane; u < c; u += 32) s += partial[f + u];
+    s = warp_sum(s);
+    if (lane == 0) y[(int64_t)__ldg(rows + w) * ldy] = s;
+  }
+}
+
+// SpMM for 2 <= k <= 16: a warp per row segment, two 16-lane slots each
+// taking every other nonzero (lane c of a slot owns column c), 4 nonzeros
+// per slot in flight; slots are combined with one shuffle.
+__global__ void __launch_bounds__(256) k_spmm16x2(int n_items, const int* __restrict__ it_row,
+                                                  const int* __restrict__ it_beg, const int* __restrict__ it_end,
+                                                  const int* __restrict__ it_slot, const int* __restrict__ col,
+                                                  const double* __restrict__ val, const double* __restrict__ V,
+                                                  int64_t ldv, int k, double* __restrict__ Y, int64_t ldy,
+                                                  double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31, s = lane >> 4, c = lane & 15;
+  const bool on = c < k;
+  const int warps_total = (gridDim.x * blockDim.x) >> 5;
+  for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += warps_total) {
+    const int b = __ldg(it_beg + it), e = __ldg(it_end + it);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int z = b + s;
+    for (; z + 6 < e; z += 8) {
+      const int j0 = __ldg(col + z), j1 = __ldg(col + z + 2), j2 = __ldg(col + z + 4), j3 = __ldg(col + z + 6);
+      const double v0 = __ldg(val + z), v1 = __ldg(val + z + 2), v2 = __ldg(val + z + 4), v3 = __ldg(val + z + 6);
+      if (on) {
+        a0 = fma(v0, __ldg(V + (int64_t)j0 * ldv + c), a0);
+        a1 = fma(v1, __ldg(V + (int64_t)j1 * ldv + c), a1);
+        a2 = fma(v2, __ldg(V + (int64_t)j2 * ldv + c), a2);
+        a3 = fma(v3, __ldg(V + (int64_t)j3 * ldv + c), a3);
+      }
+    }
+    for (; z < e; z += 2) {
+      const int j0 = __ldg(col + z);
+      const double v0 = __ldg(val + z);
+      if (on) a0 = fma(v0, __ldg(V + (int64_t)j0 * ldv + c), a0);
+    }
+    double acc = (a0 + a1) + (a2 + a3);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+    if (s == 0 && on) {
+      const int sl = __ldg(it_slot + it);
+      if (sl < 0) Y[(int64_t)__ldg(it_row + it) * ldy + c] = acc;
+      else partial[(int64_t)sl * k + c] = acc;
+    }
+  }
+}
+
 // combine the partials of split rows in a fixed order (deterministic)
 __global__ void k_spmm_combine(int n_sr, const int* __restrict__ sr_row, const int* __restrict__ sr_first,
                                const int* __restrict__ sr_count, const double* __restrict__ partial,
@@ -368,6 +536,46 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
     p->cent = dev_upload(p, cent.data(), cent.size());
     p->max_entries_per_cons = mx;
   }
+  {
+    std::vector<int32_t> lr, lb, le, ls;
+    for (size_t t = 0; t < irow.size(); ++t) {
+      const int32_t r = irow[t];
+      if (rp32[r + 1] - rp32[r] > SHORT_ROW) {
+        lr.push_back(r); lb.push_back(ibeg[t]); le.push_back(iend[t]); ls.push_back(islot[t]);
+      }
+    }
+    std::vector<int32_t> longr, huger;
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t len = rp32[i + 1] - rp32[i];
+      if (len > 256) huger.push_back((int32_t)i);
+      else if (len > SHORT_ROW) longr.push_back((int32_t)i);
+    }
+    p->n_long_rows = (int)longr.size();
+    p->n_huge_rows = (int)huger.size();
+    p->long_rows = dev_upload(p, longr.data(), longr.size());
+    p->huge_rows = dev_upload(p, huger.data(), huger.size());
+    std::vector<int32_t> hb, he, hf, hc;
+    for (int32_t r : huger) {
+      hf.push_back((int32_t)hb.size());
+      int cnt = 0;
+      for (int32_t z = rp32[r]; z < rp32[r + 1]; z += 256) {
+        hb.push_back(z);
+        he.push_back(std::min(rp32[r + 1], z + 256));
+        ++cnt;
+      }
+      hc.push_back(cnt);
+    }
+    p->n_hseg = (int)hb.size();
+    p->hseg_beg = dev_upload(p, hb.data(), hb.size());
+    p->hseg_end = dev_upload(p, he.data(), he.size());
+    p->hrow_first = dev_upload(p, hf.data(), hf.size());
+    p->hrow_count = dev_upload(p, hc.data(), hc.size());
+    p->n_long_items = (int)lr.size();
+    p->lit_row = dev_upload(p, lr.data(), lr.size());
+    p->lit_beg = dev_upload(p, lb.data(), lb.size());
+    p->lit_end = dev_upload(p, le.data(), le.size());
+    p->lit_slot = dev_upload(p, ls.data(), ls.size());
+  }
   p->it_row = dev_upload(p, irow.data(), irow.size());
   p->it_beg = dev_upload(p, ibeg.data(), ibeg.size());
   p->it_end = dev_upload(p, iend.data(), iend.size());
@@ -440,10 +648,31 @@ void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int
   double* partial = nullptr;
   if (p->n_split_items) partial = (double*)ctx->ws.get(WS_SPMM_PARTIAL, (size_t)p->n_split_items * k * sizeof(double));
   const int th = 256;
-  if (k <= 16) {
-    int per = th / 16;
-    int bl = (int)std::min<int64_t>((p->n_items + per - 1) / per, 16 * ctx->num_sms);
-    k_spmm<16><<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,
+  if (k == 1) {
+    int bl = (int)std::min<int64_t>((p->n + th - 1) / th, 16 * ctx->num_sms);
+    k_spmv_short<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n, p->rowptr, p->col, val, V, ldv, Y, ldy);
+    check_launch(ctx);
+    if (p->n_long_rows) {
+      int bl2 = (int)std::min<int64_t>((p->n_long_rows + 7) / 8, 16 * ctx->num_sms);
+      k_spmv_long<<<std::max(bl2, 1), th, 0, ctx->stream>>>(p->n_long_rows, p->long_rows, p->rowptr, p->col, val,
+                                                            V, ldv, Y, ldy);
+      check_launch(ctx);
+    }
+    if (p->n_huge_rows) {
+      double* hp = (double*)ctx->ws.get(WS_SPMM_PARTIAL + 100, (size_t)p->n_hseg * sizeof(double));
+      int bl3 = (int)std::min<int64_t>((p->n_hseg + 7) / 8, 16 * ctx->num_sms);
+      k_spmv_hseg<<<std::max(bl3, 1), th, 0, ctx->stream>>>(p->n_hseg, p->hseg_beg, p->hseg_end, p->col, val, V,
+                                                            ldv, hp);
+      check_launch(ctx);
+      int bl4 = (int)std::min<int64_t>((p->n_huge_rows + 7) / 8, 4 * ctx->num_sms);
+      k_spmv_hcombine<<<std::max(bl4, 1), th, 0, ctx->stream>>>(p->n_huge_rows, p->huge_rows, p->hrow_first,
+                                                                p->hrow_count, hp, Y, ldy);
+      check_launch(ctx);
+    }
+    return;
+  } else if (k <= 16) {
+    int bl = (int)std::min<int64_t>((p->n_items + 7) / 8, 16 * ctx->num_sms);
+    k_spmm16x2<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,
                                                         p->col, val, V, ldv, k, Y, ldy, partial);
   } else {
     int per = th / 32;
