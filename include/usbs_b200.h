@@ -78,6 +78,15 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m,
                                 const int64_t* e_idx, const int64_t* e_rows,
                                 const int64_t* e_cols, const double* e_vals,
                                 int diag_only, usbs_problem** out);
+/* Row shard of a problem for multi-GPU runs: the rank's n_rows rows of C
+ * (CSR with global column indices < n_cols) and the DIRECTED constraint
+ * entries of those rows (local row, global column, local constraint index;
+ * no mirroring).  diag_only: entry i is (i, i, row_offset + i, 1.0). */
+usbs_status usbs_problem_create_shard(usbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t m,
+                                      const int64_t* c_indptr, const int32_t* c_indices,
+                                      const double* c_data, int64_t n_entries, const int64_t* e_idx,
+                                      const int64_t* e_rows, const int64_t* e_cols,
+                                      const double* e_vals, int diag_only, usbs_problem** out);
 usbs_status usbs_problem_destroy(usbs_problem* p);
 /* nnz of the merged slack pattern and the lanczos grid size (for reporting) */
 usbs_status usbs_problem_info(usbs_problem* p, int64_t* nnz_z, int64_t* nnz_c,

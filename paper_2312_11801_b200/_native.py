@@ -38,6 +38,8 @@ PROTOS = {
     "usbs_memcpy_h2d": (_i32, [_p, _p, _p, _i64]),
     "usbs_memcpy_d2h": (_i32, [_p, _p, _p, _i64]),
     "usbs_problem_create": (_i32, [_p, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _i32, C.POINTER(_p)]),
+    "usbs_problem_create_shard": (_i32, [_p, _i64, _i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _i32,
+                                         C.POINTER(_p)]),
     "usbs_problem_destroy": (_i32, [_p]),
     "usbs_problem_info": (_i32, [_p, C.POINTER(_i64), C.POINTER(_i64), _pi, _pi]),
     "usbs_slack_assemble": (_i32, [_p, _p, _p]),

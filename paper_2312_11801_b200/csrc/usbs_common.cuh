@@ -66,7 +66,7 @@ struct usbs_ctx {
 
 struct usbs_problem {
   usbs_ctx* ctx = nullptr;
-  int64_t n = 0, m = 0, nnz = 0, nnz_c = 0, ne = 0;
+  int64_t n = 0, n_cols = 0, m = 0, nnz = 0, nnz_c = 0, ne = 0;  // n = rows (local for shards)
   bool diag_only = false;
   // merged CSR pattern of C - A*(y)
   int* rowptr = nullptr;

@@ -637,6 +637,7 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   USBS_API_BEGIN
   const int64_t n = p->n;
   if (k_c < 1) fail(USBS_ERR_CONFIG, "k_c must be at least 1");
+  if (p->n_cols != p->n) fail(USBS_ERR_SHAPE, "lanczos_top needs a square (unsharded) operator");
   if (max_restarts < 0 || inner_iters < 0) fail(USBS_ERR_CONFIG, "invalid Lanczos budget");
   if (ldvecs < k_c) fail(USBS_ERR_SHAPE, "ldvecs < k_c");
   const double* val = which ? p->zval : p->cval;

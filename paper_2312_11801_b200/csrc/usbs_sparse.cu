@@ -351,31 +351,59 @@ usbs_status usbs_memcpy_d2h(usbs_ctx* c, void* dst, const void* src, int64_t byt
   USBS_API_END
 }
 
+static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, const int64_t* c_indptr,
+                           const int32_t* c_indices, const double* c_data, int64_t ne, const int64_t* e_idx,
+                           const int64_t* e_rows, const int64_t* e_cols, const double* e_vals, int diag_only,
+                           int directed, usbs_problem** out);
+
 usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64_t* c_indptr,
                                 const int32_t* c_indices, const double* c_data, int64_t ne,
                                 const int64_t* e_idx, const int64_t* e_rows, const int64_t* e_cols,
                                 const double* e_vals, int diag_only, usbs_problem** out) {
   USBS_API_BEGIN
+  create_problem(ctx, n, n, m, c_indptr, c_indices, c_data, ne, e_idx, e_rows, e_cols, e_vals, diag_only, 0, out);
+  USBS_API_END
+}
+
+usbs_status usbs_problem_create_shard(usbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t m,
+                                      const int64_t* c_indptr, const int32_t* c_indices, const double* c_data,
+                                      int64_t ne, const int64_t* e_idx, const int64_t* e_rows,
+                                      const int64_t* e_cols, const double* e_vals, int diag_only,
+                                      usbs_problem** out) {
+  USBS_API_BEGIN
+  create_problem(ctx, n_rows, n_cols, m, c_indptr, c_indices, c_data, ne, e_idx, e_rows, e_cols, e_vals, diag_only, 1,
+                 out);
+  USBS_API_END
+}
+
+static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, const int64_t* c_indptr,
+                           const int32_t* c_indices, const double* c_data, int64_t ne, const int64_t* e_idx,
+                           const int64_t* e_rows, const int64_t* e_cols, const double* e_vals, int diag_only,
+                           int directed, usbs_problem** out) {
   if (!ctx || !out) fail(USBS_ERR_CONFIG, "null context/output");
-  if (n < 1 || m < 0 || ne < 0) fail(USBS_ERR_SHAPE, "invalid problem dimensions");
-  if (n >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "n exceeds int32 indexing");
+  if (n < 1 || n_cols < 1 || m < 0 || ne < 0) fail(USBS_ERR_SHAPE, "invalid problem dimensions");
+  if (n >= (1LL << 31) - 1 || n_cols >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "n exceeds int32 indexing");
   USBS_CUDA(cudaSetDevice(ctx->device));
   auto* p = new usbs_problem();
   p->ctx = ctx;
   p->n = n;
+  p->n_cols = n_cols;
   p->m = m;
   p->ne = ne;
   p->diag_only = diag_only != 0;
   p->nnz_c = c_indptr[n];
 
   // --- extra (row, col, entry, role) pairs from the constraint entries
+  // (square problems mirror off-diagonal entries; shard problems receive the
+  // directed entries of their own rows, with global columns)
   std::vector<int64_t> xcnt(n + 1, 0);
   for (int64_t e = 0; e < ne; ++e) {
     int64_t r = e_rows[e], c = e_cols[e], ci = e_idx[e];
-    if (r < 0 || c < 0 || r >= n || c >= n || r > c) fail(USBS_ERR_SHAPE, "constraint entry out of range or rows > cols");
+    if (r < 0 || c < 0 || r >= n || c >= n_cols || (!directed && r > c))
+      fail(USBS_ERR_SHAPE, "constraint entry out of range or rows > cols");
     if (ci < 0 || ci >= m) fail(USBS_ERR_SHAPE, "constraint index out of range");
     xcnt[r + 1]++;
-    if (r != c) xcnt[c + 1]++;
+    if (!directed && r != c) xcnt[c + 1]++;
   }
   for (int64_t i = 0; i < n; ++i) xcnt[i + 1] += xcnt[i];
   std::vector<int32_t> xcol(xcnt[n]);
@@ -386,7 +414,7 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
       int64_t r = e_rows[e], c = e_cols[e];
       xcol[pos[r]] = (int32_t)c;
       xent[pos[r]++] = e;
-      if (r != c) {
+      if (!directed && r != c) {
         xcol[pos[c]] = (int32_t)r;
         xent[pos[c]++] = e;
       }
@@ -404,7 +432,7 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
   for (int64_t i = 0; i < n; ++i) {
     crow.clear();
     for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) {
-      if (c_indices[z] < 0 || c_indices[z] >= n) fail(USBS_ERR_SHAPE, "cost column index out of range");
+      if (c_indices[z] < 0 || c_indices[z] >= n_cols) fail(USBS_ERR_SHAPE, "cost column index out of range");
       crow.emplace_back(c_indices[z], c_data[z]);
     }
     if (!std::is_sorted(crow.begin(), crow.end(),
@@ -496,14 +524,11 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
     if (m != n || ne != n) fail(USBS_ERR_SHAPE, "diag_only requires m == n == entries");
     diag_slot.resize(n);
     for (int64_t e = 0; e < ne; ++e) {
-      if (e_rows[e] != e_cols[e] || e_idx[e] != e_rows[e] || e_vals[e] != 1.0)
-        fail(USBS_ERR_SHAPE, "diag_only entries must be (i, i, i, 1.0)");
+      if ((!directed && e_rows[e] != e_cols[e]) || e_idx[e] != e_rows[e] || e_rows[e] != e || e_vals[e] != 1.0)
+        fail(USBS_ERR_SHAPE, "diag_only entries must be (i, i, col_i, 1.0) in row order");
     }
-    // slot_of_x for row r's single extra entry: recompute robustly
-    for (int64_t i = 0; i < n; ++i) {
-      auto it = std::lower_bound(col.begin() + rowptr[i], col.begin() + rowptr[i + 1], (int32_t)i);
-      diag_slot[i] = (int32_t)(it - col.begin());
-    }
+    // each row holds exactly one entry, at x-position xcnt[i]
+    for (int64_t i = 0; i < n; ++i) diag_slot[i] = (int32_t)slot_of_x[xcnt[i]];
   }
 
   // --- upload
@@ -587,7 +612,6 @@ usbs_status usbs_problem_create(usbs_ctx* ctx, int64_t n, int64_t m, const int64
   p->blk_item = dev_upload(p, blk_item.data(), blk_item.size());
   p->blk_sr = dev_upload(p, blk_sr.data(), blk_sr.size());
   *out = p;
-  USBS_API_END
 }
 
 usbs_status usbs_problem_destroy(usbs_problem* p) {

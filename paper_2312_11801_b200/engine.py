@@ -17,17 +17,34 @@ def _p(t):
 
 
 class Engine:
-    def __init__(self, dp: DeviceProblem):
+    """comm (dist.Comm or None): when the problem is row-sharded, every
+    reduction over the n/m dimension is completed with an allreduce, so the
+    callers (solver.py) are identical for 1 and N GPUs."""
+
+    def __init__(self, dp: DeviceProblem, comm=None):
         self.dp = dp
         self.rt: Runtime = dp.rt
         self.lib = self.rt.lib
         self.h = self.rt.h
         self.n, self.m = dp.n, dp.m
+        self.comm = comm if (comm is not None and comm.world > 1) else None
+        self._red2 = None
 
     # ---------------------------------------------------------------- vectors
     def vec(self, op, m, x=None, y=None, z=None, b=None, ineq=None, s0=0.0, s1=0.0, out=None, red=None):
+        if self.comm is not None and red is not None and op == N.VOP_DOTAFF:
+            if self._red2 is None:
+                self._red2 = self.rt.zeros(2)
+            check(self.lib.usbs_vec(self.h, N.VOP_DOT, int(m), _p(x), _p(y), None, None, None, 0.0, 0.0, None,
+                                    _p(self._red2)), "vec")
+            self.comm.allreduce_sum(self._red2[0:1])
+            red[0:1].copy_(self._red2[0:1] * s0 + s1)
+            return
         check(self.lib.usbs_vec(self.h, op, int(m), _p(x), _p(y), _p(z), _p(b), _p(ineq), float(s0), float(s1),
                                 _p(out), _p(red)), "vec")
+        if self.comm is not None and red is not None:
+            self.comm.allreduce_sum(red[0:1])
+            self.comm.allreduce_max(red[1:2])
 
     def dot_into(self, x, y, red, scale=1.0, shift=0.0):
         """red[0] = scale * <x, y> + shift (device scalar)."""
@@ -46,11 +63,15 @@ class Engine:
     def gram(self, A, B, out, sym=False):
         check(self.lib.usbs_gram(self.h, A.shape[0], _p(A), A.stride(0), A.shape[1], _p(B), B.stride(0),
                                  B.shape[1], _p(out), 1 if sym else 0), "gram")
+        if self.comm is not None:  # sym(sum of partials) == sum of sym(partials)
+            self.comm.allreduce_sum(out)
         return out
 
     def wcoldot(self, F, G, w, out):
         check(self.lib.usbs_wcoldot(self.h, F.shape[0], _p(F), F.stride(0), _p(G), G.stride(0), F.shape[1],
                                     _p(w), _p(out)), "wcoldot")
+        if self.comm is not None:
+            self.comm.allreduce_sum(out[0:1])
 
     def small_eigh(self, a, vals, vecs):
         check(self.lib.usbs_small_eigh(self.h, a.shape[0], _p(a), _p(vals), _p(vecs)), "small_eigh")
@@ -64,6 +85,8 @@ class Engine:
         return out
 
     def dense_update(self, X, eta, F, lams):
+        if self.comm is not None:
+            raise NotImplementedError("the explicit n x n store is not sharded; use sketch_rank > 0")
         check(self.lib.usbs_dense_update(self.h, X.shape[0], _p(X), float(eta), _p(F), F.stride(0), F.shape[1],
                                          _p(lams)), "dense_update")
 
@@ -82,6 +105,10 @@ class Engine:
         check(self.lib.usbs_cons_compressed(self.h, self.dp.h, _p(V), V.stride(0), V.shape[1], float(scale_gram),
                                             _p(gram_out), _p(a), float(scale_a), _p(a_out), _p(w), float(scale_w),
                                             _p(w_out)), "cons_compressed")
+        if self.comm is not None:
+            for t in (gram_out, a_out if a is not None else None, w_out if w is not None else None):
+                if t is not None:
+                    self.comm.allreduce_sum(t)
 
     # ---------------------------------------------------------------- ipm
     def ipm(self, k, has_eta, Q11, q12, lin_s, scal, warm, state_out, result, opts=None):

@@ -116,15 +116,20 @@ class Residuals:
 class DeviceSketchStore:
     """SketchStore + sketch.py on the device: P (n x r), Psi (n x r)."""
 
-    def __init__(self, eng: Engine, n: int, r: int, seed: int, psi_host: Optional[np.ndarray] = None):
+    def __init__(self, eng: Engine, n: int, r: int, seed: int, psi_host: Optional[np.ndarray] = None,
+                 rows: Optional[tuple] = None, shard=None, comm=None):
+        """n is the global dimension; rows = (r0, r1) selects this rank's
+        block of Psi and P when the problem is row-sharded."""
         if not 1 <= r <= n:
             raise ValueError(f"sketch rank {r} must lie in [1, {n}]")
         self.eng, self.n, self.r, self.psi_seed = eng, n, r, int(seed)
+        self.shard, self.comm = shard, comm
+        r0, r1 = rows if rows is not None else (0, n)
         rt = eng.rt
         if psi_host is None:  # make_test_matrix (sketch.py:25-27): legacy MT19937, host once
-            psi_host = np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))
+            psi_host = np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))[r0:r1]
         self.psi = rt.upload(psi_host)
-        self.P = rt.zeros(n, r)
+        self.P = rt.zeros(r1 - r0, r)
         self.G = rt.empty(64, max(r, 1))
 
     def update(self, eta: float, F, lams) -> None:
@@ -153,8 +158,9 @@ class DeviceSketchStore:
             u[:r, :r] = np.eye(r)
             return u, np.zeros(r)
         shift = math.sqrt(n) * np.finfo(float).eps * norm_p
-        ps = rt.empty(n, r)
-        eng.vec(N.VOP_AXPBY, n * r, x=self.P.view(-1), y=self.psi.view(-1), s0=1.0, s1=shift, out=ps.view(-1))
+        nl = self.P.shape[0]  # local rows (== n unless sharded)
+        ps = rt.empty(nl, r)
+        eng.vec(N.VOP_AXPBY, nl * r, x=self.P.view(-1), y=self.psi.view(-1), s0=1.0, s1=shift, out=ps.view(-1))
         core = rt.empty(r, r)
         eng.gram(self.psi, ps, core, sym=True)
         perm = rt.torch.zeros(r, dtype=rt.torch.int32, device=rt.device)
@@ -162,7 +168,7 @@ class DeviceSketchStore:
         info = rt.zeros(3)
         eng.pivchol(core, -1.0, perm, rinv, info)
         if int(info[0].item()) == r and float(info[1].item()) > 0.0:
-            half = eng.rowgemm(ps, rinv, rt.empty(n, r))
+            half = eng.rowgemm(ps, rinv, rt.empty(nl, r))
         else:  # rank-deficient core: eigenvalue pseudo-inverse (sketch.py:100-108)
             vals, vecs = rt.empty(r), rt.empty(r, r)
             eng.small_eigh(core, vals, vecs)
@@ -174,7 +180,11 @@ class DeviceSketchStore:
                 u[:r, :r] = np.eye(r)
                 return u, np.zeros(r)
             B = rt.upload(qm[:, keep] / np.sqrt(w[keep])[None, :])
-            half = eng.rowgemm(ps, B, rt.empty(n, int(keep.sum())))
+            half = eng.rowgemm(ps, B, rt.empty(nl, int(keep.sum())))
+        if self.shard is not None and self.comm is not None and self.comm.world > 1:
+            full = rt.empty(n, half.shape[1])
+            self.comm.allgather_rows(half, full, self.shard)
+            half = full
         u, sv, _ = np.linalg.svd(half.cpu().numpy(), full_matrices=False)
         return u, np.maximum(sv ** 2 - shift, 0.0)
 
@@ -297,13 +307,19 @@ S_Q22, S_LINETA, S_EQ22, S_ELINETA, S_DNU, S_CQS, S_BYC, S_RES, S_BY, S_MINI, S_
 class DeviceSolver:
     """Holds the uploaded problem and scratch buffers for one solve."""
 
-    def __init__(self, prob, cfg, dprob: Optional[DeviceProblem] = None):
+    def __init__(self, prob, cfg, dprob: Optional[DeviceProblem] = None, comm=None, engine=None):
         self.prob = prob
         self.cfg = cfg
         self.dp = dprob or DeviceProblem(prob)
-        self.eng = Engine(self.dp)
+        self.comm = comm
+        self.eng = engine or Engine(self.dp, comm)
         self.rt = self.dp.rt
         self.n, self.m = self.dp.n, self.dp.m
+        # row sharding (dist.py): local rows [r0, r1) of the global n
+        self.shard = getattr(self.dp, "shard", None)
+        self.n_global = int(prob.n)
+        self.r0 = self.shard.r0 if self.shard is not None else 0
+        self.r1 = self.shard.r1 if self.shard is not None else self.n
         self.alpha = float(prob.alpha)
         self.b = self.dp.b
         self.ineq = self.dp.ineq
@@ -314,8 +330,8 @@ class DeviceSolver:
         lz = getattr(cfg, "lanczos", None) or LanczosSettings()
         self.lz = (int(lz.inner_iters), int(lz.max_restarts), lz.tol)
         self.seed = int(cfg.seed)
-        self.k_c = min(cfg.k_c, self.n)
-        self.k_p = min(cfg.k_p, self.n - self.k_c)
+        self.k_c = min(cfg.k_c, self.n_global)
+        self.k_p = min(cfg.k_p, self.n_global - self.k_c)
         k = self.k_c + self.k_p
         self.k = k
         rt = self.rt
@@ -365,6 +381,9 @@ class DeviceSolver:
             ev0 = self.rt.torch.cuda.Event(enable_timing=True)
             ev1 = self.rt.torch.cuda.Event(enable_timing=True)
             ev0.record(self.rt.stream)
+        if self.shard is not None:
+            from .dist import lanczos_sharded
+            return lanczos_sharded(self.eng, self.dp, which, self.k_c, inner, rst, tol, self.seed, out=self.vecs)
         res = lanczos_top(op, self.k_c, inner, rst, tol, self.seed, out=self.vecs)
         if probe is not None:
             ev1.record(self.rt.stream)
@@ -383,7 +402,7 @@ class DeviceSolver:
         red = rt.zeros(2)
         while have < k:
             g = np.random.default_rng([self.seed & 0xFFFFFFFF, 0x5EED, tag, attempt])
-            v = rt.upload(g.standard_normal(n).reshape(n, 1))
+            v = rt.upload(g.standard_normal(self.n_global)[self.r0:self.r1].reshape(n, 1))
             if have:
                 cur = out[:, :have]
                 eng.gram(cur, v, coef[:have])
@@ -484,7 +503,8 @@ class DeviceSolver:
         basis = self.completion(eig.eigenvectors_dev, self.k, tag=0)
         stats = AggregateStats(0.0, 0.0, rt.zeros(self.m))
         if self.cfg.sketch_rank > 0:
-            store = DeviceSketchStore(self.eng, self.n, min(self.cfg.sketch_rank, self.n), sketch_seed)
+            store = DeviceSketchStore(self.eng, self.n_global, min(self.cfg.sketch_rank, self.n_global), sketch_seed,
+                                      rows=(self.r0, self.r1), shard=self.shard, comm=self.comm)
         else:
             store = DeviceExplicitStore(self.eng, self.n)
         model = BundleModel(basis, stats, self.k_c, self.k_p, store)
