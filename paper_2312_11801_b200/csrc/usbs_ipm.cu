@@ -61,6 +61,7 @@ __host__ __device__ inline int state_len(int k) { return 2 * k * k + 7; }
 
 constexpr int IPM_THREADS = 512;
 constexpr int SMEM_D = 210;
+constexpr int CHOL_REG_D = 66;  // register-resident Cholesky up to d = 66 (k = 11)
 constexpr int KMAX = 32;
 
 __device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }  // packed lower, i >= j
@@ -111,6 +112,33 @@ __device__ void warp_chol(double* W, int k, int* flg, int slot) {
       __syncwarp();
     }
     if (lane == 0) flg[slot] = ok;
+  }
+  __syncthreads();
+}
+
+// two independent k x k Cholesky tests at once: warp 0 factors Wa, warp 1 Wb
+// (the line search's S + d dS and T + d dT); flg[sa], flg[sb] get the results
+__device__ void warp_chol2(double* Wa, double* Wb, int k, int* flg, int sa, int sb) {
+  const int w = threadIdx.x >> 5;
+  if (w < 2) {
+    double* W = w == 0 ? Wa : Wb;
+    const int lane = threadIdx.x & 31;
+    int ok = 1;
+    for (int j = 0; j < k; ++j) {
+      const double piv = W[j * k + j];
+      if (!(piv > 0.0)) { ok = 0; break; }
+      const double r = rsqrt(piv);
+      __syncwarp();
+      if (lane == 0) W[j * k + j] = piv * r;
+      if (lane > j && lane < k) W[lane * k + j] *= r;
+      __syncwarp();
+      if (lane > j && lane < k) {
+        const double lij = W[lane * k + j];
+        for (int c = j + 1; c <= lane; ++c) W[lane * k + c] -= lij * W[c * k + j];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) flg[w == 0 ? sa : sb] = ok;
   }
   __syncthreads();
 }
@@ -392,7 +420,60 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       // __syncwarp only); the trailing update is a SYRK over 4x4 register
       // tiles by the whole block.  rdiag keeps 1 / L_jj for the solves.
       double* rdiag = sm.f1;  // f1 is dead once rhs is formed
-      {
+      if (d <= CHOL_REG_D) {
+        // d <= 66: right-looking with the matrix in REGISTERS (each thread
+        // owns <= 5 packed entries), one barrier per column; the column being
+        // eliminated is published to a double-buffered smem vector.
+        constexpr int EPT = 5;
+        const int np = d * (d + 1) / 2;
+        double val[EPT];
+        short ri[EPT], ci[EPT];
+        double* colA = sm.tmp;  // free until the E ds product below
+        double* colB = sm.ds;   // written by the solves afterwards
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+          const int x = tid + u * nth;
+          ri[u] = -1;
+          ci[u] = 0;
+          val[u] = 0.0;
+          if (x < np) {
+            int r = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+            while (r * (r + 1) / 2 > x) --r;
+            while ((r + 1) * (r + 2) / 2 <= x) ++r;
+            ri[u] = (short)r;
+            ci[u] = (short)(x - r * (r + 1) / 2);
+            val[u] = Mp[x];
+            if (ci[u] == 0) colA[r] = val[u];
+          }
+        }
+        __syncthreads();
+        for (int j = 0; j < d; ++j) {
+          const double* cur = (j & 1) ? colB : colA;
+          double* nxt = (j & 1) ? colA : colB;
+          const double piv = cur[j];
+          if (!(piv > 0.0)) { fail = 1; break; }  // uniform: all threads read the same pivot
+          const double r = rsqrt(piv), r2 = r * r;
+#pragma unroll
+          for (int u = 0; u < EPT; ++u) {
+            const int i = ri[u], c = ci[u];
+            if (i < 0 || c < j) continue;
+            if (c == j) {
+              val[u] = (i == j) ? piv * r : val[u] * r;  // final L entries of column j
+            } else {
+              val[u] -= (cur[i] * cur[c]) * r2;
+              if (c == j + 1) nxt[i] = val[u];
+            }
+          }
+          if (tid == 0) rdiag[j] = r;
+          __syncthreads();
+        }
+        if (!fail) {
+#pragma unroll
+          for (int u = 0; u < EPT; ++u)
+            if (ri[u] >= 0) Mp[tid + u * nth] = val[u];
+        }
+        __syncthreads();
+      } else {
         constexpr int CB = 16;
         for (int J = 0; J < d && !fail; J += CB) {
           const int JB = min(CB, d - J);
@@ -474,11 +555,20 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
         for (int J = 0; J < d; J += 32) {  // forward: L y = rhs
           const int JB = min(32, d - J);
           if (tid < 32) {
+            // the triangle's row of this lane and 1/L_jj preloaded into
+            // registers: the dependent chain is one shuffle + one FMA per step
             double x = lane < JB ? sm.rhs[J + lane] : 0.0;
-            for (int jj = 0; jj < JB; ++jj) {
-              const double yj = __shfl_sync(0xffffffffu, x, jj) * rdiag[J + jj];
-              if (lane == jj) x = yj;
-              else if (lane > jj && lane < JB) x -= Mp[pidx(J + lane, J + jj)] * yj;
+            const double rdl = lane < JB ? rdiag[J + lane] : 0.0;
+            double Lr[32];
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) Lr[jj] = (jj < lane && lane < JB) ? Mp[pidx(J + lane, J + jj)] : 0.0;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              if (jj < JB) {
+                const double yj = __shfl_sync(0xffffffffu, x * rdl, jj);
+                if (lane == jj) x = yj;
+                else x = fma(-Lr[jj], yj, x);
+              }
             }
             if (lane < JB) sm.rhs[J + lane] = x;
           }
@@ -495,10 +585,17 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           const int J = max(0, Jend - 32), JB = Jend - J;
           if (tid < 32) {
             double x = lane < JB ? sm.rhs[J + lane] : 0.0;
-            for (int jj = JB - 1; jj >= 0; --jj) {
-              const double xj = __shfl_sync(0xffffffffu, x, jj) * rdiag[J + jj];
-              if (lane == jj) x = xj;
-              else if (lane < jj) x -= Mp[pidx(J + jj, J + lane)] * xj;
+            const double rdl = lane < JB ? rdiag[J + lane] : 0.0;
+            double Lc[32];
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) Lc[jj] = (lane < jj && jj < JB) ? Mp[pidx(J + jj, J + lane)] : 0.0;
+#pragma unroll
+            for (int jj = 31; jj >= 0; --jj) {
+              if (jj < JB) {
+                const double xj = __shfl_sync(0xffffffffu, x * rdl, jj);
+                if (lane == jj) x = xj;
+                else x = fma(-Lc[jj], xj, x);
+              }
             }
             if (lane < JB) sm.ds[J + lane] = x;
           }
@@ -566,12 +663,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
               sm.W2[x] = sm.T[x] + delta * sm.dT[x];
             }
             __syncthreads();
-            warp_chol(sm.W1, k, sm.flg, 3);
-            int ok = sm.flg[3];
-            if (ok) {
-              warp_chol(sm.W2, k, sm.flg, 4);
-              ok = sm.flg[4];
-            }
+            warp_chol2(sm.W1, sm.W2, k, sm.flg, 3, 4);  // both PSD tests at once
+            int ok = sm.flg[3] && sm.flg[4];
             if (ok) {
               if (omega + delta * domega <= 0 || sigma + delta * dsig <= 0) ok = 0;
               if (has_eta && (eta + delta * deta <= 0 || zeta + delta * dzeta <= 0)) ok = 0;

@@ -496,7 +496,9 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->n_split_rows = (int)srow.size();
 
   // --- Lanczos block partition (row aligned, balanced on nnz + row cost)
-  int G = (int)std::min<int64_t>(ctx->num_sms,
+  // leave 4 SMs free for kernels that overlap the Lanczos kernel (the
+  // model-evaluation IPM on the auxiliary stream)
+  int G = (int)std::min<int64_t>(std::max(1, ctx->num_sms - 4),
                                  std::max<int64_t>(1, std::max<int64_t>((n + 63) / 64, (p->nnz + n + 4095) / 4096)));
   if (const char* env = getenv("USBS_LZ_BLOCKS")) G = std::max(1, std::min(ctx->num_sms, atoi(env)));
   p->lz_blocks = G;

@@ -33,17 +33,31 @@ struct TriSmem {
   int* iw;      // 64
 };
 
-__device__ inline int sturm_count(const double* d, const double* e, int N, double sigma, double pivmin) {
+// 1/q to ~1 ulp: FP32 MUFU seed + two Newton steps (4 dependent DFMA), exact
+// division only when q is outside the FP32 range.
+__device__ __forceinline__ double fast_rcp(double q) {
+  const double aq = fabs(q);
+  if (!(aq > 1e-37 && aq < 1e37)) return 1.0 / q;
+  double r = (double)__frcp_rn((float)q);
+  r = fma(r, fma(-q, r, 1.0), r);
+  r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
+// number of eigenvalues of T below sigma (LDL^T pivot signs, Kahan's form);
+// e2[i] = e[i]^2.  An approximate reciprocal perturbs e2 by ~1e-16 relative,
+// i.e. a backward-stable count.
+__device__ inline int sturm_count(const double* d, const double* e2, int N, double sigma, double pivmin) {
   int cnt = 0;
   double q = d[0] - sigma;
   if (fabs(q) < pivmin) q = -pivmin;
   if (q < 0.0) ++cnt;
   for (int i = 1; i < N; ++i) {
-    q = d[i] - sigma - (e[i - 1] * e[i - 1]) / q;
+    q = (d[i] - sigma) - e2[i - 1] * fast_rcp(q);
     if (fabs(q) < pivmin) q = -pivmin;
     if (q < 0.0) ++cnt;
   }
-  return cnt;  // number of eigenvalues < sigma
+  return cnt;
 }
 
 // All threads of the block call.  tridiagonal != 0: A already tridiagonal.
@@ -107,31 +121,25 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
           if (lane == 0) s.p[i] = beta * t;
         }
         __syncthreads();
-        if (warp == 0) {
-          double t = 0.0;
-          for (int c = lane; c < L; c += 32) t = fma(s.p[c], s.v[c], t);
-          t = warp_sum(t);
-          if (lane == 0) s.red[2] = 0.5 * beta * t;
+        // every warp forms K = beta/2 p^T v itself (no extra barrier); rows of
+        // A22 -= v w^T + w v^T with w = p - K v, and Q[:, k+1:] -= beta (Q v) v^T
+        double K = 0.0;
+        for (int c = lane; c < L; c += 32) K = fma(s.p[c], s.v[c], K);
+        K = 0.5 * beta * warp_sum(K);
+        for (int i = warp; i < L; i += nwp) {
+          const double vi = s.v[i], wi = s.p[i] - K * vi;
+          double* row = A + (k + 1 + i) * N + (k + 1);
+          for (int c = lane; c < L; c += 32) {
+            const double vc = s.v[c];
+            row[c] -= vi * (s.p[c] - K * vc) + wi * vc;
+          }
         }
-        __syncthreads();
-        const double K = s.red[2];
-        // w = p - K v (in place in p), then A22 -= v w^T + w v^T, Q[:, k+1:] -= beta (Q v) v^T
-        for (int i = tid; i < L; i += nth) s.p[i] -= K * s.v[i];
-        // Q v (row i of Q times v) into red-area-free scratch: use dd as temp (length N)
         for (int i = warp; i < N; i += nwp) {
+          double* row = s.Q + i * N + (k + 1);
           double t = 0.0;
-          for (int c = lane; c < L; c += 32) t = fma(s.Q[i * N + (k + 1 + c)], s.v[c], t);
-          t = warp_sum(t);
-          if (lane == 0) s.dd[i] = beta * t;
-        }
-        __syncthreads();
-        for (int x = tid; x < L * L; x += nth) {
-          const int i = x / L, c = x % L;
-          A[(k + 1 + i) * N + (k + 1 + c)] -= s.v[i] * s.p[c] + s.p[i] * s.v[c];
-        }
-        for (int x = tid; x < N * L; x += nth) {
-          const int i = x / L, c = x % L;
-          s.Q[i * N + (k + 1 + c)] -= s.dd[i] * s.v[c];
+          for (int c = lane; c < L; c += 32) t = fma(row[c], s.v[c], t);
+          t = beta * warp_sum(t);
+          for (int c = lane; c < L; c += 32) row[c] -= t * s.v[c];
         }
       }
       if (tid == 0) {
@@ -148,6 +156,7 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
   for (int i = tid; i < N; i += nth) {
     s.dd[i] = A[i * N + i];
     s.ee[i] = (i + 1 < N) ? A[(i + 1) * N + i] : 0.0;
+    s.p[i] = s.ee[i] * s.ee[i];  // e^2 for the Sturm counts
   }
   __syncthreads();
   TRI_MARK(0);
@@ -173,7 +182,7 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
     for (int it = 0; it < 16; ++it) {
       if (hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) * 2.0 + 1e-300) break;
       const double sig = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-      const int cnt = sturm_count(s.dd, s.ee, N, sig, pivmin);
+      const int cnt = sturm_count(s.dd, s.p, N, sig, pivmin);
       const unsigned mask = __ballot_sync(0xffffffffu, cnt >= asc + 1);
       const int first = mask ? __ffs(mask) - 1 : 32;
       const double nhi = (first < 32) ? lo + (hi - lo) * (double)(first + 1) / 33.0 : hi;
@@ -215,20 +224,23 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
         const double b = s.ee[i];  // sub-diagonal entry below the pivot
         const double dn = s.dd[i + 1] - lam;
         const double cn = (i + 2 < N) ? s.ee[i + 1] : 0.0;
+        // u0 keeps the reciprocal pivot (guarded away from zero), so the
+        // solves below only multiply
         if (fabs(a0) >= fabs(b)) {
-          const double piv = (a0 == 0.0) ? tiny : a0;
-          const double l = b / piv;
-          u0[i] = piv; u1[i] = c0; u2[i] = 0.0; lm[i] = l; swp[i] = 0;
+          const double piv = (fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0;
+          const double rp = fast_rcp(piv);
+          const double l = b * rp;
+          u0[i] = rp; u1[i] = c0; u2[i] = 0.0; lm[i] = l; swp[i] = 0;
           a0 = dn - l * c0;
           c0 = cn;
         } else {
-          const double l = a0 / b;
-          u0[i] = b; u1[i] = dn; u2[i] = cn; lm[i] = l; swp[i] = 1;
+          const double l = a0 * fast_rcp(b);
+          u0[i] = fast_rcp(b); u1[i] = dn; u2[i] = cn; lm[i] = l; swp[i] = 1;
           a0 = c0 - l * dn;
           c0 = -l * cn;
         }
       }
-      u0[N - 1] = (a0 == 0.0) ? tiny : a0;
+      u0[N - 1] = fast_rcp((fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0);
       // deterministic pseudo-random start vector in (-0.5, 0.5), three solves
       for (int i = 0; i < N; ++i) {
         unsigned h = (unsigned)(i + 1) * 2654435761u ^ (unsigned)(jj + 7) * 40503u;
@@ -237,7 +249,7 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
         h ^= h >> 15;
         z[i] = (double)(h & 0xffffff) / 16777216.0 - 0.5;
       }
-      for (int iter = 0; iter < 3; ++iter) {
+      for (int iter = 0; iter < 2; ++iter) {
         // forward: apply L^-1 with the recorded swaps
         for (int i = 0; i < N - 1; ++i) {
           if (swp[i]) {
@@ -253,8 +265,7 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
           double t = z[i];
           if (i + 1 < N) t -= u1[i] * z[i + 1];
           if (i + 2 < N) t -= u2[i] * z[i + 2];
-          const double piv = (fabs(u0[i]) < tiny) ? copysign(tiny, u0[i] == 0.0 ? 1.0 : u0[i]) : u0[i];
-          z[i] = t / piv;
+          z[i] = t * u0[i];
         }
         // re-orthogonalise against earlier cluster members, normalise
         for (int q = j; q < jj; ++q) {

@@ -21,11 +21,11 @@ class Engine:
     reduction over the n/m dimension is completed with an allreduce, so the
     callers (solver.py) are identical for 1 and N GPUs."""
 
-    def __init__(self, dp: DeviceProblem, comm=None):
+    def __init__(self, dp: DeviceProblem, comm=None, h=None):
         self.dp = dp
         self.rt: Runtime = dp.rt
         self.lib = self.rt.lib
-        self.h = self.rt.h
+        self.h = h or self.rt.h  # context (and therefore stream) the kernels go to
         self.n, self.m = dp.n, dp.m
         self.comm = comm if (comm is not None and comm.world > 1) else None
         self._red2 = None
@@ -92,6 +92,8 @@ class Engine:
 
     # ---------------------------------------------------------------- operator / constraints
     def apply(self, which, V, out, gram=None):
+        if self.h is not self.rt.h:
+            return self.dp.apply(which, V, out=out, gram=gram, h=self.h)
         return self.dp.apply(which, V, out=out, gram=gram)
 
     def image(self, V, S, out, s_is_diag=False, s_scale=1.0, beta=0.0, beta_dev=None, base=None):

@@ -364,15 +364,21 @@ class DeviceSolver:
         self.lamc = rt.empty(max(self.k_c, 1))
         self.ident = rt.upload(np.eye(max(k, 1)))
         self.lz_probe = None  # list -> (start, end, restarts, matvecs) per Lanczos call
+        # overlap the model-evaluation IPM with the Lanczos kernel (single GPU,
+        # CUDA runtime only; USBS_NO_OVERLAP=1 disables it)
+        import os
+        self.overlap = (self.shard is None and engine is None and hasattr(self.rt, "aux")
+                        and not os.environ.get("USBS_NO_OVERLAP"))
+        self.eng_aux = Engine(self.dp, None, h=self.rt.aux()[1]) if self.overlap else None
 
     # ------------------------------------------------------------ helpers
     def _fetch(self, *tensors):
         """One synchronising D2H of several small device arrays."""
         return [t.cpu().numpy() for t in tensors]
 
-    def penalized_lanczos(self, y_dev, which=1):
+    def penalized_lanczos(self, y_dev, which=1, assembled=False):
         """penalized_obj (bundle.py:212-236) minus the <b,y> term (device dot)."""
-        if which == 1:
+        if which == 1 and not assembled:
             self.dp.assemble(y_dev)
         op = DeviceLinOp(self.dp, which)
         inner, rst, tol = self.lz
@@ -665,21 +671,27 @@ class DeviceSolver:
                     out=self.ycand)
             if self.has_ineq:
                 eng.vec(N.VOP_MINI, self.m, x=self.ycand, ineq=self.ineq, red=sc[S_MINI:S_MINI + 2])
-            eig = self.penalized_lanczos(self.ycand)
-            lam_c = float(eig.eigenvalues[0])
-            # ipm_eval(assemble_eval_coeffs(prob, model, y_cand)) (subqp.py:455-468)
             tr = model.stats.trace
-            eng.apply(1, model.basis_dev, self.tmp_nk2[:, :k], gram=self.zq)
-            eng.svec(self.zq, self.lin_s, scale=-a)
-            eng.dot_into(self.ycand[:1], self.ycand[:1], sc[S_EQ22:S_EQ22 + 1], scale=0.0)
-            if tr > 0.0:
-                eng.dot_into(self.ycand, model.stats.constr_image_dev, sc[S_ELINETA:S_ELINETA + 1],
-                             scale=a / tr, shift=-(a / tr) * model.stats.cost_ip)
+            if self.overlap:
+                # the model evaluation at y_cand (assemble_eval_coeffs + ipm_eval,
+                # subqp.py:455-468) depends only on the assembled Z, so it runs on a
+                # second stream concurrently with the Lanczos kernel (which leaves
+                # a few SMs free for it)
+                torch = self.rt.torch
+                self.dp.assemble(self.ycand)
+                aux_stream, _ = self.rt.aux()
+                ev0 = torch.cuda.Event()
+                ev0.record(self.rt.stream)
+                aux_stream.wait_event(ev0)
+                self._eval_at_candidate(self.eng_aux, model, k, tr)
+                ev1 = torch.cuda.Event()
+                ev1.record(aux_stream)
+                eig = self.penalized_lanczos(self.ycand, assembled=True)
+                self.rt.stream.wait_event(ev1)
             else:
-                eng.dot_into(self.ycand[:1], self.ycand[:1], sc[S_ELINETA:S_ELINETA + 1], scale=0.0)
-            eng.ipm(k, tr > 0.0, None, None, self.lin_s, sc[S_EQ22:S_EQ22 + 2], None, self.st_e, self.res_e,
-                    self.opts)
-            eng.dot_into(self.b, self.ycand, sc[S_BYC:S_BYC + 1])
+                eig = self.penalized_lanczos(self.ycand)
+                self._eval_at_candidate(eng, model, k, tr)
+            lam_c = float(eig.eigenvalues[0])
             # s_act = alpha S (original units) for model_update
             S = self.st_q[:k * k].view(k, k)
             eng.vec(N.VOP_AXPBY, k * k, x=S.reshape(-1), s0=a, out=self.s_act.view(-1))
@@ -720,6 +732,22 @@ class DeviceSolver:
         state.last_primal = AggregateStats(state.last_primal.trace, state.last_primal.cost_ip,
                                            state.last_primal.constr_image_dev.clone())
         return state, self.primal_output(model)
+
+    def _eval_at_candidate(self, eng, model, k, tr):
+        """ipm_eval(assemble_eval_coeffs(prob, model, y_cand)) (subqp.py:455-468)
+        and <b, y_cand>, launched through `eng` (main or auxiliary stream)."""
+        sc, a = self.sc, self.alpha
+        eng.apply(1, model.basis_dev, self.tmp_nk2[:, :k], gram=self.zq)
+        eng.svec(self.zq, self.lin_s, scale=-a)
+        eng.dot_into(self.ycand[:1], self.ycand[:1], sc[S_EQ22:S_EQ22 + 1], scale=0.0)
+        if tr > 0.0:
+            eng.dot_into(self.ycand, model.stats.constr_image_dev, sc[S_ELINETA:S_ELINETA + 1],
+                         scale=a / tr, shift=-(a / tr) * model.stats.cost_ip)
+        else:
+            eng.dot_into(self.ycand[:1], self.ycand[:1], sc[S_ELINETA:S_ELINETA + 1], scale=0.0)
+        eng.ipm(k, tr > 0.0, None, None, self.lin_s, sc[S_EQ22:S_EQ22 + 2], None, self.st_e, self.res_e,
+                self.opts)
+        eng.dot_into(self.b, self.ycand, sc[S_BYC:S_BYC + 1])
 
     def residuals(self, y, f_y, lam_y, primal, pending=None, model=None) -> Residuals:
         """compute_residuals (bundle.py:344-372); also finalises the pending
