@@ -124,6 +124,14 @@ usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int which, int k_c,
  * end of cycle, Rayleigh-Ritz, restart.  reset != 0 zeroes them. */
 usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* out_host, int reset);
 
+/* Execution plan usbs_lanczos_top uses for basis size m on p: *cluster_size
+ * CTAs in one thread-block cluster holding *rows_per_cta rows of Q each in
+ * shared memory, or *cluster_size = 0 for the grid-wide cooperative kernel
+ * (*rows_per_cta = 0).  The environment variable USBS_LZ_CLUSTER=0, read when
+ * the plan is first made for p, forces the grid kernel. */
+usbs_status usbs_lanczos_plan(usbs_ctx* ctx, usbs_problem* p, int m, int* cluster_size,
+                              int* rows_per_cta);
+
 /* ---- K3: small symmetric eigendecomposition ----------------------------- */
 /* small_eigh (symlin.py:193-198): symmetrise, eigendecompose, descending.
  * k <= 64; a_dev, vals_dev (k), vecs_dev (k x k, columns = eigenvectors). */

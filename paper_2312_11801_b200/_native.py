@@ -48,6 +48,7 @@ PROTOS = {
                                  _pd, _p, _i64, _pd, _pi, _pi, _pd, _pi, _pi]),
     "usbs_small_eigh": (_i32, [_p, _i32, _p, _p, _p]),
     "usbs_lanczos_profile": (_i32, [_p, C.POINTER(C.c_uint64), _i32]),
+    "usbs_lanczos_plan": (_i32, [_p, _p, _i32, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "usbs_ipm_solve": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "usbs_ipm_state_len": (_i32, [_i32]),
     "usbs_ipm_profile": (_i32, [_p, C.POINTER(C.c_uint64), _i32]),

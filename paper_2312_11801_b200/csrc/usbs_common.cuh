@@ -117,6 +117,10 @@ struct usbs_problem {
   // rows [blk_row[b], blk_row[b+1]); split rows [blk_sr[b], blk_sr[b+1])
   int lz_blocks = 0;
   int spmv_group = 32;
+  // cached cluster-Lanczos plan (usbs_lanczos.cu): basis size it was made
+  // for, cluster size (0 = grid kernel), rows per CTA, dynamic smem bytes
+  int lz_cl_m = -1, lz_cl_cs = 0, lz_cl_R = 0, lz_cl_lg = 32;  // lg: SpMV lanes per row
+  size_t lz_cl_smem = 0;
   int* blk_item = nullptr;
   int* blk_row = nullptr;
   int* blk_sr = nullptr;

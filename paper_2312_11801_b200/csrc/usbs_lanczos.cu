@@ -372,8 +372,6 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
     grid.sync();
     LZ_MARK(4);
     // Rayleigh-Ritz (every block, identical)
-    for (int x = tid; x < m * m; x += nth) js.A[x] = a.H[(x / m) * M1 + (x % m)];
-    __syncthreads();
     // only the nw leading Ritz pairs are used: theta/Y[:, :ell] for the
     // restart, theta/Y[:, :k_c] for the output and the residual test
     const int ell_next = max(1, min(a.k_c + 3, m - 2));
@@ -390,7 +388,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       ts.lam = ts.ee + 64;
       ts.red = ts.lam + 64;
       ts.iw = (int*)(ts.red + 64);
-      rr_topk(m, nwant, cycle == 0 ? 1 : 0, ts, thetaS, Ys, m, (a.prof && b == 0) ? a.prof + 8 : nullptr);
+      rr_arrow(m, ell, nwant, a.H, M1, ts, thetaS, Ys, m, (a.prof && b == 0) ? a.prof + 8 : nullptr);
     }
     LZ_MARK(5);
     const double beta_last = a.H[m * M1 + (m - 1)];
@@ -459,6 +457,373 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
     a.flags[F_NHIST] = nhist;
     a.flags[F_MATVECS] = matvecs;
   }
+}
+
+// ------------------------------------------------------------ cluster variant
+// Small operators (n <= ~10^4, m <= 32): the same algorithm on ONE thread-block
+// cluster of CS CTAs (one per SM).  The Lanczos basis Q and the w vectors of
+// a CTA's contiguous R rows live in its shared memory for the whole call;
+// the SpMV gathers remote q_j / w'' entries through distributed shared memory
+// and the cross-CTA partial sums are read from the owners' smem, so a step
+// costs 3 cluster barriers (~0.2 us) instead of 3 grid barriers (~1.6 us)
+// and no L2 round trips for Q.  Breakdown exits spill Q to global so the
+// host can reseed exactly as in the grid variant.
+template <int LG>
+__global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int m = a.m, M1 = m + 1;
+  const int tid = threadIdx.x, nth = blockDim.x, nw = nth >> 5, lane = tid & 31, warp = tid >> 5;
+  const int b = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
+  const int r0 = min(a.n, b * R), r1 = min(a.n, r0 + R), nloc = r1 - r0;
+
+  double* Qs = (double*)smem_raw;   // M1 * R, column-major (ld R), local rows
+  double* W0s = Qs + (size_t)M1 * R;  // R
+  double* W1s = W0s + R;             // R
+  double* P1s = W1s + R;             // 64 own partials (read by every CTA)
+  double* P2s = P1s + 64;            // 64
+  double* P3s = P2s + 64;            // 8
+  double* wred = P3s + 8;            // nw * 32
+  double* cvec = wred + nw * 32;     // 64
+  double* c2vec = cvec + 64;         // 64
+  double* red = c2vec + 64;          // 64
+  double* misc = red + 64;           // 8
+  double* thetaS = misc + 8;         // 64
+  double* Ys = thetaS + 64;          // m*m
+  TriSmem ts;
+  ts.A = Ys + m * m;
+  ts.Q = ts.A + m * m;
+  ts.Z = ts.Q + m * m;
+  ts.v = ts.Z + m * m;
+  ts.p = ts.v + 64;
+  ts.dd = ts.p + 64;
+  ts.ee = ts.dd + 64;
+  ts.lam = ts.ee + 64;
+  ts.red = ts.lam + 64;
+  ts.iw = (int*)(ts.red + 64);
+  int* rp = ts.iw + 128;  // R + 1 own row pointers
+
+  // Q for the own rows from global (start vector / restart state / reseed)
+  for (int x = tid; x < M1 * nloc; x += nth) {
+    const int t = x / nloc, i = x % nloc;
+    Qs[(size_t)t * R + i] = a.Q[(int64_t)t * a.ldq + r0 + i];
+  }
+  for (int i = tid; i <= nloc; i += nth) rp[i] = a.rowptr[r0 + i];
+  cluster.sync();
+
+  int cycle = a.cycle0, ell = a.ell0, jstart = a.j0, restarts = a.restarts0, nhist = a.nhist0;
+  int matvecs = a.matvecs0, wb = a.wbuf0;
+  double beta = a.beta_prev;
+  bool from_q = a.first_from_q != 0;
+  bool pending = false;
+  int converged = 0;
+  unsigned long long lz_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long lz_last = (a.prof && b == 0 && tid == 0) ? gtimer() : 0ull;
+
+  for (; cycle <= a.max_restarts; ++cycle) {
+    for (int j = jstart; j < m; ++j) {
+      double* Wprev = wb ? W1s : W0s;
+      double* Wcur = wb ? W0s : W1s;
+      // ------------------------------------------------------------ phase A
+      const double* xloc = from_q ? Qs + (size_t)j * R : Wprev;
+      const double xs = from_q ? 1.0 : 1.0 / beta;
+      if (!from_q) {
+        for (int i = tid; i < nloc; i += nth) Qs[(size_t)j * R + i] = Wprev[i] * xs;
+        if (b == 0 && tid == 0) {
+          a.H[j * M1 + (j - 1)] = beta;
+          a.H[(j - 1) * M1 + j] = beta;
+        }
+      }
+      // x[c] lives in CTA c / R (own smem for the local band, DSMEM otherwise)
+      auto gather = [&](int c) -> double {
+        const int owner = c / R, li = c - owner * R;
+        const double* src = owner == b ? xloc : cluster.map_shared_rank(xloc, owner);
+        return src[li];
+      };
+      if constexpr (LG == 1) {
+        // short rows: one thread per row, two rows in flight per thread and
+        // the row's loads batched by U so the col -> gather chains overlap
+        constexpr int U = 8;
+        for (int il = tid; il < nloc; il += 2 * nth) {
+          const int il2 = il + nth;
+          const bool two = il2 < nloc;
+          int z1 = rp[il];
+          const int e1 = rp[il + 1];
+          int z2 = two ? rp[il2] : 0;
+          const int e2 = two ? rp[il2 + 1] : 0;
+          double acc1 = 0.0, acc2 = 0.0;
+          while (z1 < e1 || z2 < e2) {
+            int c1[U], c2[U];
+            double v1[U], v2[U], x1[U], x2[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const bool o1 = z1 + u < e1, o2 = z2 + u < e2;
+              c1[u] = o1 ? a.col[z1 + u] : -1;
+              v1[u] = o1 ? a.val[z1 + u] : 0.0;
+              c2[u] = o2 ? a.col[z2 + u] : -1;
+              v2[u] = o2 ? a.val[z2 + u] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              x1[u] = c1[u] >= 0 ? gather(c1[u]) : 0.0;
+              x2[u] = c2[u] >= 0 ? gather(c2[u]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (c1[u] >= 0) acc1 = fma(v1[u], x1[u] * xs, acc1);
+              if (c2[u] >= 0) acc2 = fma(v2[u], x2[u] * xs, acc2);
+            }
+            z1 += U;
+            z2 += U;
+          }
+          Wcur[il] = acc1;
+          if (two) Wcur[il2] = acc2;
+        }
+      } else {
+        constexpr int GPW = 32 / LG;
+        const int gw = lane / LG, t = lane % LG;
+        for (int base = warp * GPW; base < nloc; base += nw * GPW) {
+          const int il = base + gw;
+          const bool ok = il < nloc;
+          double acc = 0.0;
+          if (ok) {
+            const int rb = rp[il], re = rp[il + 1];
+            for (int z = rb + t; z < re; z += LG) acc = fma(a.val[z], gather(a.col[z]) * xs, acc);
+          }
+          acc = group_sum<LG>(acc);
+          if (ok && t == 0) Wcur[il] = acc;
+        }
+      }
+      __syncthreads();
+      LZ_MARK(7);
+      ++matvecs;
+      {
+        // partial Q^T w over the own rows (warp butterfly, Q from smem)
+        int bad = 0;
+        double acc = 0.0;
+        for (int base = warp * 32; base < nloc; base += nw * 32) {
+          const int il = base + lane;
+          const bool live = il < nloc;
+          double q[32];
+          const double w = live ? Wcur[il] : 0.0;
+          if (live && !isfinite(w)) bad = 1;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) q[t] = (live && t <= j) ? Qs[(size_t)t * R + il] * w : 0.0;
+          acc += butterfly32(q);
+        }
+        wred[warp * 32 + lane] = acc;
+        if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.flags[F_NONFINITE], 1);
+        if (tid < 32) {
+          double s = 0.0;
+          for (int w2 = 0; w2 < nw; ++w2) s += wred[w2 * 32 + tid];
+          P1s[tid] = s;
+        }
+      }
+      LZ_MARK(0);
+      cluster.sync();
+      LZ_MARK(1);
+      // ------------------------------------------------------------ phase B
+      if (*(volatile int*)&a.flags[F_NONFINITE]) {
+        if (b == 0 && tid == 0) {
+          a.flags[F_EXIT] = EXIT_NONFINITE;
+          a.flags[F_MATVECS] = matvecs;
+        }
+        cluster.sync();
+        return;
+      }
+      for (int t = warp; t <= j; t += nw) {  // c = sum over CTAs (fixed order)
+        double s = lane < CS ? cluster.map_shared_rank(P1s, lane)[t] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) cvec[t] = s;
+      }
+      __syncthreads();
+      {
+        double acc = 0.0;
+        for (int base = warp * 32; base < nloc; base += nw * 32) {
+          const int il = base + lane;
+          const bool live = il < nloc;
+          double q[32];
+          double s = 0.0;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            q[t] = (live && t <= j) ? Qs[(size_t)t * R + il] : 0.0;
+            s = fma(q[t], (t <= j) ? cvec[t] : 0.0, s);
+          }
+          double w = 0.0;
+          if (live) {
+            w = Wcur[il] - s;
+            Wcur[il] = w;
+          }
+#pragma unroll
+          for (int t = 0; t < 32; ++t) q[t] *= w;
+          acc += butterfly32(q);
+        }
+        wred[warp * 32 + lane] = acc;
+        __syncthreads();
+        if (tid < 32) {
+          double s = 0.0;
+          for (int w2 = 0; w2 < nw; ++w2) s += wred[w2 * 32 + tid];
+          P2s[tid] = s;
+        }
+      }
+      LZ_MARK(2);
+      cluster.sync();
+      LZ_MARK(1);
+      // ------------------------------------------------------------ phase C
+      for (int t = warp; t <= j; t += nw) {
+        double s = lane < CS ? cluster.map_shared_rank(P2s, lane)[t] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) c2vec[t] = s;
+      }
+      __syncthreads();
+      {
+        double ss = 0.0;
+        for (int il = tid; il < nloc; il += nth) {
+          double s = 0.0;
+          for (int t = 0; t <= j; ++t) s = fma(Qs[(size_t)t * R + il], c2vec[t], s);
+          const double w = Wcur[il] - s;
+          Wcur[il] = w;
+          ss = fma(w, w, ss);
+        }
+        ss = block_sum(ss, red);
+        if (tid == 0) P3s[0] = ss;
+      }
+      for (int t = tid; t <= j; t += nth) cvec[t] += c2vec[t];
+      __syncthreads();
+      if (b == 0)
+        for (int t = tid; t <= j; t += nth) {
+          a.H[t * M1 + j] = cvec[t];
+          a.H[j * M1 + t] = cvec[t];
+        }
+      if (tid == 0) {
+        double mx = 0.0;
+        for (int t = 0; t <= j; ++t) mx = fmax(mx, fabs(cvec[t]));
+        misc[0] = fmax(1.0, mx);
+      }
+      LZ_MARK(3);
+      cluster.sync();
+      LZ_MARK(1);
+      if (tid < 32) {
+        double s = tid < CS ? cluster.map_shared_rank(P3s, tid)[0] : 0.0;
+        s = warp_sum(s);
+        if (tid == 0) misc[1] = sqrt(s);
+      }
+      __syncthreads();
+      beta = misc[1];
+      const double scale = misc[0];
+      wb ^= 1;
+      from_q = false;
+      if (beta <= 1e-13 * scale) {
+        // spill Q for the host reseed (the host uses columns 0..j)
+        for (int x = tid; x < M1 * nloc; x += nth) {
+          const int t = x / nloc, i = x % nloc;
+          a.Q[(int64_t)t * a.ldq + r0 + i] = Qs[(size_t)t * R + i];
+        }
+        if (b == 0 && tid == 0) {
+          a.flags[F_EXIT] = EXIT_BREAKDOWN;
+          a.flags[F_J] = j;
+          a.flags[F_CYCLE] = cycle;
+          a.flags[F_ELL] = ell;
+          a.flags[F_RESTARTS] = restarts;
+          a.flags[F_NHIST] = nhist;
+          a.flags[F_MATVECS] = matvecs;
+          a.flags[F_PENDING] = wb;
+        }
+        cluster.sync();  // remote readers of this CTA's smem are done
+        return;
+      }
+      pending = (j == m - 1);
+      // the next phase A reads the other CTAs' Wcur (now Wprev): the barrier
+      // above already orders it; P1s/P2s/P3s are rewritten only after two
+      // more barriers
+    }
+    // ---------------------------------------------------------- end of cycle
+    if (pending) {
+      double* Wprev = wb ? W1s : W0s;
+      const double xs = 1.0 / beta;
+      for (int i = tid; i < nloc; i += nth) Qs[(size_t)m * R + i] = Wprev[i] * xs;
+      if (b == 0 && tid == 0) {
+        a.H[m * M1 + (m - 1)] = beta;
+        a.H[(m - 1) * M1 + m] = beta;
+      }
+      pending = false;
+    }
+    __threadfence();
+    cluster.sync();
+    LZ_MARK(4);
+    const int ell_next = max(1, min(a.k_c + 3, m - 2));
+    const int nwant = min(m, max(ell_next, a.k_c));
+    rr_arrow(m, ell, nwant, a.H, M1, ts, thetaS, Ys, m, (a.prof && b == 0) ? a.prof + 8 : nullptr);
+    LZ_MARK(5);
+    const double beta_last = a.H[m * M1 + (m - 1)];
+    if (tid == 0) {
+      bool ok = true;
+      const double tol_eff = a.tol * (1.0 + fabs(thetaS[0]));
+      for (int u = 0; u < a.k_c; ++u) {
+        const double r = fabs(beta_last * Ys[(m - 1) * m + u]);
+        if (!(r <= tol_eff)) ok = false;
+      }
+      misc[2] = ok ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (b == 0) {
+      for (int u = tid; u < nwant; u += nth) {
+        a.theta[u] = thetaS[u];
+        a.res[u] = fabs(beta_last * Ys[(m - 1) * m + u]);
+      }
+      if (tid == 0) a.hist[nhist] = thetaS[0];
+    }
+    ++nhist;
+    if (misc[2] != 0.0) { converged = 1; break; }
+    if (cycle == a.max_restarts) break;
+    ell = ell_next;
+    for (int il = tid; il < nloc; il += nth) {
+      double qrow[32];
+      for (int t = 0; t < m; ++t) qrow[t] = Qs[(size_t)t * R + il];
+      for (int u = 0; u < ell; ++u) {
+        double s = 0.0;
+        for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
+        Qs[(size_t)u * R + il] = s;
+      }
+      Qs[(size_t)ell * R + il] = Qs[(size_t)m * R + il];
+    }
+    ++restarts;
+    jstart = ell;
+    from_q = true;
+    cluster.sync();
+    if (b == 0) {
+      for (int x = tid; x < M1 * M1; x += nth) a.H[x] = 0.0;
+      __syncthreads();
+      for (int u = tid; u < ell; u += nth) a.H[u * M1 + u] = thetaS[u];
+      __syncthreads();
+    }
+    LZ_MARK(6);
+  }
+  if (a.prof && b == 0 && tid == 0)
+    for (int s = 0; s < 8; ++s) a.prof[s] += lz_acc[s];
+  for (int il = tid; il < nloc; il += nth) {
+    double qrow[32];
+    for (int t = 0; t < m; ++t) qrow[t] = Qs[(size_t)t * R + il];
+    for (int u = 0; u < a.k_c; ++u) {
+      double s = 0.0;
+      for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
+      a.vecs_out[(int64_t)(r0 + il) * a.ldvecs + u] = s;
+    }
+  }
+  if (b == 0 && tid == 0) {
+    a.flags[F_EXIT] = EXIT_DONE;
+    a.flags[F_CONV] = converged;
+    a.flags[F_RESTARTS] = restarts;
+    a.flags[F_NHIST] = nhist;
+    a.flags[F_MATVECS] = matvecs;
+  }
+  cluster.sync();  // keep smem alive until every remote read is done
+}
+
+static size_t lz_cl_smem(int m, int R, int nth) {
+  const int M1 = m + 1, nw = nth / 32;
+  return (size_t)((size_t)M1 * R + 2 * R + 64 + 64 + 8 + nw * 32 + 64 * 3 + 8 + 64 + 4 * m * m + 6 * 64) *
+             sizeof(double) + (128 + R + 1) * sizeof(int) + 64;
 }
 
 // ------------------------------------------------------------ small kernels
@@ -597,6 +962,122 @@ static void lz_launch(usbs_ctx* ctx, LzArgs& a, int G, size_t smem) {
   check_launch(ctx);
 }
 
+// Cluster plan for the small-n variant: CS CTAs in one cluster, R rows each.
+struct LzClusterPlan {
+  int cs = 0, R = 0, lg = 32;
+  size_t smem = 0;
+};
+
+template <int LG>
+static int lz_cl_max_clusters(int cs, size_t smem) {
+  auto fn = k_lanczos_cl<LG>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, (void*)fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nc;
+}
+
+static int lz_cl_max_clusters_lg(int LG, int cs, size_t smem) {
+  switch (LG) {
+    case 1: return lz_cl_max_clusters<1>(cs, smem);
+    case 4: return lz_cl_max_clusters<4>(cs, smem);
+    case 8: return lz_cl_max_clusters<8>(cs, smem);
+    case 16: return lz_cl_max_clusters<16>(cs, smem);
+    default: return lz_cl_max_clusters<32>(cs, smem);
+  }
+}
+
+// Picks the largest cluster (16, else 8) whose per-CTA Q slice fits in shared
+// memory and that the device can schedule; cs = 0 means "use the grid kernel".
+static LzClusterPlan lz_cluster_plan(usbs_ctx* ctx, int64_t n, int64_t nnz, int m, int LG) {
+  LzClusterPlan pl;
+  // short rows (<= 16 nnz on average): thread per row; else the grid
+  // kernel's group size
+  if (nnz <= 16 * n) LG = 1;
+  const char* e = getenv("USBS_LZ_CLUSTER");
+  if (e && e[0] == '0') return pl;
+  if (m > 32) return pl;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  for (int cs : {16, 8}) {
+    const int64_t R = (n + cs - 1) / cs;
+    if (R < 32) continue;  // tiny operators: one warp-row per CTA at least
+    const size_t sm = lz_cl_smem(m, (int)R, 512);
+    if (sm > (size_t)optin) continue;
+    if (lz_cl_max_clusters_lg(LG, cs, sm) < 1) continue;
+    pl.cs = cs;
+    pl.R = (int)R;
+    pl.smem = sm;
+    pl.lg = LG;
+    return pl;
+  }
+  return pl;
+}
+
+// plan cached per (problem, basis size)
+static LzClusterPlan lz_cached_plan(usbs_ctx* ctx, usbs_problem* p, int m) {
+  if (p->lz_cl_m != m) {
+    const LzClusterPlan pl = lz_cluster_plan(ctx, p->n, p->nnz, m, p->spmv_group);
+    p->lz_cl_m = m;
+    p->lz_cl_cs = pl.cs;
+    p->lz_cl_R = pl.R;
+    p->lz_cl_lg = pl.lg;
+    p->lz_cl_smem = pl.smem;
+  }
+  LzClusterPlan pl;
+  pl.cs = p->lz_cl_cs;
+  pl.R = p->lz_cl_R;
+  pl.lg = p->lz_cl_lg;
+  pl.smem = p->lz_cl_smem;
+  return pl;
+}
+
+template <int LG>
+static void lz_cl_launch_t(usbs_ctx* ctx, LzArgs& a, const LzClusterPlan& pl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.cs);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = pl.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  USBS_CUDA(cudaLaunchKernelEx(&cfg, k_lanczos_cl<LG>, a, pl.R));
+  check_launch(ctx);
+}
+
+static void lz_cl_launch(usbs_ctx* ctx, LzArgs& a, const LzClusterPlan& pl) {
+  switch (pl.lg) {
+    case 1: lz_cl_launch_t<1>(ctx, a, pl); break;
+    case 4: lz_cl_launch_t<4>(ctx, a, pl); break;
+    case 8: lz_cl_launch_t<8>(ctx, a, pl); break;
+    case 16: lz_cl_launch_t<16>(ctx, a, pl); break;
+    default: lz_cl_launch_t<32>(ctx, a, pl); break;
+  }
+}
+
 template <int NH>
 static void lz_dispatch(usbs_ctx* ctx, LzArgs& a, int G, int LG, size_t smem) {
   switch (LG) {
@@ -619,6 +1100,16 @@ extern "C" usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* o
   USBS_CUDA(cudaMemcpyAsync(out, p, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   USBS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 16 * sizeof(unsigned long long), ctx->stream));
+  USBS_API_END
+}
+
+extern "C" usbs_status usbs_lanczos_plan(usbs_ctx* ctx, usbs_problem* p, int m, int* cluster_size,
+                                         int* rows_per_cta) {
+  USBS_API_BEGIN
+  if (m < 2 || m > 64) fail(USBS_ERR_CONFIG, "Lanczos basis size must be in [2, 64]");
+  const LzClusterPlan pl = (p->n_cols == p->n) ? lz_cached_plan(ctx, p, m) : LzClusterPlan{};
+  *cluster_size = pl.cs;
+  *rows_per_cta = pl.R;
   USBS_API_END
 }
 
@@ -714,11 +1205,14 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
 
   const int nw = (NH == 1 ? 512 : 256) / 32;
   size_t smem = (size_t)(nw * 32 * NH + 64 * 3 + 8 + 64 + m * m + 4 * m * m + 64 * 2 + 32) * sizeof(double) +
-                68 * sizeof(int) + JAC_PTAB_BYTES + (6 * 64) * sizeof(double) + 64 * sizeof(int) + 64;
+                68 * sizeof(int) + JAC_PTAB_BYTES + (6 * 64) * sizeof(double) + 128 * sizeof(int) + 64;
+  // small operators: one thread-block cluster with Q resident in smem
+  const LzClusterPlan clp = lz_cached_plan(ctx, p, m);
   int64_t ctr = 0;
   int* hf = ctx->pinned_i;
   for (;;) {
-    if (NH == 1) lz_dispatch<1>(ctx, a, G, p->spmv_group, smem);
+    if (clp.cs > 0) lz_cl_launch(ctx, a, clp);
+    else if (NH == 1) lz_dispatch<1>(ctx, a, G, p->spmv_group, smem);
     else lz_dispatch<2>(ctx, a, G, p->spmv_group, smem);
     USBS_CUDA(cudaMemcpyAsync(hf, flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
     USBS_CUDA(cudaStreamSynchronize(st));

@@ -30,7 +30,7 @@ struct TriSmem {
   double* ee;   // N off-diagonal of T
   double* lam;  // 64 eigenvalues (descending)
   double* red;  // 64
-  int* iw;      // 64
+  int* iw;      // 128
 };
 
 // 1/q to ~1 ulp: FP32 MUFU seed + two Newton steps (4 dependent DFMA), exact
@@ -44,24 +44,73 @@ __device__ __forceinline__ double fast_rcp(double q) {
   return r;
 }
 
-// number of eigenvalues of T below sigma (LDL^T pivot signs, Kahan's form);
-// e2[i] = e[i]^2.  An approximate reciprocal perturbs e2 by ~1e-16 relative,
-// i.e. a backward-stable count.
-__device__ inline int sturm_count(const double* d, const double* e2, int N, double sigma, double pivmin) {
+// Top-k eigenpairs of the Lanczos projection H (m x m) for the Rayleigh-Ritz
+// step.  After a thick restart with ell kept Ritz pairs, H is an arrowhead
+// followed by a tridiagonal block:
+//
+//   H = [ diag(theta_0..theta_{ell-1})  b                       ]
+//       [ b^T                           d_ell  e_ell            ]
+//       [                               e_ell  d_ell+1  e_ell+1 ]
+//       [                                       ...             ]
+//
+// (ell = 0 in the first cycle: plain tridiagonal).  The entries outside this
+// pattern are the O(eps |H|) residue of the full reorthogonalisation; they are
+// ignored, which moves eigenvalues by O(eps |H|), the accuracy of eigh itself.
+// The structure is used directly, without a Householder reduction:
+//   Sturm counts  LDL^T of H - sigma I eliminating the arrow block first
+//                 (pivots theta_k - sigma), then the tridiagonal Schur
+//                 complement (first pivot d_ell - sigma - sum b_k^2/(theta_k -
+//                 sigma)); the tridiagonal part runs the three-term
+//                 leading-minor recurrence (one dependent FMA per row, rescaled
+//                 by powers of two every 4 rows); a pivot |q| < pivmin counts
+//                 as -pivmin as in LAPACK's ratio form.
+//   eigenvalues   multisection, one warp per eigenvalue, 32 shifts per sweep,
+//                 to |interval| <= 4 eps max|endpoint|.
+//   eigenvectors  inverse iteration, one thread per eigenvalue, all in
+//                 parallel: LU with partial pivoting of H - lam I (the arrow
+//                 block first: a swap makes the running arrow row a U row,
+//                 stored as its scale mu and its A_ell entry; then the
+//                 tridiagonal rows), two solves; eigenvalues closer than 1e-3 |H|
+//                 (LAPACK dstein's cluster rule) are perturbed apart and
+//                 modified-Gram-Schmidt orthogonalised after every solve.
+__device__ __forceinline__ void pow2_rescale(double& p, double& pm) {
+  const long long bits = __double_as_longlong(p);
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  if (ex > 0 && ex < 2046) {
+    const double sc = __longlong_as_double((long long)(2046 - ex) << 52);
+    p *= sc;
+    pm *= sc;
+  }
+}
+
+// number of eigenvalues of the arrowhead + tridiagonal H below sigma.
+// d: diagonal (theta_k for k < ell); sq: b_k^2 for k < ell, e_i^2 for i >= ell
+__device__ inline int sturm_arrow(int N, int ell, const double* d, const double* sq, double sigma, double pivmin) {
   int cnt = 0;
-  double q = d[0] - sigma;
-  if (fabs(q) < pivmin) q = -pivmin;
-  if (q < 0.0) ++cnt;
-  for (int i = 1; i < N; ++i) {
-    q = (d[i] - sigma) - e2[i - 1] * fast_rcp(q);
-    if (fabs(q) < pivmin) q = -pivmin;
-    if (q < 0.0) ++cnt;
+  double s = 0.0;
+  for (int k = 0; k < ell; ++k) {
+    double piv = d[k] - sigma;
+    if (fabs(piv) < pivmin) piv = -pivmin;
+    cnt += piv < 0.0;
+    s = fma(sq[k], fast_rcp(piv), s);
+  }
+  double pm = 1.0, p = (d[ell] - sigma) - s;
+  if (fabs(p) < pivmin) p = -pivmin;
+  cnt += p < 0.0;
+  for (int i = ell + 1; i < N; ++i) {
+    double pn = fma(d[i] - sigma, p, -sq[i - 1] * pm);
+    if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;
+    cnt += (pn < 0.0) != (p < 0.0);
+    pm = p;
+    p = pn;
+    if (((i - ell) & 3) == 0) pow2_rescale(p, pm);
   }
   return cnt;
 }
 
-// All threads of the block call.  tridiagonal != 0: A already tridiagonal.
-// Outputs: vals[0..nw) descending, Y (row-major N x nw, ld ldy).
+// All threads of the block call.  H: row-major with leading dimension ldh
+// (global or shared).  Outputs: vals[0..nw) descending, Y (row-major N x nw,
+// ld ldy; also used as scratch, so it must hold N * nw doubles).
 __device__ __forceinline__ unsigned long long tri_clock() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -77,95 +126,41 @@ __device__ __forceinline__ unsigned long long tri_clock() {
     }                                                   \
   } while (0)
 
-__device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double* vals, double* Y, int ldy,
-                               unsigned long long* tprof = nullptr) {
+__device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh, TriSmem s, double* vals, double* Y,
+                                int ldy, unsigned long long* tprof = nullptr) {
   unsigned long long tlast = (tprof && threadIdx.x == 0) ? tri_clock() : 0ull;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwp = nth >> 5;
-  double* A = s.A;
-  // ------------------------------------------------ 1. tridiagonalisation
-  for (int x = tid; x < N * N; x += nth) s.Q[x] = (x / N == x % N) ? 1.0 : 0.0;
-  __syncthreads();
-  if (!tridiagonal) {
-    for (int k = 0; k + 2 < N; ++k) {
-      const int L = N - k - 1;  // length of x = A[k+1.., k]
-      // Householder vector (warp 0): v(0) = 1, beta
-      if (warp == 0) {
-        double sg = 0.0;
-        for (int i = 1 + lane; i < L; i += 32) {
-          const double xi = A[(k + 1 + i) * N + k];
-          sg = fma(xi, xi, sg);
-        }
-        sg = warp_sum(sg);
-        const double x0 = A[(k + 1) * N + k];
-        double beta = 0.0, mu = x0, v0 = 1.0;
-        if (sg != 0.0) {
-          mu = sqrt(fma(x0, x0, sg));
-          v0 = (x0 <= 0.0) ? x0 - mu : -sg / (x0 + mu);
-          beta = 2.0 * v0 * v0 / (sg + v0 * v0);
-          // H x = mu e1 when x0 <= 0 ... GvL: H x = ||x|| e1
-        }
-        for (int i = lane; i < L; i += 32) s.v[i] = (i == 0) ? 1.0 : (sg != 0.0 ? A[(k + 1 + i) * N + k] / v0 : 0.0);
-        if (lane == 0) {
-          s.red[0] = beta;
-          s.red[1] = (sg != 0.0) ? mu : x0;
-        }
-      }
-      __syncthreads();
-      const double beta = s.red[0];
-      if (beta != 0.0) {
-        // p = beta A22 v (warp per row)
-        for (int i = warp; i < L; i += nwp) {
-          double t = 0.0;
-          for (int c = lane; c < L; c += 32) t = fma(A[(k + 1 + i) * N + (k + 1 + c)], s.v[c], t);
-          t = warp_sum(t);
-          if (lane == 0) s.p[i] = beta * t;
-        }
-        __syncthreads();
-        // every warp forms K = beta/2 p^T v itself (no extra barrier); rows of
-        // A22 -= v w^T + w v^T with w = p - K v, and Q[:, k+1:] -= beta (Q v) v^T
-        double K = 0.0;
-        for (int c = lane; c < L; c += 32) K = fma(s.p[c], s.v[c], K);
-        K = 0.5 * beta * warp_sum(K);
-        for (int i = warp; i < L; i += nwp) {
-          const double vi = s.v[i], wi = s.p[i] - K * vi;
-          double* row = A + (k + 1 + i) * N + (k + 1);
-          for (int c = lane; c < L; c += 32) {
-            const double vc = s.v[c];
-            row[c] -= vi * (s.p[c] - K * vc) + wi * vc;
-          }
-        }
-        for (int i = warp; i < N; i += nwp) {
-          double* row = s.Q + i * N + (k + 1);
-          double t = 0.0;
-          for (int c = lane; c < L; c += 32) t = fma(row[c], s.v[c], t);
-          t = beta * warp_sum(t);
-          for (int c = lane; c < L; c += 32) row[c] -= t * s.v[c];
-        }
-      }
-      if (tid == 0) {
-        A[(k + 1) * N + k] = s.red[1];
-        A[k * N + (k + 1)] = s.red[1];
-      }
-      for (int i = k + 2 + tid; i < N; i += nth) {
-        A[i * N + k] = 0.0;
-        A[k * N + i] = 0.0;
-      }
-      __syncthreads();
+  double* U0 = s.A;  // [i * nw + j]: reciprocal pivots (arrow: 1/(theta_k - lam))
+  double* U1 = s.Q;  // [i * nw + j]: first super-diagonal of U
+  double* LM = Y;    // [i * nw + j]: multipliers (Y is written last)
+  double* Z = s.Z;   // [i * nw + j]: eigenvectors
+  // ------------------------------------------------ 0. read the pattern
+  for (int i = tid; i < N; i += nth) {
+    s.dd[i] = H[(size_t)i * ldh + i];
+    if (i < ell) {
+      const double bk = H[(size_t)i * ldh + ell];
+      s.v[i] = bk;
+      s.p[i] = bk * bk;
+    } else {
+      const double ei = (i + 1 < N) ? H[(size_t)(i + 1) * ldh + i] : 0.0;
+      s.ee[i] = ei;
+      s.p[i] = ei * ei;
     }
   }
-  for (int i = tid; i < N; i += nth) {
-    s.dd[i] = A[i * N + i];
-    s.ee[i] = (i + 1 < N) ? A[(i + 1) * N + i] : 0.0;
-    s.p[i] = s.ee[i] * s.ee[i];  // e^2 for the Sturm counts
-  }
   __syncthreads();
-  TRI_MARK(0);
-  // ------------------------------------------------ 2. multisection bisection
+  // Gershgorin bounds and |H| (every thread, identical)
   double tnorm = 0.0, glo = 0.0, ghi = 0.0;
   {
-    double lo = INFINITY, hi = -INFINITY, nm = 0.0;
-    for (int i = 0; i < N; ++i) {
-      const double r = (i > 0 ? fabs(s.ee[i - 1]) : 0.0) + (i + 1 < N ? fabs(s.ee[i]) : 0.0);
+    double lo = INFINITY, hi = -INFINITY, nm = 0.0, bsum = 0.0;
+    for (int k = 0; k < ell; ++k) {
+      const double r = fabs(s.v[k]);
+      bsum += r;
+      lo = fmin(lo, s.dd[k] - r);
+      hi = fmax(hi, s.dd[k] + r);
+      nm = fmax(nm, fabs(s.dd[k]) + r);
+    }
+    for (int i = ell; i < N; ++i) {
+      const double r = (i > ell ? fabs(s.ee[i - 1]) : bsum) + (i + 1 < N ? fabs(s.ee[i]) : 0.0);
       lo = fmin(lo, s.dd[i] - r);
       hi = fmax(hi, s.dd[i] + r);
       nm = fmax(nm, fabs(s.dd[i]) + r);
@@ -176,13 +171,15 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
     ghi = hi + pad;
   }
   const double pivmin = 1e-300 + 2.2e-16 * 2.2e-16 * tnorm * tnorm;
+  TRI_MARK(0);
+  // ------------------------------------------------ 1. multisection
   for (int j = warp; j < nw; j += nwp) {
     const int asc = N - 1 - j;  // ascending index of the j-th largest
     double lo = glo, hi = ghi;
-    for (int it = 0; it < 16; ++it) {
-      if (hi - lo <= 2.2e-16 * fmax(fabs(lo), fabs(hi)) * 2.0 + 1e-300) break;
+    for (int it = 0; it < 24; ++it) {
+      if (hi - lo <= 4.4e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300) break;
       const double sig = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-      const int cnt = sturm_count(s.dd, s.p, N, sig, pivmin);
+      const int cnt = sturm_arrow(N, ell, s.dd, s.p, sig, pivmin);
       const unsigned mask = __ballot_sync(0xffffffffu, cnt >= asc + 1);
       const int first = mask ? __ffs(mask) - 1 : 32;
       const double nhi = (first < 32) ? lo + (hi - lo) * (double)(first + 1) / 33.0 : hi;
@@ -193,103 +190,180 @@ __device__ inline void rr_topk(int N, int nw, int tridiagonal, TriSmem s, double
     if (lane == 0) s.lam[j] = 0.5 * (lo + hi);
   }
   __syncthreads();
-  TRI_MARK(1);
-  // ------------------------------------------------ 3. inverse iteration
-  // cluster boundaries (descending order): new cluster when the gap exceeds 1e-3 |T|
+  // clusters (descending order): a new one when the gap exceeds 1e-3 |H|;
+  // iw[j] = position of j inside its cluster, iw[32 + j] = cluster id
   if (tid == 0) {
-    int c = 0;
+    int c = 0, pos = 0;
     for (int j = 0; j < nw; ++j) {
-      if (j > 0 && s.lam[j - 1] - s.lam[j] > 1e-3 * tnorm) ++c;
-      s.iw[j] = c;
+      if (j > 0 && s.lam[j - 1] - s.lam[j] > 1e-3 * tnorm) {
+        ++c;
+        pos = 0;
+      }
+      s.iw[j] = pos++;
+      s.iw[64 + j] = c;
     }
   }
   __syncthreads();
-  // one thread per eigenvalue solves (T - lam I) z = b twice; clusters are
-  // handled by their first member's thread, sequentially (re-orthogonalised)
+  TRI_MARK(1);
+  // ------------------------------------------------ 2. inverse iteration
   const double eps = 2.2e-16;
-  for (int j = tid; j < nw; j += nth) {
-    if (j > 0 && s.iw[j] == s.iw[j - 1]) continue;  // not a cluster leader
-    int jend = j;
-    while (jend + 1 < nw && s.iw[jend + 1] == s.iw[j]) ++jend;
-    for (int jj = j; jj <= jend; ++jj) {
-      // perturb members of a cluster apart as dstein does
-      const double lam = s.lam[jj] - (double)(jj - j) * 10.0 * eps * tnorm;
-      double* z = s.Z + (size_t)jj * N;
-      // LU with partial pivoting of T - lam I: rows hold (l, u0, u1, u2)
-      double u0[64], u1[64], u2[64], lm[64];
-      int swp[64];
-      double a0 = s.dd[0] - lam, c0 = N > 1 ? s.ee[0] : 0.0;
-      const double tiny = eps * tnorm + 1e-300;
-      for (int i = 0; i < N - 1; ++i) {
-        const double b = s.ee[i];  // sub-diagonal entry below the pivot
-        const double dn = s.dd[i + 1] - lam;
-        const double cn = (i + 2 < N) ? s.ee[i + 1] : 0.0;
-        // u0 keeps the reciprocal pivot (guarded away from zero), so the
-        // solves below only multiply
-        if (fabs(a0) >= fabs(b)) {
-          const double piv = (fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0;
-          const double rp = fast_rcp(piv);
-          const double l = b * rp;
-          u0[i] = rp; u1[i] = c0; u2[i] = 0.0; lm[i] = l; swp[i] = 0;
-          a0 = dn - l * c0;
-          c0 = cn;
-        } else {
-          const double l = a0 * fast_rcp(b);
-          u0[i] = fast_rcp(b); u1[i] = dn; u2[i] = cn; lm[i] = l; swp[i] = 1;
-          a0 = c0 - l * dn;
-          c0 = -l * cn;
-        }
-      }
-      u0[N - 1] = fast_rcp((fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0);
-      // deterministic pseudo-random start vector in (-0.5, 0.5), three solves
-      for (int i = 0; i < N; ++i) {
-        unsigned h = (unsigned)(i + 1) * 2654435761u ^ (unsigned)(jj + 7) * 40503u;
-        h ^= h >> 13;
-        h *= 0x5bd1e995u;
-        h ^= h >> 15;
-        z[i] = (double)(h & 0xffffff) / 16777216.0 - 0.5;
-      }
-      for (int iter = 0; iter < 2; ++iter) {
-        // forward: apply L^-1 with the recorded swaps
-        for (int i = 0; i < N - 1; ++i) {
-          if (swp[i]) {
-            const double t = z[i];
-            z[i] = z[i + 1];
-            z[i + 1] = t - lm[i] * z[i];
-          } else {
-            z[i + 1] -= lm[i] * z[i];
-          }
-        }
-        // backward: U z = y
-        for (int i = N - 1; i >= 0; --i) {
-          double t = z[i];
-          if (i + 1 < N) t -= u1[i] * z[i + 1];
-          if (i + 2 < N) t -= u2[i] * z[i + 2];
-          z[i] = t * u0[i];
-        }
-        // re-orthogonalise against earlier cluster members, normalise
-        for (int q = j; q < jj; ++q) {
-          const double* zq = s.Z + (size_t)q * N;
-          double dp = 0.0;
-          for (int i = 0; i < N; ++i) dp = fma(zq[i], z[i], dp);
-          for (int i = 0; i < N; ++i) z[i] -= dp * zq[i];
-        }
-        double nrm = 0.0;
-        for (int i = 0; i < N; ++i) nrm = fma(z[i], z[i], nrm);
-        nrm = sqrt(nrm);
-        const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-        for (int i = 0; i < N; ++i) z[i] *= inv;
+  const double tiny = eps * tnorm + 1e-300;
+  unsigned long long swp = 0ull;
+  if (tid < nw) {
+    const int j = tid;
+    const double lam = s.lam[j] - (double)s.iw[j] * 10.0 * eps * tnorm;
+    // arrow block by partial pivoting: column k's candidates are row k
+    // (theta_k - lam) and the running arrow row, whose entries in the
+    // columns still to come are mu * b_c (scaled by each swap), A_ell at
+    // column ell and mu * e_ell at column ell + 1
+    double mu = 1.0, aell = s.dd[ell] - lam;
+    for (int k = 0; k < ell; ++k) {
+      const double D = s.dd[k] - lam, ak = mu * s.v[k];
+      if (fabs(D) >= fabs(ak)) {
+        const double piv = (fabs(D) < tiny) ? copysign(tiny, D == 0.0 ? 1.0 : D) : D;
+        const double g = fast_rcp(piv);
+        const double l = ak * g;
+        U0[k * nw + j] = g;
+        LM[k * nw + j] = l;
+        aell = fma(-l, s.v[k], aell);
+      } else {
+        const double g = fast_rcp(ak);
+        const double l = D * g;
+        U0[k * nw + j] = g;
+        LM[k * nw + j] = l;
+        U1[k * nw + j] = aell;
+        swp |= 1ull << k;
+        mu = -l * mu;
+        aell = fma(-l, aell, s.v[k]);
       }
     }
+    double a0 = aell, c0 = (ell + 1 < N) ? mu * s.ee[ell] : 0.0;
+    for (int i = ell; i < N - 1; ++i) {
+      const double bsub = s.ee[i];
+      const double dn = s.dd[i + 1] - lam;
+      const double cn = (i + 2 < N) ? s.ee[i + 1] : 0.0;
+      if (fabs(a0) >= fabs(bsub)) {
+        const double piv = (fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0;
+        const double rp = fast_rcp(piv);
+        const double l = bsub * rp;
+        U0[i * nw + j] = rp;
+        U1[i * nw + j] = c0;
+        LM[i * nw + j] = l;
+        a0 = dn - l * c0;
+        c0 = cn;
+      } else {
+        const double rb = fast_rcp(bsub);
+        const double l = a0 * rb;
+        U0[i * nw + j] = rb;
+        U1[i * nw + j] = dn;
+        LM[i * nw + j] = l;
+        swp |= 1ull << i;
+        a0 = c0 - l * dn;
+        c0 = -l * cn;
+      }
+    }
+    U0[(N - 1) * nw + j] = fast_rcp((fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0);
+    // deterministic pseudo-random start vector in (-0.5, 0.5)
+    for (int i = 0; i < N; ++i) {
+      unsigned h = (unsigned)(i + 1) * 2654435761u ^ (unsigned)(j + 7) * 40503u;
+      h ^= h >> 13;
+      h *= 0x5bd1e995u;
+      h ^= h >> 15;
+      Z[i * nw + j] = (double)(h & 0xffffff) / 16777216.0 - 0.5;
+    }
   }
-  __syncthreads();
+  for (int iter = 0; iter < 2; ++iter) {
+    if (tid < nw) {
+      const int j = tid;
+      // arrow forward (row k keeps its rhs, or takes the arrow's on a swap)
+      double t = Z[ell * nw + j];
+      for (int k = 0; k < ell; ++k) {
+        const double l = LM[k * nw + j], zk = Z[k * nw + j];
+        if ((swp >> k) & 1ull) {
+          Z[k * nw + j] = t;
+          t = fma(-l, t, zk);
+        } else {
+          t = fma(-l, zk, t);
+        }
+      }
+      // tridiagonal forward: L^-1 with the recorded swaps (z_i carried)
+      double zi = t;
+      for (int i = ell; i < N - 1; ++i) {
+        const double zn = Z[(i + 1) * nw + j], l = LM[i * nw + j];
+        if ((swp >> i) & 1ull) {
+          Z[i * nw + j] = zn;
+          zi = fma(-l, zn, zi);
+        } else {
+          Z[i * nw + j] = zi;
+          zi = fma(-l, zi, zn);
+        }
+      }
+      Z[(N - 1) * nw + j] = zi;
+      // backward: U z = y  (U row i: 1/U0, U1, and e_{i+1} after a swap)
+      double z1 = 0.0, z2 = 0.0;
+      for (int i = N - 1; i >= ell; --i) {
+        double tt = Z[i * nw + j];
+        if (i + 1 < N) tt -= U1[i * nw + j] * z1;
+        if (i + 2 < N && ((swp >> i) & 1ull)) tt -= s.ee[i + 1] * z2;
+        const double zi = tt * U0[i * nw + j];
+        Z[i * nw + j] = zi;
+        z2 = z1;
+        z1 = zi;
+      }
+      // arrow back-substitution; S = sum_{k < c < ell} b_c z_c for the
+      // swapped (dense) rows
+      const double zl = Z[ell * nw + j], zl1 = (ell + 1 < N) ? Z[(ell + 1) * nw + j] : 0.0;
+      double S = 0.0;
+      for (int k = ell - 1; k >= 0; --k) {
+        const double g = U0[k * nw + j], rk = Z[k * nw + j];
+        double y;
+        if ((swp >> k) & 1ull)
+          y = fma(rk - U1[k * nw + j] * zl, g, -(S + s.ee[ell] * zl1) * fast_rcp(s.v[k]));
+        else
+          y = fma(-s.v[k], zl, rk) * g;
+        Z[k * nw + j] = y;
+        S = fma(s.v[k], y, S);
+      }
+      double nrm = 0.0;
+      for (int i = 0; i < N; ++i) nrm = fma(Z[i * nw + j], Z[i * nw + j], nrm);
+      const double inv = nrm > 0.0 ? rsqrt(nrm) : 0.0;
+      for (int i = 0; i < N; ++i) Z[i * nw + j] *= inv;
+    }
+    __syncthreads();
+    // modified Gram-Schmidt inside clusters: step q removes z_q from the
+    // later members (one warp each), z_q already final
+    for (int q = 0; q + 1 < nw; ++q) {
+      if (s.iw[64 + q + 1] != s.iw[64 + q]) continue;  // q ends its cluster
+      const int cid = s.iw[64 + q];
+      for (int jj = q + 1 + warp; jj < nw && s.iw[64 + jj] == cid; jj += nwp) {
+        double qq = 0.0, qz = 0.0;
+        for (int i = lane; i < N; i += 32) {
+          const double zq = Z[i * nw + q];
+          qq = fma(zq, zq, qq);
+          qz = fma(zq, Z[i * nw + jj], qz);
+        }
+        qq = warp_sum(qq);
+        qz = warp_sum(qz);
+        const double f = qq > 0.0 ? qz / qq : 0.0;
+        for (int i = lane; i < N; i += 32) Z[i * nw + jj] = fma(-f, Z[i * nw + q], Z[i * nw + jj]);
+        // normalise jj now if it is the next pivot (keeps magnitudes sane)
+      }
+      __syncthreads();
+    }
+    if (tid < nw) {
+      const int j = tid;
+      double nrm = 0.0;
+      for (int i = 0; i < N; ++i) nrm = fma(Z[i * nw + j], Z[i * nw + j], nrm);
+      const double inv = nrm > 0.0 ? rsqrt(nrm) : 0.0;
+      for (int i = 0; i < N; ++i) Z[i * nw + j] *= inv;
+    }
+    __syncthreads();
+  }
   TRI_MARK(2);
-  // ------------------------------------------------ 4. Y = Q Z
+  // ------------------------------------------------ 3. output
   for (int x = tid; x < N * nw; x += nth) {
     const int i = x / nw, j = x % nw;
-    double t = 0.0;
-    for (int c = 0; c < N; ++c) t = fma(s.Q[i * N + c], s.Z[(size_t)j * N + c], t);
-    Y[i * ldy + j] = t;
+    Y[(size_t)i * ldy + j] = Z[x];
   }
   for (int j = tid; j < nw; j += nth) vals[j] = s.lam[j];
   __syncthreads();

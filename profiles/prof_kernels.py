@@ -42,12 +42,13 @@ def main(which):
         if os.environ.get("USBS_LZ_PROF"):
             out = (C.c_uint64 * 12)()
             dp.rt.lib.usbs_lanczos_profile(dp.rt.h, out, 1)
-            names = ["phaseA", "barriers", "phaseB", "phaseC", "endcycle", "rayleigh_ritz", "restart", "-"]
-            tot = sum(out[:7])
-            for nm, v in zip(names, out[:7]):
+            names = ["phaseA", "barriers", "phaseB", "phaseC", "endcycle", "rayleigh_ritz", "restart",
+                     "spmv(cluster)"]
+            tot = sum(out[:8])
+            for nm, v in zip(names, out[:8]):
                 print(f"  {nm:14s} {v / 1e6 / (reps + 4):8.3f} ms/call  {100 * v / max(tot, 1):5.1f}%")
             nrr = (reps + 4) * (r.restarts + 1)
-            for nm, v in zip(["householder", "bisection", "inverse-it", "QZ"], out[8:12]):
+            for nm, v in zip(["setup", "bisection", "inverse-it", "output"], out[8:12]):
                 print(f"    rr {nm:12s} {v / 1e3 / nrr:8.2f} us per Rayleigh-Ritz")
         if os.environ.get("USBS_LZ_SWEEP"):
             for g in (8, 16, 32, 64, 148):

@@ -159,6 +159,49 @@ def test_lanczos_vs_oracle(name):
     np.testing.assert_allclose(r.eigenvalues, ro.eigenvalues, rtol=1e-5, atol=1e-9)
 
 
+@pytest.mark.parametrize("name", ["C2", "C1", "C5s", "qap3"])
+def test_lanczos_cluster_matches_grid(name, monkeypatch):
+    """The cluster (Q in shared memory) and grid-wide kernels run the same
+    recurrence: same restarts/matvecs, eigenvalues to rounding."""
+    eigen, runtime = dev()
+    p = case_problem(name)
+    y = np.random.default_rng(11).standard_normal(p.m) * 1e-3
+    if p.ineq_mask.any():
+        y[p.ineq_mask] = np.abs(y[p.ineq_mask])
+    dp_c = runtime.DeviceProblem(p)
+    monkeypatch.setenv("USBS_LZ_CLUSTER", "0")
+    dp_g = runtime.DeviceProblem(p)
+    assert dp_g.lanczos_plan(32) == (0, 0)
+    monkeypatch.delenv("USBS_LZ_CLUSTER")
+    cs, rows = dp_c.lanczos_plan(32)
+    if p.n >= 512:
+        assert cs in (8, 16) and cs * rows >= p.n
+    rc = eigen.lanczos_top(eigen.dual_slack_operator(dp_c, y), 10, seed=3)
+    rg = eigen.lanczos_top(eigen.dual_slack_operator(dp_g, y), 10, seed=3)
+    assert rc.restarts == rg.restarts and rc.matvecs == rg.matvecs
+    np.testing.assert_allclose(rc.eigenvalues, rg.eigenvalues, rtol=1e-11, atol=1e-13)
+    assert _projector_err(rc.eigenvectors, rg.eigenvectors) <= 1e-7
+
+
+@pytest.mark.parametrize("cluster", [True, False])
+def test_lanczos_breakdown_three_levels(cluster, monkeypatch):
+    """Diagonal operator with 3 distinct values at n=3000: the Krylov space
+    has dimension 3, so every cycle breaks down and reseeds (eigsolve.py:136-147)
+    — on the cluster kernel this exercises the Q spill / host reseed / resume."""
+    eigen, runtime = dev()
+    n = 3000
+    d = np.array([3.0, 2.0, 1.0])[np.arange(n) % 3]
+    if not cluster:
+        monkeypatch.setenv("USBS_LZ_CLUSTER", "0")
+    dp = runtime.DeviceProblem(dense_problem(np.diag(d)))
+    assert (dp.lanczos_plan(32)[0] > 0) == cluster
+    r = eigen.lanczos_top(eigen.cost_operator(dp), 2, seed=0)
+    ro = O.lanczos(O.Op(n, lambda v: d * v if v.ndim == 1 else d[:, None] * v), 2, seed=0)
+    np.testing.assert_allclose(r.eigenvalues, ro.eigenvalues, atol=1e-10)
+    assert r.converged == ro.converged
+    assert r.matvecs == ro.matvecs
+
+
 def test_lanczos_breakdown_diag_spike():
     """eigsolve breakdown path (reference test_eigsolve.py:11-15)."""
     eigen, runtime = dev()
