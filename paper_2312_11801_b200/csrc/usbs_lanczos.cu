@@ -480,10 +480,13 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   double* Qs = (double*)smem_raw;   // M1 * R, column-major (ld R), local rows
   double* W0s = Qs + (size_t)M1 * R;  // R
   double* W1s = W0s + R;             // R
-  double* P1s = W1s + R;             // 64 own partials (read by every CTA)
-  double* P2s = P1s + 64;            // 64
-  double* P3s = P2s + 64;            // 8
-  double* wred = P3s + 8;            // nw * 32
+  // partial-sum exchange: every CTA pushes its 32 column partials (and its
+  // ||w''||^2 share) into slot [rank] of EVERY CTA's buffer before the
+  // barrier, so the sums after it are local, fixed-order reads
+  double* XA = W1s + R;              // 16 * 32  Q^T w partials
+  double* XB = XA + 16 * 32;         // 16 * 32  Q^T w' partials
+  double* XC = XB + 16 * 32;         // 16       ||w''||^2 partials
+  double* wred = XC + 16;            // nw * 32
   double* cvec = wred + nw * 32;     // 64
   double* c2vec = cvec + 64;         // 64
   double* red = c2vec + 64;          // 64
@@ -502,6 +505,43 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   ts.red = ts.lam + 64;
   ts.iw = (int*)(ts.red + 64);
   int* rp = ts.iw + 128;  // R + 1 own row pointers
+  // c / R as a multiply-high: exact for c * R < 2^32 (host checks n * R)
+  const unsigned rmagic = (unsigned)((0x100000000ull + (unsigned)R - 1) / (unsigned)R);
+
+  // sum over the own rows of Q[:, lane] * x for lane <= j: warp w takes a
+  // contiguous block of rows, four independent FMA chains (R is odd, so the
+  // 32 lanes' column reads are bank-conflict free)
+  auto colsum = [&](const double* x, int j) -> double {
+    const int rpw = (nloc + nw - 1) / nw;
+    const int i0 = min(nloc, warp * rpw), i1 = min(nloc, i0 + rpw);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (lane <= j) {
+      const double* qc = Qs + (size_t)lane * R;
+      int i = i0;
+      for (; i + 3 < i1; i += 4) {
+        a0 = fma(qc[i], x[i], a0);
+        a1 = fma(qc[i + 1], x[i + 1], a1);
+        a2 = fma(qc[i + 2], x[i + 2], a2);
+        a3 = fma(qc[i + 3], x[i + 3], a3);
+      }
+      for (; i < i1; ++i) a0 = fma(qc[i], x[i], a0);
+    }
+    return (a0 + a1) + (a2 + a3);
+  };
+  // row il of Q (m <= 32 columns) into registers, and its product with Y[:, u]
+  auto load_qrow = [&](int il, double (&q)[32]) {
+#pragma unroll
+    for (int t = 0; t < 32; ++t) q[t] = t < m ? Qs[(size_t)t * R + il] : 0.0;
+  };
+  auto qrow_dot = [&](const double (&q)[32], int u) -> double {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 32; t += 2) {
+      if (t < m) s0 = fma(q[t], Ys[t * m + u], s0);
+      if (t + 1 < m) s1 = fma(q[t + 1], Ys[(t + 1) * m + u], s1);
+    }
+    return s0 + s1;
+  };
 
   // Q for the own rows from global (start vector / restart state / reseed)
   for (int x = tid; x < M1 * nloc; x += nth) {
@@ -536,7 +576,7 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
       }
       // x[c] lives in CTA c / R (own smem for the local band, DSMEM otherwise)
       auto gather = [&](int c) -> double {
-        const int owner = c / R, li = c - owner * R;
+        const int owner = (int)__umulhi((unsigned)c, rmagic), li = c - owner * R;
         const double* src = owner == b ? xloc : cluster.map_shared_rank(xloc, owner);
         return src[li];
       };
@@ -598,115 +638,102 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
       LZ_MARK(7);
       ++matvecs;
       {
-        // partial Q^T w over the own rows (warp butterfly, Q from smem)
-        int bad = 0;
-        double acc = 0.0;
-        for (int base = warp * 32; base < nloc; base += nw * 32) {
-          const int il = base + lane;
-          const bool live = il < nloc;
-          double q[32];
-          const double w = live ? Wcur[il] : 0.0;
-          if (live && !isfinite(w)) bad = 1;
-#pragma unroll
-          for (int t = 0; t < 32; ++t) q[t] = (live && t <= j) ? Qs[(size_t)t * R + il] * w : 0.0;
-          acc += butterfly32(q);
-        }
+        // partial Q^T w over the own rows: lane = column, warp = row block
+        const double acc = colsum(Wcur, j);
         wred[warp * 32 + lane] = acc;
-        if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.flags[F_NONFINITE], 1);
-        if (tid < 32) {
+        __syncthreads();
+        if (warp == 0) {
           double s = 0.0;
-          for (int w2 = 0; w2 < nw; ++w2) s += wred[w2 * 32 + tid];
-          P1s[tid] = s;
+          for (int w2 = 0; w2 < nw; ++w2) s += wred[w2 * 32 + lane];
+          for (int d = 0; d < CS; ++d) cluster.map_shared_rank(XA, d)[b * 32 + lane] = s;
         }
       }
       LZ_MARK(0);
       cluster.sync();
       LZ_MARK(1);
       // ------------------------------------------------------------ phase B
-      if (*(volatile int*)&a.flags[F_NONFINITE]) {
+      if (warp == 0) {  // c = sum over CTAs in rank order (identical everywhere)
+        double s = 0.0;
+        for (int src = 0; src < CS; ++src) s += XA[src * 32 + lane];
+        cvec[lane] = s;
+      }
+      __syncthreads();
+      // a non-finite w entry makes every column sum non-finite (inf * 0 = NaN)
+      if (!isfinite(cvec[0])) {
         if (b == 0 && tid == 0) {
+          atomicOr(&a.flags[F_NONFINITE], 1);
           a.flags[F_EXIT] = EXIT_NONFINITE;
           a.flags[F_MATVECS] = matvecs;
         }
         cluster.sync();
         return;
       }
-      for (int t = warp; t <= j; t += nw) {  // c = sum over CTAs (fixed order)
-        double s = lane < CS ? cluster.map_shared_rank(P1s, lane)[t] : 0.0;
-        s = warp_sum(s);
-        if (lane == 0) cvec[t] = s;
-      }
-      __syncthreads();
       {
-        double acc = 0.0;
-        for (int base = warp * 32; base < nloc; base += nw * 32) {
-          const int il = base + lane;
-          const bool live = il < nloc;
-          double q[32];
-          double s = 0.0;
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            q[t] = (live && t <= j) ? Qs[(size_t)t * R + il] : 0.0;
-            s = fma(q[t], (t <= j) ? cvec[t] : 0.0, s);
+        // w' = w - Q c (lane = row), then partial Q^T w' (lane = column)
+        for (int il = tid; il < nloc; il += nth) {
+          double s0 = 0.0, s1 = 0.0;
+          int t = 0;
+          for (; t + 1 <= j; t += 2) {
+            s0 = fma(Qs[(size_t)t * R + il], cvec[t], s0);
+            s1 = fma(Qs[(size_t)(t + 1) * R + il], cvec[t + 1], s1);
           }
-          double w = 0.0;
-          if (live) {
-            w = Wcur[il] - s;
-            Wcur[il] = w;
-          }
-#pragma unroll
-          for (int t = 0; t < 32; ++t) q[t] *= w;
-          acc += butterfly32(q);
+          if (t <= j) s0 = fma(Qs[(size_t)t * R + il], cvec[t], s0);
+          Wcur[il] -= s0 + s1;
         }
+        __syncthreads();
+        const double acc = colsum(Wcur, j);
         wred[warp * 32 + lane] = acc;
         __syncthreads();
-        if (tid < 32) {
+        if (warp == 0) {
           double s = 0.0;
-          for (int w2 = 0; w2 < nw; ++w2) s += wred[w2 * 32 + tid];
-          P2s[tid] = s;
+          for (int w2 = 0; w2 < nw; ++w2) s += wred[w2 * 32 + lane];
+          for (int d = 0; d < CS; ++d) cluster.map_shared_rank(XB, d)[b * 32 + lane] = s;
         }
       }
       LZ_MARK(2);
       cluster.sync();
       LZ_MARK(1);
       // ------------------------------------------------------------ phase C
-      for (int t = warp; t <= j; t += nw) {
-        double s = lane < CS ? cluster.map_shared_rank(P2s, lane)[t] : 0.0;
-        s = warp_sum(s);
-        if (lane == 0) c2vec[t] = s;
+      if (warp == 0) {
+        double s = 0.0;
+        for (int src = 0; src < CS; ++src) s += XB[src * 32 + lane];
+        c2vec[lane] = s;
+        // H column j = c + c' and the breakdown scale max(1, max|c + c'|)
+        const double ct = cvec[lane] + s;
+        cvec[lane] = ct;
+        const double mx = warp_max(lane <= j ? fabs(ct) : 0.0);
+        if (lane == 0) misc[0] = fmax(1.0, mx);
       }
       __syncthreads();
       {
         double ss = 0.0;
         for (int il = tid; il < nloc; il += nth) {
-          double s = 0.0;
-          for (int t = 0; t <= j; ++t) s = fma(Qs[(size_t)t * R + il], c2vec[t], s);
-          const double w = Wcur[il] - s;
+          double s0 = 0.0, s1 = 0.0;
+          int t = 0;
+          for (; t + 1 <= j; t += 2) {
+            s0 = fma(Qs[(size_t)t * R + il], c2vec[t], s0);
+            s1 = fma(Qs[(size_t)(t + 1) * R + il], c2vec[t + 1], s1);
+          }
+          if (t <= j) s0 = fma(Qs[(size_t)t * R + il], c2vec[t], s0);
+          const double w = Wcur[il] - (s0 + s1);
           Wcur[il] = w;
           ss = fma(w, w, ss);
         }
         ss = block_sum(ss, red);
-        if (tid == 0) P3s[0] = ss;
+        if (tid < CS) cluster.map_shared_rank(XC, tid)[b] = ss;
       }
-      for (int t = tid; t <= j; t += nth) cvec[t] += c2vec[t];
-      __syncthreads();
       if (b == 0)
         for (int t = tid; t <= j; t += nth) {
           a.H[t * M1 + j] = cvec[t];
           a.H[j * M1 + t] = cvec[t];
         }
-      if (tid == 0) {
-        double mx = 0.0;
-        for (int t = 0; t <= j; ++t) mx = fmax(mx, fabs(cvec[t]));
-        misc[0] = fmax(1.0, mx);
-      }
       LZ_MARK(3);
       cluster.sync();
       LZ_MARK(1);
-      if (tid < 32) {
-        double s = tid < CS ? cluster.map_shared_rank(P3s, tid)[0] : 0.0;
+      if (warp == 0) {
+        double s = lane < CS ? XC[lane] : 0.0;
         s = warp_sum(s);
-        if (tid == 0) misc[1] = sqrt(s);
+        if (lane == 0) misc[1] = sqrt(s);
       }
       __syncthreads();
       beta = misc[1];
@@ -779,12 +806,8 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
     ell = ell_next;
     for (int il = tid; il < nloc; il += nth) {
       double qrow[32];
-      for (int t = 0; t < m; ++t) qrow[t] = Qs[(size_t)t * R + il];
-      for (int u = 0; u < ell; ++u) {
-        double s = 0.0;
-        for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
-        Qs[(size_t)u * R + il] = s;
-      }
+      load_qrow(il, qrow);
+      for (int u = 0; u < ell; ++u) Qs[(size_t)u * R + il] = qrow_dot(qrow, u);
       Qs[(size_t)ell * R + il] = Qs[(size_t)m * R + il];
     }
     ++restarts;
@@ -803,12 +826,8 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
     for (int s = 0; s < 8; ++s) a.prof[s] += lz_acc[s];
   for (int il = tid; il < nloc; il += nth) {
     double qrow[32];
-    for (int t = 0; t < m; ++t) qrow[t] = Qs[(size_t)t * R + il];
-    for (int u = 0; u < a.k_c; ++u) {
-      double s = 0.0;
-      for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
-      a.vecs_out[(int64_t)(r0 + il) * a.ldvecs + u] = s;
-    }
+    load_qrow(il, qrow);
+    for (int u = 0; u < a.k_c; ++u) a.vecs_out[(int64_t)(r0 + il) * a.ldvecs + u] = qrow_dot(qrow, u);
   }
   if (b == 0 && tid == 0) {
     a.flags[F_EXIT] = EXIT_DONE;
@@ -822,7 +841,7 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
 
 static size_t lz_cl_smem(int m, int R, int nth) {
   const int M1 = m + 1, nw = nth / 32;
-  return (size_t)((size_t)M1 * R + 2 * R + 64 + 64 + 8 + nw * 32 + 64 * 3 + 8 + 64 + 4 * m * m + 6 * 64) *
+  return (size_t)((size_t)M1 * R + 2 * R + 16 * 32 * 2 + 16 + nw * 32 + 64 * 3 + 8 + 64 + 4 * m * m + 6 * 64) *
              sizeof(double) + (128 + R + 1) * sizeof(int) + 64;
 }
 
@@ -1018,8 +1037,9 @@ static LzClusterPlan lz_cluster_plan(usbs_ctx* ctx, int64_t n, int64_t nnz, int 
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   for (int cs : {16, 8}) {
-    const int64_t R = (n + cs - 1) / cs;
+    const int64_t R = ((n + cs - 1) / cs) | 1;  // odd: conflict-free column reads
     if (R < 32) continue;  // tiny operators: one warp-row per CTA at least
+    if (n * R >= (int64_t(1) << 32)) continue;  // owner = c / R by multiply-high
     const size_t sm = lz_cl_smem(m, (int)R, 512);
     if (sm > (size_t)optin) continue;
     if (lz_cl_max_clusters_lg(LG, cs, sm) < 1) continue;

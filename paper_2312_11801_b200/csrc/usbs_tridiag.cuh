@@ -57,15 +57,16 @@ __device__ __forceinline__ double fast_rcp(double q) {
 // pattern are the O(eps |H|) residue of the full reorthogonalisation; they are
 // ignored, which moves eigenvalues by O(eps |H|), the accuracy of eigh itself.
 // The structure is used directly, without a Householder reduction:
-//   Sturm counts  LDL^T of H - sigma I eliminating the arrow block first
-//                 (pivots theta_k - sigma), then the tridiagonal Schur
-//                 complement (first pivot d_ell - sigma - sum b_k^2/(theta_k -
-//                 sigma)); the tridiagonal part runs the three-term
-//                 leading-minor recurrence (one dependent FMA per row, rescaled
-//                 by powers of two every 4 rows); a pivot |q| < pivmin counts
-//                 as -pivmin as in LAPACK's ratio form.
+//   Sturm counts  signs of the LDL^T pivots of H - sigma I, eliminating the
+//                 arrow block first (pivots theta_k - sigma), then the
+//                 tridiagonal Schur complement, evaluated division-free as
+//                 ratios of leading minors (Barth-Martin-Wilkinson): one
+//                 dependent FMA per row, minors rescaled by powers of two
+//                 every 4 rows; a pivot |q| < pivmin counts as -pivmin as in
+//                 LAPACK's ratio form.
 //   eigenvalues   multisection, one warp per eigenvalue, 32 shifts per sweep,
-//                 to |interval| <= 4 eps max|endpoint|.
+//                 to |interval| <= max(4 eps max|endpoint|, eps |H|)
+//                 (LAPACK dstebz's default absolute tolerance).
 //   eigenvectors  inverse iteration, one thread per eigenvalue, all in
 //                 parallel: LU with partial pivoting of H - lam I (the arrow
 //                 block first: a swap makes the running arrow row a U row,
@@ -84,19 +85,29 @@ __device__ __forceinline__ void pow2_rescale(double& p, double& pm) {
 }
 
 // number of eigenvalues of the arrowhead + tridiagonal H below sigma.
-// d: diagonal (theta_k for k < ell); sq: b_k^2 for k < ell, e_i^2 for i >= ell
+// d: diagonal (theta_k for k < ell); sq: b_k^2 for k < ell, e_i^2 for i >= ell.
+// Division-free: the arrow block's pivots theta_k - sigma are counted
+// directly while a_k = prod_{i<k}(theta_i - sigma) and
+// b_k = sum_{i<k} b_i^2 prod_{i'<k, i'!=i}(theta_i' - sigma) accumulate the
+// leading minor of the arrow, det = (d_ell - sigma) a_ell - b_ell; from there
+// the tridiagonal minors follow the three-term recurrence.  The sign of the
+// ratio of consecutive minors is the sign of the LDL^T pivot.
 __device__ inline int sturm_arrow(int N, int ell, const double* d, const double* sq, double sigma, double pivmin) {
   int cnt = 0;
-  double s = 0.0;
+  double pa = 1.0, pb = 0.0;
   for (int k = 0; k < ell; ++k) {
-    double piv = d[k] - sigma;
-    if (fabs(piv) < pivmin) piv = -pivmin;
-    cnt += piv < 0.0;
-    s = fma(sq[k], fast_rcp(piv), s);
+    double f = d[k] - sigma;
+    if (fabs(f) < pivmin) f = -pivmin;
+    cnt += f < 0.0;
+    pb = fma(pb, f, sq[k] * pa);
+    pa *= f;
+    if ((k & 3) == 3) pow2_rescale(pa, pb);
   }
-  double pm = 1.0, p = (d[ell] - sigma) - s;
-  if (fabs(p) < pivmin) p = -pivmin;
-  cnt += p < 0.0;
+  double pm = pa;
+  double p = fma(d[ell] - sigma, pa, -pb);
+  if (fabs(p) < pivmin * fabs(pm)) p = -pivmin * pm;
+  cnt += (p < 0.0) != (pm < 0.0);
+  pow2_rescale(p, pm);
   for (int i = ell + 1; i < N; ++i) {
     double pn = fma(d[i] - sigma, p, -sq[i - 1] * pm);
     if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;
@@ -177,7 +188,7 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
     const int asc = N - 1 - j;  // ascending index of the j-th largest
     double lo = glo, hi = ghi;
     for (int it = 0; it < 24; ++it) {
-      if (hi - lo <= 4.4e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300) break;
+      if (hi - lo <= fmax(4.4e-16 * fmax(fabs(lo), fabs(hi)), 2.2e-16 * tnorm) + 1e-300) break;
       const double sig = lo + (hi - lo) * (double)(lane + 1) / 33.0;
       const int cnt = sturm_arrow(N, ell, s.dd, s.p, sig, pivmin);
       const unsigned mask = __ballot_sync(0xffffffffu, cnt >= asc + 1);
