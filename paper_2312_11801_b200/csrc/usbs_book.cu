@@ -428,91 +428,118 @@ __global__ void k_vec_final(int nb, const double* __restrict__ red, double* __re
 // pick max remaining norm; stop when <= drop_tol * max input column norm.
 // Outputs: perm[r] (chosen columns), rank, Rinv (r x r upper, row-major, ld c),
 // cond flag = min(selected residual / max norm) for the exact-path guard.
-__global__ void k_pivchol(int c, const double* __restrict__ G, double drop_tol, int* __restrict__ perm,
-                          double* __restrict__ Rinv, double* __restrict__ info) {
+// Block-parallel; every matrix element sees the same operation sequence as
+// a serial left-to-right sweep (bit-reproducible, no atomics).
+__global__ void __launch_bounds__(256) k_pivchol(int c, const double* __restrict__ G, double drop_tol,
+                                                 int* __restrict__ perm, double* __restrict__ Rinv,
+                                                 double* __restrict__ info) {
   __shared__ double A[40 * 40];
   __shared__ double R[40 * 40];
+  __shared__ double X[40 * 40];
   __shared__ int alive[40];
-  __shared__ int rank_s;
-  __shared__ double minratio_s, maxn_s;
-  for (int x = threadIdx.x; x < c * c; x += blockDim.x) { A[x] = G[x]; R[x] = 0.0; }
-  for (int x = threadIdx.x; x < c; x += blockDim.x) alive[x] = 1;
+  __shared__ int sel_s, ok_s;
+  __shared__ double bn_s, maxn_s, rjj_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
+  for (int x = tid; x < c * c; x += nth) A[x] = G[x];
+  for (int x = tid; x < 40 * 40; x += nth) R[x] = 0.0;
+  for (int x = tid; x < c; x += nth) alive[x] = 1;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     double mx = 0.0;
-    for (int j = 0; j < c; ++j) mx = fmax(mx, sqrt(fmax(A[j * c + j], 0.0)));
-    maxn_s = mx;
-    const double thresh = drop_tol < 0.0 ? 0.0 : drop_tol * mx;
-    int r = 0;
-    double minratio = 1.0;
-    if (mx > 0.0) {
-      for (int step = 0; step < c; ++step) {
-        int best = -1;
-        double bn = -1.0;
-        for (int j = 0; j < c; ++j)
-          if (alive[j]) {
-            double nj = sqrt(fmax(A[j * c + j], 0.0));
-            if (drop_tol < 0.0) {  // no pivoting: natural column order
-              best = j;
-              bn = nj;
-              break;
-            }
-            if (nj > bn) { bn = nj; best = j; }
-          }
-        if (best < 0 || bn <= thresh) break;
-        alive[best] = 0;
-        minratio = fmin(minratio, bn / mx);
-        // R row r: R[r][best] = bn, R[r][j] = A[best][j]/bn for alive j (Schur update)
-        perm[r] = best;
-        const double rb = sqrt(A[best * c + best]);
-        // Schur complement update on alive columns
-        for (int j = 0; j < c; ++j)
-          if (alive[j]) {
-            const double l = A[best * c + j] / rb;
-            for (int i2 = 0; i2 < c; ++i2)
-              if (alive[i2]) A[i2 * c + j] -= (A[best * c + i2] / rb) * l;
-          }
-        ++r;
-      }
-    }
-    rank_s = r;
-    minratio_s = minratio;
+    for (int jj = lane; jj < c; jj += 32) mx = fmax(mx, sqrt(fmax(A[jj * c + jj], 0.0)));
+    mx = warp_max(mx);
+    if (lane == 0) maxn_s = mx;
   }
   __syncthreads();
-  // R in pivot order from the original Gram: R = chol(G_pp) for the picked columns
-  const int r = rank_s;
-  if (threadIdx.x == 0 && r > 0) {
-    // Cholesky of G restricted to perm (upper R with G_pp = R^T R)
-    for (int a = 0; a < r; ++a)
-      for (int b2 = 0; b2 < r; ++b2) A[a * 40 + b2] = G[perm[a] * c + perm[b2]];
-    int ok = 1;
-    for (int j = 0; j < r && ok; ++j) {
-      double s = A[j * 40 + j];
-      for (int q = 0; q < j; ++q) s -= R[q * 40 + j] * R[q * 40 + j];
-      if (!(s > 0.0)) { ok = 0; break; }
-      const double rjj = sqrt(s);
-      R[j * 40 + j] = rjj;
-      for (int b2 = j + 1; b2 < r; ++b2) {
+  const double mx = maxn_s;
+  const double thresh = drop_tol < 0.0 ? 0.0 : drop_tol * mx;
+  int r = 0;
+  double minratio = 1.0;
+  if (mx > 0.0) {
+    for (int step = 0; step < c; ++step) {
+      if (warp == 0) {
+        // pivot: largest remaining column norm, first index on ties; natural
+        // order (first alive column) without pivoting
+        double bn = -1.0;
+        int best = 1 << 30;
+        for (int jj = lane; jj < c; jj += 32)
+          if (alive[jj]) {
+            const double nj = sqrt(fmax(A[jj * c + jj], 0.0));
+            const bool take = drop_tol < 0.0 ? (jj < best) : (nj > bn || (nj == bn && jj < best));
+            if (take) { bn = nj; best = jj; }
+          }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, bn, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, best, o);
+          const bool take = drop_tol < 0.0 ? (oj < best) : (ob > bn || (ob == bn && oj < best));
+          if (take) { bn = ob; best = oj; }
+        }
+        if (lane == 0) {
+          sel_s = best < (1 << 30) ? best : -1;
+          bn_s = bn;
+          if (best < (1 << 30) && !(bn <= thresh)) alive[best] = 0;
+        }
+      }
+      __syncthreads();
+      const int best = sel_s;
+      const double bn = bn_s;
+      if (best < 0 || bn <= thresh) break;
+      minratio = fmin(minratio, bn / mx);
+      if (tid == 0) perm[r] = best;
+      const double rb = sqrt(A[best * c + best]);
+      for (int x = tid; x < c * c; x += nth) {
+        const int i2 = x / c, jj = x % c;
+        if (alive[i2] && alive[jj]) A[i2 * c + jj] -= (A[best * c + i2] / rb) * (A[best * c + jj] / rb);
+      }
+      ++r;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // R = chol(G_pp) in pivot order (row-oriented: R[j][b] = (G_pp[j][b] -
+  // sum_{q<j} R[q][j] R[q][b]) / R[j][j], q ascending)
+  double mr = minratio;
+  if (r > 0) {
+    for (int x = tid; x < r * r; x += nth) {
+      const int a2 = x / r, b2 = x % r;
+      A[a2 * 40 + b2] = G[perm[a2] * c + perm[b2]];
+    }
+    if (tid == 0) ok_s = 1;
+    __syncthreads();
+    for (int j = 0; j < r; ++j) {
+      if (tid == 0) {
+        double s = A[j * 40 + j];
+        for (int q = 0; q < j; ++q) s -= R[q * 40 + j] * R[q * 40 + j];
+        if (!(s > 0.0)) ok_s = 0;
+        rjj_s = sqrt(s);
+        if (s > 0.0) R[j * 40 + j] = rjj_s;
+      }
+      __syncthreads();
+      if (!ok_s) break;
+      const double rjj = rjj_s;
+      for (int b2 = j + 1 + tid; b2 < r; b2 += nth) {
         double t = A[j * 40 + b2];
         for (int q = 0; q < j; ++q) t -= R[q * 40 + j] * R[q * 40 + b2];
         R[j * 40 + b2] = t / rjj;
       }
-      for (int b2 = 0; b2 < j; ++b2) R[j * 40 + b2] = 0.0;
+      __syncthreads();
     }
-    if (!ok) minratio_s = 0.0;
-    // Rinv (upper) by back substitution, column by column
-    for (int col = 0; col < r; ++col)
+    if (!ok_s) mr = 0.0;
+    // Rinv (upper) by back substitution, one thread per column
+    for (int col = tid; col < r; col += nth)
       for (int row = r - 1; row >= 0; --row) {
         double s = (row == col) ? 1.0 : 0.0;
-        for (int q = row + 1; q < r; ++q) s -= R[row * 40 + q] * Rinv[q * c + col];
-        Rinv[row * c + col] = (row <= col) ? s / R[row * 40 + row] : 0.0;
+        for (int q = row + 1; q < r; ++q) s -= R[row * 40 + q] * X[q * 40 + col];
+        X[row * 40 + col] = (row <= col) ? s / R[row * 40 + row] : 0.0;
       }
+    __syncthreads();
+    for (int x = tid; x < r * r; x += nth) Rinv[(x / r) * c + (x % r)] = X[(x / r) * 40 + (x % r)];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     info[0] = r;
-    info[1] = minratio_s;
-    info[2] = maxn_s;
+    info[1] = mr;
+    info[2] = mx;
   }
 }
 
@@ -661,7 +688,7 @@ usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* G, double drop_tol,
                          double* info) {
   USBS_API_BEGIN
   if (c < 1 || c > 40) fail(USBS_ERR_SHAPE, "pivchol: 1 <= c <= 40");
-  k_pivchol<<<1, 64, 0, ctx->stream>>>(c, G, drop_tol, perm, Rinv, info);
+  k_pivchol<<<1, 256, 0, ctx->stream>>>(c, G, drop_tol, perm, Rinv, info);
   check_launch(ctx);
   USBS_API_END
 }

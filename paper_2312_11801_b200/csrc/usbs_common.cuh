@@ -92,15 +92,13 @@ struct usbs_problem {
   int* it_beg = nullptr;
   int* it_end = nullptr;
   int* it_slot = nullptr;  // -1: whole row, else index into the split-partial scratch
-  // SpMV hybrid: rows with 32 < nnz <= 1024 (warp per row), > 1024 (block per row)
-  int n_long_rows = 0, n_huge_rows = 0;
-  int* long_rows = nullptr;
+  // k = 1 SpMV: rows with more than 2048 nonzeros get a block each
+  int n_huge_rows = 0;
   int* huge_rows = nullptr;
-  int n_hseg = 0;  // 256-nnz segments of the huge rows
-  int* hseg_beg = nullptr;
-  int* hseg_end = nullptr;
-  int* hrow_first = nullptr;
-  int* hrow_count = nullptr;
+  int n_stiles = 0;  // CSR-stream tiles of consecutive rows (k = 1 SpMV)
+  int st_nnz = 1024;  // nonzeros per tile (rows above it get a block)
+  int* stile_r0 = nullptr;
+  int* stile_r1 = nullptr;
   // the subset of items that belong to rows longer than 32
   int n_long_items = 0;
   int* lit_row = nullptr;

@@ -95,130 +95,99 @@ __global__ void __launch_bounds__(256) k_spmm(int n_items, const int* __restrict
   }
 }
 
-// SpMV (k = 1): groups of 4 lanes per row segment, each lane keeps 4
-// independent nonzeros in flight (16 per group per iteration), so a warp has
-// 8 segments and up to 128 gathers outstanding.  Read-only data via the
-// non-coherent path.  Segment partials of split rows go to `partial`.
-__global__ void __launch_bounds__(256) k_spmv4(int n_items, const int* __restrict__ it_row,
-                                               const int* __restrict__ it_beg, const int* __restrict__ it_end,
-                                               const int* __restrict__ it_slot, const int* __restrict__ col,
-                                               const double* __restrict__ val, const double* __restrict__ x,
-                                               int64_t ldx, double* __restrict__ y, int64_t ldy,
-                                               double* __restrict__ partial) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int warps_total = (gridDim.x * blockDim.x) >> 5;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (int base = gw * 8; base < n_items; base += warps_total * 8) {
-    const int it = base + g;
-    const bool ok = it < n_items;
-    double acc = 0.0;
-    if (ok) {
-      const int b = __ldg(it_beg + it), e = __ldg(it_end + it);
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int z = b + t;
-      for (; z + 12 < e; z += 16) {
-        const int j0 = __ldg(col + z), j1 = __ldg(col + z + 4), j2 = __ldg(col + z + 8), j3 = __ldg(col + z + 12);
-        const double v0 = __ldg(val + z), v1 = __ldg(val + z + 4), v2 = __ldg(val + z + 8), v3 = __ldg(val + z + 12);
-        a0 = fma(v0, __ldg(x + (int64_t)j0 * ldx), a0);
-        a1 = fma(v1, __ldg(x + (int64_t)j1 * ldx), a1);
-        a2 = fma(v2, __ldg(x + (int64_t)j2 * ldx), a2);
-        a3 = fma(v3, __ldg(x + (int64_t)j3 * ldx), a3);
-      }
-      for (; z < e; z += 4) a0 = fma(__ldg(val + z), __ldg(x + (int64_t)__ldg(col + z) * ldx), a0);
-      acc = (a0 + a1) + (a2 + a3);
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (ok && t == 0) {
-      const int sl = __ldg(it_slot + it);
-      if (sl < 0) y[(int64_t)__ldg(it_row + it) * ldy] = acc;
-      else partial[sl] = acc;
-    }
-  }
-}
-
-// SpMV over the short rows (nnz <= SHORT_ROW): one thread per row, four
-// independent nonzeros in flight per thread; the warp's rows are contiguous
-// so its col/val loads stream through L1.  Long rows are skipped here and
-// handled by k_spmv4 over their segment list.
+// k = 1: rows longer than SHORT_ROW nonzeros get a warp (<= 256) or a block
+// (> 256); the short ones go through CSR-stream tiles.
 constexpr int SHORT_ROW = 32;
-__global__ void __launch_bounds__(256) k_spmv_short(int64_t n, const int* __restrict__ rowptr,
-                                                    const int* __restrict__ col, const double* __restrict__ val,
-                                                    const double* __restrict__ x, int64_t ldx, double* __restrict__ y,
-                                                    int64_t ldy) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = __ldg(rowptr + i), e = __ldg(rowptr + i + 1);
-    if (e - b > SHORT_ROW) continue;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int z = b;
-    for (; z + 3 < e; z += 4) {
-      const int j0 = __ldg(col + z), j1 = __ldg(col + z + 1), j2 = __ldg(col + z + 2), j3 = __ldg(col + z + 3);
-      a0 = fma(__ldg(val + z), __ldg(x + (int64_t)j0 * ldx), a0);
-      a1 = fma(__ldg(val + z + 1), __ldg(x + (int64_t)j1 * ldx), a1);
-      a2 = fma(__ldg(val + z + 2), __ldg(x + (int64_t)j2 * ldx), a2);
-      a3 = fma(__ldg(val + z + 3), __ldg(x + (int64_t)j3 * ldx), a3);
-    }
-    for (; z < e; ++z) a0 = fma(__ldg(val + z), __ldg(x + (int64_t)__ldg(col + z) * ldx), a0);
-    y[i * ldy] = (a0 + a1) + (a2 + a3);
-  }
-}
 
-// SpMV over long rows (SHORT_ROW < nnz <= 1024): one warp per row, lanes
-// stride over the nonzeros (coalesced col/val), fixed-order warp reduction.
-__global__ void __launch_bounds__(256) k_spmv_long(int nrows, const int* __restrict__ rows,
-                                                   const int* __restrict__ rowptr, const int* __restrict__ col,
-                                                   const double* __restrict__ val, const double* __restrict__ x,
-                                                   int64_t ldx, double* __restrict__ y, int64_t ldy) {
-  const int lane = threadIdx.x & 31;
-  const int warps_total = (gridDim.x * blockDim.x) >> 5;
-  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows; w += warps_total) {
-    const int r = __ldg(rows + w);
-    const int b = __ldg(rowptr + r), e = __ldg(rowptr + r + 1);  // e - b <= 256
-    double a[8];
+// CSR-stream tiles: the tile's nonzeros are read fully coalesced (one per
+// thread, 8 in flight), their products staged in shared memory, then one
+// thread per row sums its products in column order (a sequential CSR loop's
+// order).
+constexpr int ST_ROWS = 1024;  // rows per tile (empty rows add no nonzeros)
+
+// All of a k = 1 apply in ONE launch, block roles by blockIdx (huge rows
+// first so they never form the tail): [0, H) one block per row with more
+// than ST_NNZ nonzeros (thread-strided partial sums, fixed-order block
+// tree); then the CSR-stream tiles, each a run of consecutive rows with at
+// most ST_NNZ nonzeros in total; inside a tile a thread sums each short row
+// (<= SHORT_ROW) and a warp each longer one.  Deterministic, no atomics.
+template <int ST_NNZ, int ST_THREADS, int MINB>
+__global__ void __launch_bounds__(ST_THREADS, MINB) k_spmv_fused(int nhuge, const int* __restrict__ huge_rows, int ntiles,
+                                                    const int* __restrict__ tile_r0, const int* __restrict__ tile_r1,
+                                                    const int* __restrict__ rowptr, const int* __restrict__ col,
+                                                    const double* __restrict__ val, const double* __restrict__ x,
+                                                    int64_t ldx, double* __restrict__ y, int64_t ldy) {
+  __shared__ double prod[ST_NNZ];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int b = blockIdx.x;
+  if (b < nhuge) {
+    const int r = __ldg(huge_rows + b);
+    const int zb = __ldg(rowptr + r), ze = __ldg(rowptr + r + 1);
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int z0 = zb; z0 < ze; z0 += ST_THREADS * 4) {
+      int cc[4];
+      double vv[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int z = b + lane + 32 * u;
-      a[u] = (z < e) ? __ldg(val + z) * __ldg(x + (int64_t)__ldg(col + z) * ldx) : 0.0;
-    }
-    const double s = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
-    if (lane == 0) y[(int64_t)r * ldy] = s;
-  }
-}
-
-// SpMV over 256-nnz segments of huge rows (nnz > 1024): one warp per segment
-// into a partial; k_spmv_hcombine sums each row's partials with one warp in a
-// fixed order (deterministic, no atomics).
-__global__ void __launch_bounds__(256) k_spmv_hseg(int nseg, const int* __restrict__ sbeg,
-                                                   const int* __restrict__ send, const int* __restrict__ col,
-                                                   const double* __restrict__ val, const double* __restrict__ x,
-                                                   int64_t ldx, double* __restrict__ partial) {
-  const int lane = threadIdx.x & 31;
-  const int warps_total = (gridDim.x * blockDim.x) >> 5;
-  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nseg; w += warps_total) {
-    const int b = __ldg(sbeg + w), e = __ldg(send + w);
-    double a[8];
+      for (int u = 0; u < 4; ++u) {
+        const int z = z0 + tid + ST_THREADS * u;
+        cc[u] = z < ze ? __ldg(col + z) : -1;
+        vv[u] = z < ze ? __ldg(val + z) : 0.0;
+      }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int z = b + lane + 32 * u;
-      a[u] = (z < e) ? __ldg(val + z) * __ldg(x + (int64_t)__ldg(col + z) * ldx) : 0.0;
+      for (int u = 0; u < 4; ++u)
+        if (cc[u] >= 0) a[u & 3] = fma(vv[u], __ldg(x + (int64_t)cc[u] * ldx), a[u & 3]);
     }
-    const double s = warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
-    if (lane == 0) partial[w] = s;
+    double s = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+    if (lane == 0) prod[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+      s = lane < ST_THREADS / 32 ? prod[lane] : 0.0;
+      s = warp_sum(s);
+      if (lane == 0) y[(int64_t)r * ldy] = s;
+    }
+    return;
   }
-}
-
-__global__ void __launch_bounds__(256) k_spmv_hcombine(int nrows, const int* __restrict__ rows,
-                                                       const int* __restrict__ first, const int* __restrict__ count,
-                                                       const double* __restrict__ partial, double* __restrict__ y,
-                                                       int64_t ldy) {
-  const int lane = threadIdx.x & 31;
-  const int warps_total = (gridDim.x * blockDim.x) >> 5;
-  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows; w += warps_total) {
-    const int f = __ldg(first + w), c = __ldg(count + w);
+  b -= nhuge;
+  if (b >= ntiles) return;
+  __shared__ int rps[ST_ROWS + 1];  // tile row pointers relative to base
+  __shared__ int longl[ST_ROWS];    // tile rows longer than SHORT_ROW
+  __shared__ int nlong;
+  const int r0 = __ldg(tile_r0 + b), r1 = __ldg(tile_r1 + b);
+  const int base = __ldg(rowptr + r0), cnt = __ldg(rowptr + r1) - base;
+  int cc[ST_NNZ / ST_THREADS];
+  double vv[ST_NNZ / ST_THREADS];
+#pragma unroll
+  for (int u = 0; u < ST_NNZ / ST_THREADS; ++u) {
+    const int z = tid + u * ST_THREADS;
+    cc[u] = z < cnt ? __ldg(col + base + z) : 0;
+    vv[u] = z < cnt ? __ldg(val + base + z) : 0.0;
+  }
+  for (int i = tid; i <= r1 - r0; i += ST_THREADS) rps[i] = __ldg(rowptr + r0 + i) - base;
+  if (tid == 0) nlong = 0;
+#pragma unroll
+  for (int u = 0; u < ST_NNZ / ST_THREADS; ++u) {
+    const int z = tid + u * ST_THREADS;
+    if (z < cnt) prod[z] = vv[u] * __ldg(x + (int64_t)cc[u] * ldx);
+  }
+  __syncthreads();
+  for (int il = tid; il < r1 - r0; il += ST_THREADS) {
+    const int bb = rps[il], e = rps[il + 1];
+    if (e - bb > SHORT_ROW) {
+      longl[atomicAdd(&nlong, 1)] = il;  // list order is irrelevant: one row, one sum
+      continue;
+    }
     double s = 0.0;
-    for (int u = lane; u < c; u += 32) s += partial[f + u];
+    for (int z = bb; z < e; ++z) s += prod[z];
+    y[(int64_t)(r0 + il) * ldy] = s;
+  }
+  __syncthreads();
+  for (int t = warp; t < nlong; t += ST_THREADS / 32) {
+    const int il = longl[t];
+    const int bb = rps[il], e = rps[il + 1];
+    double s = 0.0;
+    for (int z = bb + lane; z < e; z += 32) s += prod[z];
     s = warp_sum(s);
-    if (lane == 0) y[(int64_t)__ldg(rows + w) * ldy] = s;
+    if (lane == 0) y[(int64_t)(r0 + il) * ldy] = s;
   }
 }
 
@@ -571,32 +540,27 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
         lr.push_back(r); lb.push_back(ibeg[t]); le.push_back(iend[t]); ls.push_back(islot[t]);
       }
     }
-    std::vector<int32_t> longr, huger;
-    for (int64_t i = 0; i < n; ++i) {
-      const int32_t len = rp32[i + 1] - rp32[i];
-      if (len > 256) huger.push_back((int32_t)i);
-      else if (len > SHORT_ROW) longr.push_back((int32_t)i);
-    }
-    p->n_long_rows = (int)longr.size();
-    p->n_huge_rows = (int)huger.size();
-    p->long_rows = dev_upload(p, longr.data(), longr.size());
-    p->huge_rows = dev_upload(p, huger.data(), huger.size());
-    std::vector<int32_t> hb, he, hf, hc;
-    for (int32_t r : huger) {
-      hf.push_back((int32_t)hb.size());
-      int cnt = 0;
-      for (int32_t z = rp32[r]; z < rp32[r + 1]; z += 256) {
-        hb.push_back(z);
-        he.push_back(std::min(rp32[r + 1], z + 256));
-        ++cnt;
+    // CSR-stream tiles: maximal runs of at most ST_ROWS consecutive rows with
+    // at most ST_NNZ nonzeros in total; longer rows get a block of their own
+    {
+      const char* te = getenv("USBS_SPMV_TILE");
+      const int ST_NNZ = (te && atoi(te) == 2048) ? 2048 : (te && atoi(te) == 4096) ? 4096 : 1024;
+      p->st_nnz = ST_NNZ;
+      std::vector<int32_t> t0, t1, hr;
+      int64_t i = 0;
+      while (i < n) {
+        if (rp32[i + 1] - rp32[i] > ST_NNZ) { hr.push_back((int32_t)i); ++i; continue; }
+        const int64_t s0 = i;
+        while (i < n && i - s0 < ST_ROWS && rp32[i + 1] - rp32[i] <= ST_NNZ && rp32[i + 1] - rp32[s0] <= ST_NNZ) ++i;
+        t0.push_back((int32_t)s0);
+        t1.push_back((int32_t)i);
       }
-      hc.push_back(cnt);
+      p->n_stiles = (int)t0.size();
+      p->stile_r0 = dev_upload(p, t0.data(), t0.size());
+      p->stile_r1 = dev_upload(p, t1.data(), t1.size());
+      p->n_huge_rows = (int)hr.size();
+      p->huge_rows = dev_upload(p, hr.data(), hr.size());
     }
-    p->n_hseg = (int)hb.size();
-    p->hseg_beg = dev_upload(p, hb.data(), hb.size());
-    p->hseg_end = dev_upload(p, he.data(), he.size());
-    p->hrow_first = dev_upload(p, hf.data(), hf.size());
-    p->hrow_count = dev_upload(p, hc.data(), hc.size());
     p->n_long_items = (int)lr.size();
     p->lit_row = dev_upload(p, lr.data(), lr.size());
     p->lit_beg = dev_upload(p, lb.data(), lb.size());
@@ -675,24 +639,17 @@ void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int
   if (p->n_split_items) partial = (double*)ctx->ws.get(WS_SPMM_PARTIAL, (size_t)p->n_split_items * k * sizeof(double));
   const int th = 256;
   if (k == 1) {
-    int bl = (int)std::min<int64_t>((p->n + th - 1) / th, 16 * ctx->num_sms);
-    k_spmv_short<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n, p->rowptr, p->col, val, V, ldv, Y, ldy);
-    check_launch(ctx);
-    if (p->n_long_rows) {
-      int bl2 = (int)std::min<int64_t>((p->n_long_rows + 7) / 8, 16 * ctx->num_sms);
-      k_spmv_long<<<std::max(bl2, 1), th, 0, ctx->stream>>>(p->n_long_rows, p->long_rows, p->rowptr, p->col, val,
-                                                            V, ldv, Y, ldy);
-      check_launch(ctx);
-    }
-    if (p->n_huge_rows) {
-      double* hp = (double*)ctx->ws.get(WS_SPMM_PARTIAL + 100, (size_t)p->n_hseg * sizeof(double));
-      int bl3 = (int)std::min<int64_t>((p->n_hseg + 7) / 8, 16 * ctx->num_sms);
-      k_spmv_hseg<<<std::max(bl3, 1), th, 0, ctx->stream>>>(p->n_hseg, p->hseg_beg, p->hseg_end, p->col, val, V,
-                                                            ldv, hp);
-      check_launch(ctx);
-      int bl4 = (int)std::min<int64_t>((p->n_huge_rows + 7) / 8, 4 * ctx->num_sms);
-      k_spmv_hcombine<<<std::max(bl4, 1), th, 0, ctx->stream>>>(p->n_huge_rows, p->huge_rows, p->hrow_first,
-                                                                p->hrow_count, hp, Y, ldy);
+    const int64_t nb = (int64_t)p->n_huge_rows + p->n_stiles;
+    if (nb > 0) {
+#define USBS_SPMV_ARGS p->n_huge_rows, p->huge_rows, p->n_stiles, p->stile_r0, p->stile_r1, p->rowptr, p->col, \
+                       val, V, ldv, Y, ldy
+      if (p->st_nnz == 2048)
+        k_spmv_fused<2048, 512, 3><<<(unsigned)nb, 512, 0, ctx->stream>>>(USBS_SPMV_ARGS);
+      else if (p->st_nnz == 4096)
+        k_spmv_fused<4096, 512, 2><<<(unsigned)nb, 512, 0, ctx->stream>>>(USBS_SPMV_ARGS);
+      else
+        k_spmv_fused<1024, 256, 6><<<(unsigned)nb, 256, 0, ctx->stream>>>(USBS_SPMV_ARGS);
+#undef USBS_SPMV_ARGS
       check_launch(ctx);
     }
     return;

@@ -3,6 +3,7 @@
     python profiles/prof_kernels.py lanczos   # k_lanczos on C2 slack operator
     python profiles/prof_kernels.py ipm       # k_ipm (d = 66) on a C2-like subproblem
     python profiles/prof_kernels.py spmm      # K1 on C4 (n = 1e6), k = 1 and 11
+    python profiles/prof_kernels.py lanczos4  # k_lanczos on the C4 slack operator (HBM-resident Q)
 """
 from __future__ import annotations
 
@@ -21,8 +22,8 @@ def main(which):
     from paper_2312_11801_b200 import eigen, instances as inst, subproblem
     from paper_2312_11801_b200.runtime import DeviceProblem
 
-    if which == "lanczos":
-        p = inst.baseline_config("C2").problem
+    if which in ("lanczos", "lanczos4"):
+        p = inst.baseline_config("C2" if which == "lanczos" else "C4").problem
         dp = DeviceProblem(p)
         y = np.random.default_rng(1234).standard_normal(p.m) * 1e-3
         import ctypes as C
@@ -38,7 +39,17 @@ def main(which):
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / reps
         print("lanczos", r.eigenvalues[0], r.restarts, r.matvecs, f"{dt * 1e3:.3f} ms/call",
-              f"{dt / r.matvecs * 1e6:.2f} us/step", "blocks", dp.info().lanczos_blocks)
+              f"{dt / r.matvecs * 1e6:.2f} us/step", "blocks", dp.info().lanczos_blocks,
+              "plan", dp.lanczos_plan(max(32, 11)))
+        # step j moves B_apply(1) + 24 n (j+1) + 16 n bytes (fused 3-read CGS2)
+        nnz = dp.info().nnz_z
+        bapp = 12 * nnz + 4 * (p.n + 1) + 8 * p.n + 16 * p.n
+        m, ell, tot, j0 = 32, 13, 0, 0
+        for c in range(r.restarts + 1):
+            for j in range(j0, m):
+                tot += bapp + 24 * p.n * (j + 1) + 16 * p.n
+            j0 = ell
+        print(f"  algorithmic {tot / 1e9:.3f} GB/call -> {tot / dt / 1e9:.0f} GB/s")
         if os.environ.get("USBS_LZ_PROF"):
             out = (C.c_uint64 * 12)()
             dp.rt.lib.usbs_lanczos_profile(dp.rt.h, out, 1)
@@ -113,11 +124,23 @@ def main(which):
         p = inst.baseline_config("C4").problem
         dp = DeviceProblem(p)
         dp.assemble(dp.rt.upload(np.random.default_rng(1).standard_normal(p.m) * 1e-3))
+        nnz = dp.info().nnz_z
         for k in (1, 11):
             V = dp.rt.upload(np.random.default_rng(2).standard_normal((p.n, k)))
+            out = dp.rt.empty(p.n, k)
             for _ in range(3):
-                dp.apply(1, V)
-        torch.cuda.synchronize()
+                dp.apply(1, V, out=out)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 20
+            e0.record()
+            for _ in range(reps):
+                dp.apply(1, V, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / reps
+            b = 12 * nnz + 4 * (p.n + 1) + 8 * p.n + 16 * p.n * k  # SURVEY 8(d) B_apply(k)
+            print(f"spmm C4 k={k}: {us:.1f} us/apply  {b / us / 1e3:.0f} GB/s (B_apply = {b / 1e6:.1f} MB, L2-warm)")
         print("spmm done")
 
 
