@@ -120,8 +120,13 @@ usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int which, int k_c,
                              int* matvecs);
 
 /* Phase timers of the Lanczos kernel (ns, accumulated while the environment
- * variable USBS_LZ_PROF is set): phase A, grid barriers, phase B, phase C,
- * end of cycle, Rayleigh-Ritz, restart.  reset != 0 zeroes them. */
+ * variable USBS_LZ_PROF is set); out_host holds 1024 entries: [0..7] phase A,
+ * barriers, phase B, phase C, end of cycle, Rayleigh-Ritz, restart, SpMV
+ * (cluster kernel), all measured on block 0; [8..11] Rayleigh-Ritz setup,
+ * bisection, inverse iteration, output; [32 + 4b + s] block b's work in the
+ * SpMV, the Q^T w sums, phase B and phase C with barrier waits excluded
+ * (grid kernel).  reset != 0
+ * zeroes them. */
 usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* out_host, int reset);
 
 /* Execution plan usbs_lanczos_top uses for basis size m on p: *cluster_size

@@ -111,21 +111,25 @@ struct usbs_problem {
   int* sr_first = nullptr;  // first split slot
   int* sr_count = nullptr;
   int* sr_block = nullptr;  // owning Lanczos block of each split row (ascending)
-  // Lanczos partition: block b owns items [blk_item[b], blk_item[b+1]) and
-  // rows [blk_row[b], blk_row[b+1]); split rows [blk_sr[b], blk_sr[b+1])
+  // Lanczos partition: block b owns rows [blk_row[b], blk_row[b+1])
   int lz_blocks = 0;
   int spmv_group = 32;
   // cached cluster-Lanczos plan (usbs_lanczos.cu): basis size it was made
   // for, cluster size (0 = grid kernel), rows per CTA, dynamic smem bytes
   int lz_cl_m = -1, lz_cl_cs = 0, lz_cl_R = 0, lz_cl_lg = 32;  // lg: SpMV lanes per row
   size_t lz_cl_smem = 0;
-  int* blk_item = nullptr;
   int* blk_row = nullptr;
-  int* blk_sr = nullptr;
+  int* blk_seg = nullptr;  // Lanczos block b's SpMV segments [blk_seg[b], blk_seg[b+1])
+  int* seg_r0 = nullptr;   // segment rows [seg_r0, seg_r1): <= LZT_NNZ nonzeros or one row
+  int* seg_r1 = nullptr;
   std::vector<void*> owned;
 };
 
 namespace usbs {
+
+// grid-Lanczos SpMV segments: at most LZT_NNZ nonzeros and LZT_ROWS rows
+constexpr int LZT_NNZ = 4096;
+constexpr int LZT_ROWS = 2048;
 
 template <typename T>
 T* dev_upload(usbs_problem* p, const T* host, size_t count) {

@@ -11,7 +11,9 @@
 //               thick restart: ell = max(1, min(k_c+3, m-2)),
 //               Q[:, :ell] = Q[:, :m] Y[:, :ell], Q[:, ell] = q_m, H = diag(theta[:ell])
 //
-// Device layout: Q column-major (ldq >= n), two n-vectors W0/W1 (double
+// Device layout: Q row-blocked (qidx: 32-row tiles, all m+1 columns of a
+// tile contiguous, so a warp's 32-row chunk of every column is one streamed
+// 8.4 KB region), two n-vectors W0/W1 (double
 // buffered so the SpMV of step j+1 can gather w''_j / beta_j from any row
 // while this step's w is being written), H (m+1)^2 row-major in global.
 // Grid: G blocks (one per SM at most), each owning a contiguous row range
@@ -45,29 +47,22 @@ enum LzExit { EXIT_DONE = 0, EXIT_BREAKDOWN = 1, EXIT_NONFINITE = 2 };
 
 struct LzArgs {
   int n, m, k_c, max_restarts;
-  int64_t ldq;
+  int64_t ldq;  // row stride of W0/W1 (>= n)
   double tol;
   const int* rowptr;
   const int* col;
   const double* val;
-  const int* it_row;
-  const int* it_beg;
-  const int* it_end;
-  const int* it_slot;
-  const int* blk_item;
-  const int* blk_row;
-  const int* blk_sr;
-  const int* sr_row;
-  const int* sr_first;
-  const int* sr_count;
+  const int* blk_row;  // block b owns rows [blk_row[b], blk_row[b+1]) (Q passes)
+  const int* blk_seg;  // ... and SpMV segments [blk_seg[b], blk_seg[b+1]) (nnz-balanced)
+  const int* seg_r0;   // segment: rows [seg_r0, seg_r1), <= LZT_NNZ nonzeros,
+  const int* seg_r1;   //   or a single row with more (block-wide sum)
   double* Q;
   double* W0;
   double* W1;
   double* H;
-  double* P1;  // [G][64]
-  double* P2;  // [G][64]
+  double* P1;  // [64][G] column partials, P1[t * G + b]
+  double* P2;  // [64][G]
   double* P3;  // [G]
-  double* split;
   int* flags;
   double* theta;  // [m]   output (after the last Rayleigh-Ritz)
   double* Y;      // [m*m] output
@@ -81,6 +76,11 @@ struct LzArgs {
   int64_t ldvecs;
   unsigned long long* prof;  // optional phase timer accumulators (ns), block 0
 };
+
+// Q element (row i, column t) in the row-blocked layout
+__host__ __device__ __forceinline__ int64_t qidx(int64_t i, int t, int M1) {
+  return ((i >> 5) * M1 + t) * 32 + (i & 31);
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -97,6 +97,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
       lz_acc[slot] += _t - lz_last;                     \
       lz_last = _t;                                     \
     }                                                   \
+  } while (0)
+
+// per-block work timers (every block's thread 0): [32 + 4b + s] for the
+// SpMV, the Q^T w sums, phase B and phase C; barrier waits excluded
+#define BW_START()                                      \
+  do {                                                  \
+    if (a.prof && tid == 0) bw_last = gtimer();         \
+  } while (0)
+#define BW_STOP(slot)                                   \
+  do {                                                  \
+    if (a.prof && tid == 0) bw_acc[slot] += gtimer() - bw_last; \
   } while (0)
 
 template <int LG>
@@ -141,7 +152,7 @@ __device__ __forceinline__ void column_reduce(const LzArgs& a, int j, int r0, in
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
         const int tt = h * 32 + t;
-        q[h][t] = (live && tt <= j) ? a.Q[(int64_t)tt * a.ldq + i] : 0.0;
+        q[h][t] = (live && tt <= j) ? __ldcg(a.Q + qidx(i, tt, a.m + 1)) : 0.0;
       }
     double x = 0.0;
     if (live) x = rowfn(i, q);
@@ -163,13 +174,19 @@ __device__ __forceinline__ void column_reduce(const LzArgs& a, int j, int r0, in
   __syncthreads();
 }
 
-// out[t] = sum_{b < G} P[b*64 + t] for t < cols: one warp per column, lanes
-// stride over blocks (a few independent L2 loads each), fixed-order shuffles
+// out[t] = sum_{b < G} P[t*G + b] for t < cols: one warp per column, lanes
+// stride over blocks (coalesced: the column's partials are contiguous), all
+// loads issued before the fixed-order adds
 __device__ __forceinline__ void cross_block_sum(const double* P, int G, int cols, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int t = warp; t < cols; t += nw) {
-    double s = 0.0;
-    for (int bb = lane; bb < G; bb += 32) s += P[(int64_t)bb * 64 + t];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int bb = lane + 32 * u;
+      v[u] = bb < G ? P[(int64_t)t * G + bb] : 0.0;
+    }
+    double s = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
     s = warp_sum(s);
     if (lane == 0) out[t] = s;
   }
@@ -183,8 +200,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   const int tid = threadIdx.x, nth = blockDim.x, nw = nth >> 5;
   const int b = blockIdx.x, G = gridDim.x;
   const int r0 = a.blk_row[b], r1 = a.blk_row[b + 1];
-  const int i0 = a.blk_item[b], i1 = a.blk_item[b + 1];
-  const int s0 = a.blk_sr[b], s1 = a.blk_sr[b + 1];
+  const int e0 = a.blk_seg[b], e1 = a.blk_seg[b + 1];
 
   // shared memory carve-up
   double* wred = (double*)smem_raw;              // nw * 32 * NH
@@ -205,6 +221,11 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   js.mate = (int*)(js.red + 32);
   js.flag = js.mate + 64;
   js.ptab = (unsigned char*)(js.flag + 4);
+  // SpMV staging (after the Rayleigh-Ritz scratch, see the smem size below)
+  double* sp_prod = (double*)(js.ptab + JAC_PTAB_BYTES) + 6 * 64 + 64;  // LZT_NNZ
+  int* sp_rp = (int*)(sp_prod + LZT_NNZ);                             // LZT_ROWS + 1
+  int* sp_long = sp_rp + LZT_ROWS + 1;                                 // LZT_ROWS
+  int* sp_nl = sp_long + LZT_ROWS;                                     // 1
 
   int cycle = a.cycle0, ell = a.ell0, jstart = a.j0, restarts = a.restarts0, nhist = a.nhist0;
   int matvecs = a.matvecs0, wb = a.wbuf0;
@@ -214,6 +235,8 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   int converged = 0;
   unsigned long long lz_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long lz_last = (a.prof && b == 0 && tid == 0) ? gtimer() : 0ull;
+  unsigned long long bw_acc[4] = {0ull, 0ull, 0ull, 0ull}, bw_last = 0ull;
+  BW_START();
 
   for (; cycle <= a.max_restarts; ++cycle) {
     for (int j = jstart; j < m; ++j) {
@@ -223,45 +246,89 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       const double* xsrc;
       double xs;
       if (from_q) {
-        xsrc = a.Q + (int64_t)j * a.ldq;
+        xsrc = nullptr;  // gathers read Q[:, j] through qidx
         xs = 1.0;
       } else {
         xsrc = Wprev;
         xs = 1.0 / beta;
-        for (int i = r0 + tid; i < r1; i += nth) a.Q[(int64_t)j * a.ldq + i] = Wprev[i] * xs;
+        for (int i = r0 + tid; i < r1; i += nth) a.Q[qidx(i, j, M1)] = Wprev[i] * xs;
         if (b == 0 && tid == 0) {
           a.H[j * M1 + (j - 1)] = beta;
           a.H[(j - 1) * M1 + j] = beta;
         }
       }
-      {
-        // warp-uniform trip count: every lane reaches the group shuffles
-        constexpr int GPW = 32 / LG;
-        const int lane = tid & 31, warp = tid >> 5, gw = lane / LG, t = lane % LG;
-        for (int base = i0 + warp * GPW; base < i1; base += nw * GPW) {
-          const int it = base + gw;
-          const bool ok = it < i1;
-          double acc = 0.0;
-          if (ok) {
-            const int rb = a.it_beg[it], re = a.it_end[it];
-            for (int z = rb + t; z < re; z += LG) acc = fma(a.val[z], xsrc[a.col[z]] * xs, acc);
+      // SpMV over the block's segments (CSR-stream): a tile's nonzeros are
+      // loaded coalesced, LZT_NNZ / nth per thread in flight, products staged
+      // in smem and summed per row (a thread per short row, a warp per longer
+      // one); a row above LZT_NNZ nonzeros is summed by the whole block.
+      for (int e = e0; e < e1; ++e) {
+        const int t0 = a.seg_r0[e], t1 = a.seg_r1[e];
+        const int base = a.rowptr[t0], cnt = a.rowptr[t1] - base;
+        if (cnt > LZT_NNZ) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int z0 = 0; z0 < cnt; z0 += nth * 8) {
+            int cc[8];
+            double vv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int z = z0 + tid + nth * u;
+              cc[u] = z < cnt ? __ldcg(a.col + base + z) : -1;
+              vv[u] = z < cnt ? __ldcg(a.val + base + z) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (cc[u] >= 0) acc[u & 3] = fma(vv[u], (from_q ? a.Q[qidx(cc[u], j, M1)] : Wprev[cc[u]]) * xs, acc[u & 3]);
           }
-          acc = group_sum<LG>(acc);
-          if (ok && t == 0) {
-            const int sl = a.it_slot[it];
-            if (sl < 0) Wcur[a.it_row[it]] = acc;
-            else a.split[sl] = acc;
-          }
+          const double tot = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), red);
+          if (tid == 0) Wcur[t0] = tot;
+          continue;  // block_sum ends with a barrier
+        }
+        constexpr int PER = LZT_NNZ / (NH == 1 ? 512 : 256);
+        int cc[PER];
+        double vv[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int z = tid + u * nth;
+          cc[u] = z < cnt ? __ldcg(a.col + base + z) : 0;
+          vv[u] = z < cnt ? __ldcg(a.val + base + z) : 0.0;
+        }
+        for (int i = tid; i <= t1 - t0; i += nth) sp_rp[i] = a.rowptr[t0 + i] - base;
+        if (tid == 0) sp_nl[0] = 0;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int z = tid + u * nth;
+          if (z < cnt) sp_prod[z] = vv[u] * ((from_q ? a.Q[qidx(cc[u], j, M1)] : Wprev[cc[u]]) * xs);
         }
         __syncthreads();
-        for (int s = s0 + tid; s < s1; s += nth) {
-          const int f = a.sr_first[s], cnt = a.sr_count[s];
-          double acc = 0.0;
-          for (int u = 0; u < cnt; ++u) acc += a.split[f + u];
-          Wcur[a.sr_row[s]] = acc;
+        for (int il = tid; il < t1 - t0; il += nth) {
+          const int zb = sp_rp[il], ze = sp_rp[il + 1];
+          if (ze - zb > 32) {
+            sp_long[atomicAdd(sp_nl, 1)] = il;  // order irrelevant: one row, one sum
+            continue;
+          }
+          double sacc = 0.0;
+          for (int z = zb; z < ze; ++z) sacc += sp_prod[z];
+          Wcur[t0 + il] = sacc;
+        }
+        __syncthreads();
+        {
+          const int lane = tid & 31, warp = tid >> 5;
+          for (int q = warp; q < sp_nl[0]; q += nw) {
+            const int il = sp_long[q];
+            const int zb = sp_rp[il], ze = sp_rp[il + 1];
+            double sacc = 0.0;
+            for (int z = zb + lane; z < ze; z += 32) sacc += sp_prod[z];
+            sacc = warp_sum(sacc);
+            if (lane == 0) Wcur[t0 + il] = sacc;
+          }
         }
         __syncthreads();
       }
+      BW_STOP(0);
+      // the SpMV segments are balanced on nonzeros, the rows below on rows:
+      // every W row must be final before the column sums
+      grid.sync();
+      BW_START();
       ++matvecs;
       {
         int bad = 0;
@@ -271,11 +338,13 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
           return w;
         });
         if (__syncthreads_or(bad) && tid == 0) atomicOr(&a.flags[F_NONFINITE], 1);
-        for (int t = tid; t <= j; t += nth) a.P1[(int64_t)b * 64 + t] = red[t];
+        for (int t = tid; t <= j; t += nth) a.P1[(int64_t)t * G + b] = red[t];
       }
+      BW_STOP(1);
       LZ_MARK(0);
       grid.sync();
       LZ_MARK(1);
+      BW_START();
       // ------------------------------------------------------------ phase B
       if (*(volatile int*)&a.flags[F_NONFINITE]) {
         if (b == 0 && tid == 0) {
@@ -297,21 +366,45 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         Wcur[i] = w;
         return w;
       });
-      for (int t = tid; t <= j; t += nth) a.P2[(int64_t)b * 64 + t] = red[t];
+      for (int t = tid; t <= j; t += nth) a.P2[(int64_t)t * G + b] = red[t];
+      BW_STOP(2);
       LZ_MARK(2);
       grid.sync();
       LZ_MARK(1);
+      BW_START();
       // ------------------------------------------------------------ phase C
       cross_block_sum(a.P2, G, j + 1, c2vec);
       __syncthreads();
       {
+        // w'' = w' - Q c' with the row's Q entries loaded unrolled (all in
+        // flight at once), lane = row
+        const int lane = tid & 31, warp = tid >> 5;
         double ss = 0.0;
-        for (int i = r0 + tid; i < r1; i += nth) {
-          double s = 0.0;
-          for (int t = 0; t <= j; ++t) s = fma(a.Q[(int64_t)t * a.ldq + i], c2vec[t], s);
-          double w = Wcur[i] - s;
-          Wcur[i] = w;
-          ss = fma(w, w, ss);
+        for (int base = r0 + warp * 32; base < r1; base += nw * 32) {
+          const int i = base + lane;
+          const bool live = i < r1;
+          double q[NH][32];
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const int tt = h * 32 + t;
+              q[h][t] = (live && tt <= j) ? __ldcg(a.Q + qidx(i, tt, M1)) : 0.0;
+            }
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int t = 0; t < 32; t += 2) {
+              const int tt = h * 32 + t;
+              if (tt <= j) s0 = fma(q[h][t], c2vec[tt], s0);
+              if (tt + 1 <= j) s1 = fma(q[h][t + 1], c2vec[tt + 1], s1);
+            }
+          if (live) {
+            const double w = Wcur[i] - (s0 + s1);
+            Wcur[i] = w;
+            ss = fma(w, w, ss);
+          }
         }
         ss = block_sum(ss, red);
         if (tid == 0) a.P3[b] = ss;
@@ -329,12 +422,17 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         for (int t = 0; t <= j; ++t) mx = fmax(mx, fabs(cvec[t]));
         misc[0] = fmax(1.0, mx);
       }
+      BW_STOP(3);
       LZ_MARK(3);
       grid.sync();
       LZ_MARK(1);
+      BW_START();
       if (tid < 32) {
         double s = 0.0;
-        for (int bb = tid; bb < G; bb += 32) s += a.P3[bb];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (tid + 32 * u < G) ? a.P3[tid + 32 * u] : 0.0;
+        s = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         s = warp_sum(s);
         if (tid == 0) misc[1] = sqrt(s);
       }
@@ -362,7 +460,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
     if (pending) {
       double* Wprev = wb ? a.W1 : a.W0;
       const double xs = 1.0 / beta;
-      for (int i = r0 + tid; i < r1; i += nth) a.Q[(int64_t)m * a.ldq + i] = Wprev[i] * xs;
+      for (int i = r0 + tid; i < r1; i += nth) a.Q[qidx(i, m, M1)] = Wprev[i] * xs;
       if (b == 0 && tid == 0) {
         a.H[m * M1 + (m - 1)] = beta;
         a.H[(m - 1) * M1 + m] = beta;
@@ -416,13 +514,13 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
     ell = max(1, min(a.k_c + 3, m - 2));
     for (int i = r0 + tid; i < r1; i += nth) {
       double qrow[64];
-      for (int t = 0; t < m; ++t) qrow[t] = a.Q[(int64_t)t * a.ldq + i];
+      for (int t = 0; t < m; ++t) qrow[t] = a.Q[qidx(i, t, M1)];
       for (int u = 0; u < ell; ++u) {
         double s = 0.0;
         for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
-        a.Q[(int64_t)u * a.ldq + i] = s;
+        a.Q[qidx(i, u, M1)] = s;
       }
-      a.Q[(int64_t)ell * a.ldq + i] = a.Q[(int64_t)m * a.ldq + i];
+      a.Q[qidx(i, ell, M1)] = a.Q[qidx(i, m, M1)];
     }
     ++restarts;
     jstart = ell;
@@ -441,9 +539,11 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
   // ---------------------------------------------------------------- output
   if (a.prof && b == 0 && tid == 0)
     for (int s = 0; s < 8; ++s) a.prof[s] += lz_acc[s];
+  if (a.prof && tid == 0)
+    for (int s = 0; s < 4; ++s) a.prof[32 + 4 * b + s] += bw_acc[s];
   for (int i = r0 + tid; i < r1; i += nth) {
     double qrow[64];
-    for (int t = 0; t < m; ++t) qrow[t] = a.Q[(int64_t)t * a.ldq + i];
+    for (int t = 0; t < m; ++t) qrow[t] = a.Q[qidx(i, t, M1)];
     for (int u = 0; u < a.k_c; ++u) {
       double s = 0.0;
       for (int t = 0; t < m; ++t) s = fma(qrow[t], Ys[t * m + u], s);
@@ -546,7 +646,7 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   // Q for the own rows from global (start vector / restart state / reseed)
   for (int x = tid; x < M1 * nloc; x += nth) {
     const int t = x / nloc, i = x % nloc;
-    Qs[(size_t)t * R + i] = a.Q[(int64_t)t * a.ldq + r0 + i];
+    Qs[(size_t)t * R + i] = a.Q[qidx(r0 + i, t, M1)];
   }
   for (int i = tid; i <= nloc; i += nth) rp[i] = a.rowptr[r0 + i];
   cluster.sync();
@@ -744,7 +844,7 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
         // spill Q for the host reseed (the host uses columns 0..j)
         for (int x = tid; x < M1 * nloc; x += nth) {
           const int t = x / nloc, i = x % nloc;
-          a.Q[(int64_t)t * a.ldq + r0 + i] = Qs[(size_t)t * R + i];
+          a.Q[qidx(r0 + i, t, M1)] = Qs[(size_t)t * R + i];
         }
         if (b == 0 && tid == 0) {
           a.flags[F_EXIT] = EXIT_BREAKDOWN;
@@ -852,24 +952,31 @@ __global__ void k_copy(int64_t n, const double* __restrict__ x, double* __restri
 }
 
 // c[t] = Q[:, t] . v  for t < used  (one block per column, deterministic)
-__global__ void k_colmajor_dot(int64_t n, const double* __restrict__ Q, int64_t ldq,
-                               const double* __restrict__ v, double* __restrict__ c) {
+// reseed helpers on the row-blocked Q: c[t] = Q[:, t] . v (one block per t),
+// v -= Q[:, :used] c, Q[:, t] = s * v (v == nullptr: zero)
+__global__ void k_qcol_dot(int64_t n, const double* __restrict__ Q, int M1, const double* __restrict__ v,
+                           double* __restrict__ c) {
   __shared__ double red[32];
   const int t = blockIdx.x;
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(Q[(int64_t)t * ldq + i], v[i], s);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(Q[qidx(i, t, M1)], v[i], s);
   s = block_sum(s, red);
   if (threadIdx.x == 0) c[t] = s;
 }
 
-// v -= Q[:, :used] c ; then scale v by 1/||v|| is done separately
-__global__ void k_colmajor_sub(int64_t n, const double* __restrict__ Q, int64_t ldq, int used,
-                               const double* __restrict__ c, double* __restrict__ v) {
+__global__ void k_qcol_sub(int64_t n, const double* __restrict__ Q, int M1, int used, const double* __restrict__ c,
+                           double* __restrict__ v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int t = 0; t < used; ++t) s = fma(Q[(int64_t)t * ldq + i], c[t], s);
+    for (int t = 0; t < used; ++t) s = fma(Q[qidx(i, t, M1)], c[t], s);
     v[i] -= s;
   }
+}
+
+__global__ void k_qcol_set(int64_t n, const double* __restrict__ v, double sc, double* __restrict__ Q, int t,
+                           int M1) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    Q[qidx(i, t, M1)] = v ? v[i] * sc : 0.0;
 }
 
 __global__ void k_norm2(int64_t n, const double* __restrict__ v, double* __restrict__ out) {
@@ -1116,10 +1223,10 @@ using namespace usbs;
 // [phase A, grid barriers, phase B, phase C, end of cycle, Rayleigh-Ritz, restart, -]
 extern "C" usbs_status usbs_lanczos_profile(usbs_ctx* ctx, unsigned long long* out, int reset) {
   USBS_API_BEGIN
-  auto* p = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 16 * sizeof(unsigned long long));
-  USBS_CUDA(cudaMemcpyAsync(out, p, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  auto* p = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 1024 * sizeof(unsigned long long));
+  USBS_CUDA(cudaMemcpyAsync(out, p, 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   USBS_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 16 * sizeof(unsigned long long), ctx->stream));
+  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 1024 * sizeof(unsigned long long), ctx->stream));
   USBS_API_END
 }
 
@@ -1191,24 +1298,25 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   double* W = (double*)ctx->ws.get(WS_LZ_W, (size_t)2 * ldq * sizeof(double));
   double* H = (double*)ctx->ws.get(WS_LZ_H, (size_t)(m + 1) * (m + 1) * sizeof(double));
   double* P = (double*)ctx->ws.get(WS_LZ_P, (size_t)(G * 64 * 2 + G) * sizeof(double));
-  double* SP = (double*)ctx->ws.get(WS_LZ_SPLIT, (size_t)std::max(1, p->n_split_items) * sizeof(double));
   int* flags = (int*)ctx->ws.get(WS_LZ_FLAGS, 64 * sizeof(int));
   double* out = (double*)ctx->ws.get(WS_LZ_OUT, (size_t)(m + m * m + m + max_restarts + 1 + 8) * sizeof(double));
   double* tmp = (double*)ctx->ws.get(WS_LZ_TMP, (size_t)(ldq + 128) * sizeof(double));
   USBS_CUDA(cudaMemsetAsync(H, 0, (size_t)(m + 1) * (m + 1) * sizeof(double), st));
   USBS_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), st));
-  USBS_CUDA(cudaMemcpyAsync(Q, v0, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  {
+    int bl0 = (int)std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms);
+    k_qcol_set<<<bl0, 256, 0, st>>>(n, v0, 1.0, Q, 0, m + 1);
+    check_launch(ctx);
+  }
 
   LzArgs a{};
   a.n = (int)n; a.m = m; a.k_c = k_c; a.max_restarts = max_restarts; a.ldq = ldq;
   a.tol = tol < 0 ? 1e-9 : tol;
   a.rowptr = p->rowptr; a.col = p->col; a.val = val;
-  a.it_row = p->it_row; a.it_beg = p->it_beg; a.it_end = p->it_end; a.it_slot = p->it_slot;
-  a.blk_item = p->blk_item; a.blk_row = p->blk_row; a.blk_sr = p->blk_sr;
-  a.sr_row = p->sr_row; a.sr_first = p->sr_first; a.sr_count = p->sr_count;
+  a.blk_row = p->blk_row; a.blk_seg = p->blk_seg; a.seg_r0 = p->seg_r0; a.seg_r1 = p->seg_r1;
   a.Q = Q; a.W0 = W; a.W1 = W + ldq; a.H = H;
   a.P1 = P; a.P2 = P + G * 64; a.P3 = P + 2 * G * 64;
-  a.split = SP; a.flags = flags;
+  a.flags = flags;
   a.theta = out; a.Y = out + m; a.res = out + m + m * m; a.hist = out + 2 * m + m * m;
   a.vecs_out = vecs_dev; a.ldvecs = ldvecs;
   a.cycle0 = 0; a.ell0 = 0; a.j0 = 0; a.restarts0 = 0; a.nhist0 = 0; a.matvecs0 = 0; a.wbuf0 = 0;
@@ -1216,16 +1324,17 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   a.prof = nullptr;
   if (getenv("USBS_LZ_PROF")) {
     static bool zeroed = false;
-    a.prof = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 16 * sizeof(unsigned long long));
+    a.prof = (unsigned long long*)ctx->ws.get(WS_LZ_PROF, 1024 * sizeof(unsigned long long));
     if (!zeroed) {
-      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 16 * sizeof(unsigned long long), st));
+      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 1024 * sizeof(unsigned long long), st));
       zeroed = true;
     }
   }
 
   const int nw = (NH == 1 ? 512 : 256) / 32;
   size_t smem = (size_t)(nw * 32 * NH + 64 * 3 + 8 + 64 + m * m + 4 * m * m + 64 * 2 + 32) * sizeof(double) +
-                68 * sizeof(int) + JAC_PTAB_BYTES + (6 * 64) * sizeof(double) + 128 * sizeof(int) + 64;
+                68 * sizeof(int) + JAC_PTAB_BYTES + (6 * 64) * sizeof(double) + 128 * sizeof(int) + 64 +
+                LZT_NNZ * sizeof(double) + (2 * LZT_ROWS + 2) * sizeof(int);
   // small operators: one thread-block cluster with Q resident in smem
   const LzClusterPlan clp = lz_cached_plan(ctx, p, m);
   int64_t ctr = 0;
@@ -1256,9 +1365,9 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
       int thr = 256, bl = (int)std::min<int64_t>((n + thr - 1) / thr, 4 * ctx->num_sms);
       k_scale_into<<<bl, thr, 0, st>>>(n, v, 1.0 / nv0, v);
       check_launch(ctx);
-      k_colmajor_dot<<<used, 512, 0, st>>>(n, Q, ldq, v, cbuf);
+      k_qcol_dot<<<used, 512, 0, st>>>(n, Q, m + 1, v, cbuf);
       check_launch(ctx);
-      k_colmajor_sub<<<bl, thr, 0, st>>>(n, Q, ldq, used, cbuf, v);
+      k_qcol_sub<<<bl, thr, 0, st>>>(n, Q, m + 1, used, cbuf, v);
       check_launch(ctx);
       k_norm2<<<1, 1024, 0, st>>>(n, v, cbuf + 64);
       check_launch(ctx);
@@ -1266,12 +1375,16 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
       USBS_CUDA(cudaStreamSynchronize(st));
       double nv = std::sqrt(ctx->pinned[0]);
       if (nv > 1e-8) {
-        k_scale_into<<<bl, thr, 0, st>>>(n, v, 1.0 / nv, Q + (int64_t)(j + 1) * ldq);
+        k_qcol_set<<<bl, thr, 0, st>>>(n, v, 1.0 / nv, Q, j + 1, m + 1);
         check_launch(ctx);
         got = true;
       }
     }
-    if (!got) USBS_CUDA(cudaMemsetAsync(Q + (int64_t)(j + 1) * ldq, 0, n * sizeof(double), st));
+    if (!got) {
+      int bl = (int)std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms);
+      k_qcol_set<<<bl, 256, 0, st>>>(n, nullptr, 0.0, Q, j + 1, m + 1);
+      check_launch(ctx);
+    }
     const int M1 = m + 1;
     double zero = 0.0;
     USBS_CUDA(cudaMemcpyAsync(H + (j + 1) * M1 + j, &zero, sizeof(double), cudaMemcpyHostToDevice, st));

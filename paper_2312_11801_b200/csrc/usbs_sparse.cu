@@ -464,31 +464,57 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->n_split_items = nsplit;
   p->n_split_rows = (int)srow.size();
 
-  // --- Lanczos block partition (row aligned, balanced on nnz + row cost)
+  // --- Lanczos grid partition: rows for the Q passes, SpMV segments apart
   // leave 4 SMs free for kernels that overlap the Lanczos kernel (the
   // model-evaluation IPM on the auxiliary stream)
   int G = (int)std::min<int64_t>(std::max(1, ctx->num_sms - 4),
                                  std::max<int64_t>(1, std::max<int64_t>((n + 63) / 64, (p->nnz + n + 4095) / 4096)));
   if (const char* env = getenv("USBS_LZ_BLOCKS")) G = std::max(1, std::min(ctx->num_sms, atoi(env)));
   p->lz_blocks = G;
-  std::vector<int32_t> blk_row(G + 1, (int32_t)n), blk_item(G + 1, p->n_items), blk_sr(G + 1, p->n_split_rows);
+  std::vector<int32_t> blk_row(G + 1, (int32_t)n), blk_seg(G + 1, 0), seg_r0, seg_r1;
   {
-    const double ROWCOST = 4.0;
-    double total = (double)p->nnz + ROWCOST * n;
+    // rows (the CGS2 passes over Q): balanced on rows; the SpMV runs in its
+    // own phase, so its segments are balanced separately on nonzeros
+    const double NNZCOST = 0.02;  // row loop bookkeeping per nonzero, in row units
+    double total = (double)n + NNZCOST * (double)p->nnz;
     double acc = 0.0;
     int b = 0;
     blk_row[0] = 0;
     for (int64_t i = 0; i < n && b + 1 < G; ++i) {
-      acc += (rp32[i + 1] - rp32[i]) + ROWCOST;
+      acc += 1.0 + NNZCOST * (rp32[i + 1] - rp32[i]);
       if (acc >= total * (b + 1) / G) blk_row[++b] = (int32_t)(i + 1);
     }
     for (int bb = b + 1; bb < G; ++bb) blk_row[bb] = (int32_t)n;
     blk_row[G] = (int32_t)n;
-    // items and split rows are sorted by row: locate the boundaries
-    for (int bb = 0; bb <= G; ++bb) {
-      blk_item[bb] = (int32_t)(std::lower_bound(irow.begin(), irow.end(), blk_row[bb]) - irow.begin());
-      blk_sr[bb] = (int32_t)(std::lower_bound(srow.begin(), srow.end(), blk_row[bb]) - srow.begin());
+    // align the boundaries to the 32-row tiles of the Lanczos basis layout
+    for (int bb = 1; bb < G; ++bb) blk_row[bb] = (int32_t)std::min<int64_t>(n, (blk_row[bb] + 31) / 32 * 32);
+    for (int bb = 1; bb <= G; ++bb) blk_row[bb] = std::max(blk_row[bb], blk_row[bb - 1]);
+    // SpMV segments over the whole matrix: <= LZT_NNZ nonzeros and
+    // <= LZT_ROWS rows, or one row with more
+    int64_t i = 0;
+    while (i < n) {
+      const int64_t s0 = i;
+      if (rp32[i + 1] - rp32[i] > LZT_NNZ) {
+        ++i;
+      } else {
+        while (i < n && i - s0 < LZT_ROWS && rp32[i + 1] - rp32[i] <= LZT_NNZ && rp32[i + 1] - rp32[s0] <= LZT_NNZ)
+          ++i;
+      }
+      seg_r0.push_back((int32_t)s0);
+      seg_r1.push_back((int32_t)i);
     }
+    // contiguous segment ranges per block, balanced on nonzeros + 2 per row
+    const int64_t ns = (int64_t)seg_r0.size();
+    double stot = 0.0;
+    for (int64_t e = 0; e < ns; ++e) stot += (rp32[seg_r1[e]] - rp32[seg_r0[e]]) + 2.0 * (seg_r1[e] - seg_r0[e]);
+    double sacc = 0.0;
+    int sb = 0;
+    blk_seg[0] = 0;
+    for (int64_t e = 0; e < ns && sb + 1 < G; ++e) {
+      sacc += (rp32[seg_r1[e]] - rp32[seg_r0[e]]) + 2.0 * (seg_r1[e] - seg_r0[e]);
+      if (sacc >= stot * (sb + 1) / G) blk_seg[++sb] = (int32_t)(e + 1);
+    }
+    for (int bb = sb + 1; bb <= G; ++bb) blk_seg[bb] = (int32_t)ns;
   }
   std::vector<int32_t> diag_slot;
   if (p->diag_only) {
@@ -575,8 +601,9 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->sr_first = dev_upload(p, sfirst.data(), sfirst.size());
   p->sr_count = dev_upload(p, scount.data(), scount.size());
   p->blk_row = dev_upload(p, blk_row.data(), blk_row.size());
-  p->blk_item = dev_upload(p, blk_item.data(), blk_item.size());
-  p->blk_sr = dev_upload(p, blk_sr.data(), blk_sr.size());
+  p->blk_seg = dev_upload(p, blk_seg.data(), blk_seg.size());
+  p->seg_r0 = dev_upload(p, seg_r0.data(), seg_r0.size());
+  p->seg_r1 = dev_upload(p, seg_r1.data(), seg_r1.size());
   *out = p;
 }
 

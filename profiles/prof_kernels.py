@@ -51,7 +51,7 @@ def main(which):
             j0 = ell
         print(f"  algorithmic {tot / 1e9:.3f} GB/call -> {tot / dt / 1e9:.0f} GB/s")
         if os.environ.get("USBS_LZ_PROF"):
-            out = (C.c_uint64 * 12)()
+            out = (C.c_uint64 * 1024)()
             dp.rt.lib.usbs_lanczos_profile(dp.rt.h, out, 1)
             names = ["phaseA", "barriers", "phaseB", "phaseC", "endcycle", "rayleigh_ritz", "restart",
                      "spmv(cluster)"]
@@ -61,6 +61,13 @@ def main(which):
             nrr = (reps + 4) * (r.restarts + 1)
             for nm, v in zip(["setup", "bisection", "inverse-it", "output"], out[8:12]):
                 print(f"    rr {nm:12s} {v / 1e3 / nrr:8.2f} us per Rayleigh-Ritz")
+            G = dp.info().lanczos_blocks
+            pb = np.array([[out[32 + 4 * b + q] for q in range(4)] for b in range(G)], float)
+            pb /= 1e3 * (reps + 4) * r.matvecs
+            if pb.sum() > 0:
+                for q, nm in enumerate(["spmv", "Q^T w", "phase B", "phase C"]):
+                    print(f"  per-block {nm:8s} us/step: mean {pb[:, q].mean():6.1f} max {pb[:, q].max():6.1f} "
+                          f"(b={pb[:, q].argmax()}) min {pb[:, q].min():6.1f}")
         if os.environ.get("USBS_LZ_SWEEP"):
             for g in (8, 16, 32, 64, 148):
                 os.environ["USBS_LZ_BLOCKS"] = str(g)
