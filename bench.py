@@ -271,6 +271,10 @@ def run_device(args):
     peak, peak_src = peaks()
     lz_share = float(np.sum(lz_ms)) / total_ms if total_ms else None
     tr = traffic_from_profile()
+    cs, rows = ds.dp.lanczos_plan(max(32, cfg_b.k_c + 1))
+    lz_kernel = (f"k_lanczos_cl (one {cs}-CTA thread-block cluster, Q resident in shared memory, "
+                 f"{rows} rows per CTA; 1 launch per lanczos_top)" if cs else
+                 "k_lanczos (persistent cooperative grid; 1 launch per lanczos_top)")
 
     # ---- e2e: public API from host buffers (problem upload + per-iteration y D2H inside the timed region)
     torch.cuda.synchronize()
@@ -320,12 +324,14 @@ def run_device(args):
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "flushed (256 MiB write) between timed iterations",
                        "step": "one USBS outer iteration"},
-            "roofline": {"kernel": "k_lanczos (persistent thick-restart Lanczos, 1 launch per lanczos_top)",
+            "roofline": {"kernel": lz_kernel,
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": avg_ms,
                          "launches": len(lz), "share_of_step": lz_share,
-                         "note": "C2 working set (Z 0.7 MB, Q 2.6 MB) is L2-resident; latency-bound"},
+                         "note": "C2 working set (Z 0.7 MB, Q 2.6 MB) lives in shared memory / L2: the HBM "
+                                 "fraction is low by construction; the kernel is latency-bound (3 cluster "
+                                 "barriers per step, Rayleigh-Ritz per cycle), see DESIGN.md"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / max(e2e_steps, 1),
                     "d2h_bytes_per_step": d2h["bytes"] / max(e2e_steps, 1),
@@ -379,6 +385,24 @@ def c4_operator_apply(rt):
         ms = float(np.median(ts))
         gbs = b / (ms / 1e3) / 1e9
         out[f"k{k}"] = {"ms": ms, "algorithmic_bytes": b, "achieved_gbs": gbs, "frac_of_measured_peak": gbs / peak}
+    # one lanczos_top on the C4 slack operator (grid kernel, Q streamed from HBM)
+    from paper_2312_11801_b200 import eigen
+    op = eigen.dual_slack_operator(dp, y)
+    eigen.lanczos_top(op, 10, seed=0)
+    ts, r = [], None
+    for _ in range(3):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(rt.stream)
+        r = eigen.lanczos_top(op, 10, seed=0)
+        e1.record(rt.stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    b = lanczos_bytes(p.n, info.nnz_z, r.restarts)
+    out["lanczos_top"] = {"ms": ms, "matvecs": r.matvecs, "restarts": r.restarts, "algorithmic_bytes": b,
+                          "achieved_gbs": b / (ms / 1e3) / 1e9, "frac_of_measured_peak": b / (ms / 1e3) / 1e9 / peak,
+                          "kernel": "k_lanczos (grid)"}
     return out
 
 

@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB) k_spmv_fused(int nhuge, cons
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int z = z0 + tid + ST_THREADS * u;
-        cc[u] = z < ze ? __ldg(col + z) : -1;
-        vv[u] = z < ze ? __ldg(val + z) : 0.0;
+        cc[u] = z < ze ? __ldcg(col + z) : -1;
+        vv[u] = z < ze ? __ldcg(val + z) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(ST_THREADS, MINB) k_spmv_fused(int nhuge, cons
 #pragma unroll
   for (int u = 0; u < ST_NNZ / ST_THREADS; ++u) {
     const int z = tid + u * ST_THREADS;
-    cc[u] = z < cnt ? __ldg(col + base + z) : 0;
-    vv[u] = z < cnt ? __ldg(val + base + z) : 0.0;
+    cc[u] = z < cnt ? __ldcg(col + base + z) : 0;
+    vv[u] = z < cnt ? __ldcg(val + base + z) : 0.0;
   }
   for (int i = tid; i <= r1 - r0; i += ST_THREADS) rps[i] = __ldg(rowptr + r0 + i) - base;
   if (tid == 0) nlong = 0;
