@@ -42,37 +42,49 @@ __global__ void k_image_diag(int64_t n, const double* __restrict__ V, int64_t ld
   }
 }
 
-__global__ void k_image_entries(int64_t m, const int* __restrict__ cptr, const int* __restrict__ cent,
-                                const int* __restrict__ erow, const int* __restrict__ ecol,
-                                const double* __restrict__ eval, const double* __restrict__ V, int64_t ldv,
-                                int k, const double* __restrict__ S, int sdiag, double sscale,
-                                const double* beta_dev, double beta, const double* __restrict__ base,
-                                double* __restrict__ out) {
-  __shared__ double Ss[64 * 64];
-  for (int x = threadIdx.x; x < (sdiag ? k : k * k); x += blockDim.x) Ss[x] = sscale * S[x];
+// A(V S V^T) for entry constraints: <A_i, V S V^T> = sum over the entries
+// (r, c, val) of constraint i of (2 - [r == c]) val (V S V^T)[r, c], with
+// (V S V^T)[r, c] = W[r, :] . V[c, :] and W = V S computed once by k_rowgemm
+// (k FMAs per entry instead of k^2).  Eight lanes per constraint stride over
+// its entries; a fixed shuffle tree sums them (deterministic).
+__global__ void __launch_bounds__(256) k_image_entries(int64_t m, const int* __restrict__ cptr,
+                                                       const int* __restrict__ cent, const int* __restrict__ erow,
+                                                       const int* __restrict__ ecol, const double* __restrict__ eval,
+                                                       const double* __restrict__ V, int64_t ldv,
+                                                       const double* __restrict__ W, int64_t ldw, int k,
+                                                       const double* __restrict__ S, int sdiag, double sscale,
+                                                       const double* beta_dev, double beta,
+                                                       const double* __restrict__ base, double* __restrict__ out) {
+  __shared__ double Sd[64];
+  if (sdiag)
+    for (int x = threadIdx.x; x < k; x += blockDim.x) Sd[x] = sscale * S[x];
   if (beta_dev) beta *= beta_dev[0];
   __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, gw = lane >> 3, t = lane & 7;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wb = wid * 4; wb < m; wb += nwarps * 4) {
+    const int64_t i = wb + gw;
     double acc = 0.0;
-    for (int t = cptr[i]; t < cptr[i + 1]; ++t) {
-      const int e = cent[t];
-      const int r = erow[e], c = ecol[e];
-      const double* vr = V + (int64_t)r * ldv;
-      const double* vc = V + (int64_t)c * ldv;
-      double q = 0.0;
-      if (sdiag) {
-        for (int j = 0; j < k; ++j) q = fma(vr[j] * Ss[j], vc[j], q);
-      } else {
-        for (int j = 0; j < k; ++j) {
-          double mid = 0.0;
-          for (int l = 0; l < k; ++l) mid = fma(vr[l], Ss[l * k + j], mid);
-          q = fma(mid, vc[j], q);
+    if (i < m) {
+      for (int q = cptr[i] + t; q < cptr[i + 1]; q += 8) {
+        const int e = cent[q];
+        const int r = erow[e], c = ecol[e];
+        const double* vc = V + (int64_t)c * ldv;
+        double v = 0.0;
+        if (sdiag) {
+          const double* vr = V + (int64_t)r * ldv;
+          for (int j = 0; j < k; ++j) v = fma(vr[j] * Sd[j], vc[j], v);
+        } else {
+          const double* wr = W + (int64_t)r * ldw;
+          for (int j = 0; j < k; ++j) v = fma(wr[j], vc[j], v);
         }
+        acc = fma(v, (r == c) ? eval[e] : 2.0 * eval[e], acc);
       }
-      const double eff = (r == c) ? eval[e] : 2.0 * eval[e];
-      acc += q * eff;
     }
-    out[i] = (base ? beta * base[i] : 0.0) + acc;
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 8);
+    if (i < m && t == 0) out[i] = (base ? beta * base[i] : 0.0) + acc;
   }
 }
 
@@ -562,19 +574,51 @@ usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* V, int
     k_image_diag<<<nblocks(ctx, p->n), 256, 0, ctx->stream>>>(p->n, V, ldv, k, S, s_is_diag, s_scale, beta_dev, beta,
                                                               base, out);
   } else {
-    k_image_entries<<<nblocks(ctx, p->m), 256, 0, ctx->stream>>>(p->m, p->cptr, p->cent, p->e_row, p->e_col,
-                                                                 p->e_val, V, ldv, k, S, s_is_diag, s_scale, beta_dev,
-                                                                 beta, base, out);
+    const double* W = nullptr;
+    if (!s_is_diag) {
+      if (k * k > 4096) fail(USBS_ERR_SHAPE, "cons_image: k too large for a dense S");
+      const int64_t nv = std::max<int64_t>(p->n, p->n_cols);
+      double* Wb = (double*)ctx->ws.get(WS_BOOK_W, (size_t)nv * k * sizeof(double));
+      k_rowgemm<<<nblocks(ctx, nv * k), 256, 0, ctx->stream>>>(nv, V, ldv, k, S, k, k, nullptr, s_scale, 0.0,
+                                                               nullptr, 0, Wb, k);
+      check_launch(ctx);
+      W = Wb;
+    }
+    k_image_entries<<<nblocks(ctx, (p->m + 3) / 4 * 32), 256, 0, ctx->stream>>>(
+        p->m, p->cptr, p->cent, p->e_row, p->e_col, p->e_val, V, ldv, W, k, k, S, s_is_diag, s_scale, beta_dev,
+        beta, base, out);
   }
   check_launch(ctx);
   USBS_API_END
 }
+
+__global__ void k_svec(int k, const double* __restrict__ A, double scale, double* __restrict__ out);
 
 usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k,
                                  double scale_gram, double* gram_out, const double* a_vec, double scale_a,
                                  double* a_out, const double* w_vec, double scale_w, double* w_out) {
   USBS_API_BEGIN
   if (k < 1 || k > 32) fail(USBS_ERR_SHAPE, "cons_compressed: 1 <= k <= 32");
+  if (!p->diag_only && p->n_cols == p->n && (a_vec || w_vec)) {
+    // sum_i v_i c_i = svec(V^T A*(v) V): assemble A*(v) on the merged
+    // pattern, one SpMM and one Gram (O(E + nnz k + n k^2) instead of the
+    // O(E d) row-by-row generation); the d x d Gram below needs the rows
+    double* tval = (double*)ctx->ws.get(WS_BOOK_T, (size_t)p->nnz * sizeof(double));
+    double* Y = (double*)ctx->ws.get(WS_BOOK_W, (size_t)p->n * k * sizeof(double));
+    double* G = (double*)ctx->ws.get(WS_BOOK_G, (size_t)k * k * sizeof(double));
+    for (int u = 0; u < 2; ++u) {
+      const double* vec = u ? w_vec : a_vec;
+      if (!vec) continue;
+      launch_adjoint_values(ctx, p, vec, tval);
+      launch_spmm_vals(ctx, p, tval, V, ldv, k, Y, k);
+      launch_gram_tn(ctx, p->n, V, ldv, k, Y, k, k, G, true);
+      k_svec<<<1, 256, 0, ctx->stream>>>(k, G, u ? scale_w : scale_a, u ? w_out : a_out);
+      check_launch(ctx);
+    }
+    a_vec = nullptr;
+    w_vec = nullptr;
+    if (!gram_out) return USBS_OK;
+  }
   const int d = k * (k + 1) / 2;
   const int nt = (d + 3) / 4, ntiles = nt * (nt + 1) / 2;
   const int tpt = gram_out ? (ntiles + 255) / 256 : 1;

@@ -68,7 +68,7 @@ __device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; 
 
 struct IpmSmem {
   double *S, *T, *H, *dS, *dT, *W1, *W2, *X1, *X2;  // k x k
-  double *s, *t, *vI, *h, *g, *f1, *rhs, *ds, *dt, *rd, *tmp;  // d
+  double *s, *t, *vI, *h, *g, *f1, *rhs, *ds, *dt, *rd, *tmp, *cb0, *cb1;  // d
   unsigned char *pi, *pj;
   double* red;   // 32
   double* sc;    // scalars 64
@@ -207,6 +207,112 @@ __device__ double trace_k(const double* A, int k) {
   return tr;
 }
 
+
+// D = A B + C on the FP64 tensor cores (m8n8k4): a = A[lane>>2][lane&3],
+// b = B[lane&3][lane>>2], c/d = C[lane>>2][2(lane&3) + {0,1}]
+__device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+// Blocked right-looking Cholesky of the packed lower matrix M (d x d) by
+// 8-column panels: (1) the 8 x 8 diagonal block by one warp (potrf: fails on
+// a pivot <= 0 or NaN), (2) the panel below it by forward substitution, a
+// thread per row, (3) the trailing update C_IK -= L_IJ L_KJ^T per 8 x 8 tile
+// pair with two DMMA m8n8k4 per tile, warps over tile pairs.  rdiag[j] =
+// 1 / L_jj.  Returns 0 on failure (uniform).
+__device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ rdiag, int* flag) {
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwp = nth >> 5;
+  const int T = (d + 7) >> 3;
+  for (int J = 0; J < T; ++J) {
+    const int j0 = J * 8, jb = min(8, d - j0);
+    // (1) diagonal block by warp 0: lane l owns entries (l >> 3, l & 7) and
+    // (4 + (l >> 3), l & 7) of the 8 x 8 block (row i, column t, t <= i);
+    // per column: the pivot and the two column values each update needs
+    // arrive by shuffle, so the chain is shfl -> rsqrt -> shfl -> fma
+    if (warp == 0) {
+      const int t = lane & 7, ia = lane >> 3, ib = 4 + (lane >> 3);
+      double ea = (ia < jb && t <= ia) ? Mp[pidx(j0 + ia, j0 + t)] : 0.0;
+      double eb = (ib < jb && t <= ib) ? Mp[pidx(j0 + ib, j0 + t)] : 0.0;
+      int ok = 1;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < jb) {
+          // pivot (c, c): lane (c & 3) * 8 + c, entry a if c < 4 else b
+          const double pv = __shfl_sync(0xffffffffu, c < 4 ? ea : eb, (c & 3) * 8 + c);
+          if (!(pv > 0.0)) ok = 0;
+          const double r = ok ? rsqrt(pv) : 0.0;
+          // column c: entries (i, c) for i >= c live on lanes (i & 3) * 8 + c
+          if (t == c) {
+            if (ia > c) ea *= r; else if (ia == c) ea = pv * r;
+            if (ib > c) eb *= r; else if (ib == c) eb = pv * r;
+          }
+          if (lane == 0) rdiag[j0 + c] = r;
+          // trailing: e(i, t) -= L(i, c) L(t, c) for c < t <= i
+          const double lia = __shfl_sync(0xffffffffu, ea, (ia & 3) * 8 + c);  // L(ia, c), ia < 4
+          const double lib = __shfl_sync(0xffffffffu, eb, (ib & 3) * 8 + c);  // L(ib, c)
+          const double lta_a = __shfl_sync(0xffffffffu, ea, (t & 3) * 8 + c);
+          const double lta_b = __shfl_sync(0xffffffffu, eb, (t & 3) * 8 + c);
+          const double lta = t < 4 ? lta_a : lta_b;  // L(t, c)
+          if (t > c) {
+            if (t <= ia) ea -= lia * lta;
+            if (t <= ib) eb -= lib * lta;
+          }
+        }
+      }
+      if (ia < jb && t <= ia) Mp[pidx(j0 + ia, j0 + t)] = ea;
+      if (ib < jb && t <= ib) Mp[pidx(j0 + ib, j0 + t)] = eb;
+      if (lane == 0) *flag = ok;
+    }
+    __syncthreads();
+    if (!*flag) return 0;
+    // (2) panel rows below: x = a L_JJ^{-T}
+    for (int i = j0 + jb + tid; i < d; i += nth) {
+      double* ri = Mp + pidx(i, j0);
+      double x[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < jb) {
+          double s = ri[c];
+          for (int t = 0; t < c; ++t) s -= x[t] * Mp[pidx(j0 + c, j0 + t)];
+          x[c] = s * rdiag[j0 + c];
+          ri[c] = x[c];
+        }
+      }
+    }
+    __syncthreads();
+    // (3) trailing tiles K <= I, both > J: tile pairs dealt round-robin to
+    // the warps in row-major order (balanced), (I, K) advanced incrementally
+    const int R = T - J - 1, npairs = R * (R + 1) / 2;
+    const int g = lane >> 2, q = lane & 3;
+    int I = 0, K = warp;
+    while (K > I) { K -= I + 1; ++I; }
+    for (int pq = warp; pq < npairs; pq += nwp) {
+      const int i0 = (J + 1 + I) * 8, ra = i0 + g;
+      const int oa = ra < d ? pidx(ra, 0) : 0;
+      const double a0 = (ra < d && q < jb) ? -Mp[oa + j0 + q] : 0.0;
+      const double a1 = (ra < d && q + 4 < jb) ? -Mp[oa + j0 + 4 + q] : 0.0;
+      const int k0 = (J + 1 + K) * 8, rb = k0 + g;
+      const int ob = rb < d ? pidx(rb, 0) : 0;
+      const double b0 = (rb < d && q < jb) ? Mp[ob + j0 + q] : 0.0;
+      const double b1 = (rb < d && q + 4 < jb) ? Mp[ob + j0 + 4 + q] : 0.0;
+      const int cc = k0 + 2 * q;
+      const bool v0 = ra < d && cc <= ra, v1 = ra < d && cc + 1 <= ra;
+      double c0 = v0 ? Mp[oa + cc] : 0.0, c1 = v1 ? Mp[oa + cc + 1] : 0.0;
+      double d0, d1;
+      dmma8x8x4(d0, d1, a0, b0, c0, c1);
+      dmma8x8x4(d0, d1, a1, b1, d0, d1);
+      if (v0) Mp[oa + cc] = d0;
+      if (v1) Mp[oa + cc + 1] = d1;
+      K += nwp;
+      while (K > I) { K -= I + 1; ++I; }
+    }
+    __syncthreads();
+  }
+  return 1;
+}
+
 // ---------------------------------------------------------------- kernel
 __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -218,8 +324,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   sm.W1 = sm.dT + kk; sm.W2 = sm.W1 + kk; sm.X1 = sm.W2 + kk; sm.X2 = sm.X1 + kk;
   sm.s = sm.X2 + kk; sm.t = sm.s + d; sm.vI = sm.t + d; sm.h = sm.vI + d; sm.g = sm.h + d;
   sm.f1 = sm.g + d; sm.rhs = sm.f1 + d; sm.ds = sm.rhs + d; sm.dt = sm.ds + d; sm.rd = sm.dt + d;
-  sm.tmp = sm.rd + d;
-  sm.red = sm.tmp + d; sm.sc = sm.red + 32;
+  sm.tmp = sm.rd + d; sm.cb0 = sm.tmp + d; sm.cb1 = sm.cb0 + d;
+  sm.red = sm.cb1 + d; sm.sc = sm.red + 32;
   sm.M = sm.sc + 64;
   const bool m_in_smem = d <= SMEM_D;
   double* Mp = m_in_smem ? sm.M : a.gM;
@@ -423,13 +529,20 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       if (d <= CHOL_REG_D) {
         // d <= 66: right-looking with the matrix in REGISTERS (each thread
         // owns <= 5 packed entries), one barrier per column; the column being
-        // eliminated is published to a double-buffered smem vector.
+        // eliminated is published to a double-buffered smem vector.  Entries
+        // are numbered in the reversed packed order (i', c') = (d-1-c, d-1-i),
+        // so the entries still active at column j (c >= j) are exactly the
+        // prefix x < (d-j)(d-j+1)/2: idle threads and slots drop out as the
+        // trailing matrix shrinks.
         constexpr int EPT = 5;
         const int np = d * (d + 1) / 2;
         double val[EPT];
         short ri[EPT], ci[EPT];
-        double* colA = sm.tmp;  // free until the E ds product below
-        double* colB = sm.ds;   // written by the solves afterwards
+        // two columns per barrier: the pre-update columns j and j+1 are
+        // published (A/B buffers, double-buffered), every thread forms the
+        // 2x2 pivot block itself and applies both rank-1 updates
+        double* pA[2] = {sm.tmp, sm.ds};    // column j   (tmp free until E ds, ds until the solves)
+        double* pB[2] = {sm.cb0, sm.cb1};   // column j+1
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
           const int x = tid + u * nth;
@@ -437,115 +550,70 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           ci[u] = 0;
           val[u] = 0.0;
           if (x < np) {
-            int r = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
-            while (r * (r + 1) / 2 > x) --r;
-            while ((r + 1) * (r + 2) / 2 <= x) ++r;
+            int ip = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
+            while (ip * (ip + 1) / 2 > x) --ip;
+            while ((ip + 1) * (ip + 2) / 2 <= x) ++ip;
+            const int cp = x - ip * (ip + 1) / 2;
+            const int r = d - 1 - cp, c = d - 1 - ip;  // r >= c
             ri[u] = (short)r;
-            ci[u] = (short)(x - r * (r + 1) / 2);
-            val[u] = Mp[x];
-            if (ci[u] == 0) colA[r] = val[u];
+            ci[u] = (short)c;
+            val[u] = Mp[pidx(r, c)];
+            if (c == 0) pA[0][r] = val[u];
+            if (c == 1) pB[0][r] = val[u];
           }
         }
         __syncthreads();
-        for (int j = 0; j < d; ++j) {
-          const double* cur = (j & 1) ? colB : colA;
-          double* nxt = (j & 1) ? colA : colB;
-          const double piv = cur[j];
-          if (!(piv > 0.0)) { fail = 1; break; }  // uniform: all threads read the same pivot
-          const double r = rsqrt(piv), r2 = r * r;
+        int buf = 0;
+        for (int j = 0; j < d; j += 2) {
+          const double* ca = pA[buf];
+          const double* cb = pB[buf];
+          double* na = pA[buf ^ 1];
+          double* nb = pB[buf ^ 1];
+          const bool two = j + 1 < d;
+          const double p0 = ca[j];
+          if (!(p0 > 0.0)) { fail = 1; break; }  // uniform
+          const double r0 = rsqrt(p0);
+          double l1 = 0.0, p1 = 1.0, r1 = 0.0;
+          if (two) {
+            l1 = ca[j + 1] * r0;
+            p1 = cb[j + 1] - l1 * l1;
+            if (!(p1 > 0.0)) { fail = 1; break; }
+            r1 = rsqrt(p1);
+          }
+          const int act = (d - j) * (d - j + 1) / 2;  // active entries: x < act
 #pragma unroll
           for (int u = 0; u < EPT; ++u) {
+            if (tid + u * nth >= act) break;
             const int i = ri[u], c = ci[u];
-            if (i < 0 || c < j) continue;
+            const double lij = ca[i] * r0;
             if (c == j) {
-              val[u] = (i == j) ? piv * r : val[u] * r;  // final L entries of column j
+              val[u] = (i == j) ? p0 * r0 : lij;
+            } else if (c == j + 1) {
+              val[u] = (i == j + 1) ? p1 * r1 : (cb[i] - lij * l1) * r1;
             } else {
-              val[u] -= (cur[i] * cur[c]) * r2;
-              if (c == j + 1) nxt[i] = val[u];
+              const double lcj = ca[c] * r0;
+              const double li1 = (cb[i] - lij * l1) * r1, lc1 = (cb[c] - lcj * l1) * r1;
+              val[u] -= lij * lcj + li1 * lc1;
+              if (c == j + 2) na[i] = val[u];
+              if (c == j + 3) nb[i] = val[u];
             }
           }
-          if (tid == 0) rdiag[j] = r;
+          if (tid == 0) {
+            rdiag[j] = r0;
+            if (two) rdiag[j + 1] = r1;
+          }
+          buf ^= 1;
           __syncthreads();
         }
         if (!fail) {
 #pragma unroll
           for (int u = 0; u < EPT; ++u)
-            if (ri[u] >= 0) Mp[tid + u * nth] = val[u];
+            if (ri[u] >= 0) Mp[pidx(ri[u], ci[u])] = val[u];
         }
         __syncthreads();
       } else {
-        constexpr int CB = 16;
-        for (int J = 0; J < d && !fail; J += CB) {
-          const int JB = min(CB, d - J);
-          if (tid < 32) {
-            const int lane = tid;
-            int ok = 1;
-            for (int jj = 0; jj < JB; ++jj) {
-              const int c = J + jj;
-              __syncwarp();
-              const double piv = Mp[pidx(c, c)];
-              if (!(piv > 0.0)) { ok = 0; break; }
-              const double r = rsqrt(piv);
-              __syncwarp();
-              if (lane == 0) { Mp[pidx(c, c)] = piv * r; rdiag[c] = r; }
-              for (int i = c + 1 + lane; i < d; i += 32) Mp[pidx(i, c)] *= r;
-              __syncwarp();
-              const int cmax = J + JB - 1;
-              if (c < cmax)
-                for (int i = c + 1 + lane; i < d; i += 32) {
-                  const int bi = i * (i + 1) / 2;
-                  const double li = Mp[bi + c];
-                  const int cend = min(i, cmax);
-                  for (int c2 = c + 1; c2 <= cend; ++c2) Mp[bi + c2] -= li * Mp[pidx(c2, c)];
-                }
-            }
-            __syncwarp();
-            if (lane == 0) sm.flg[5] = ok;
-          }
-          __syncthreads();
-          if (!sm.flg[5]) { fail = 1; break; }
-          // trailing SYRK: rows/cols >= J + JB
-          const int T0 = J + JB, T = d - T0;
-          if (T > 0) {
-            const int nt = (T + 3) / 4, ntiles = nt * (nt + 1) / 2;
-            for (int x = tid; x < ntiles; x += nth) {
-              int R = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
-              while (R * (R + 1) / 2 > x) --R;
-              while ((R + 1) * (R + 2) / 2 <= x) ++R;
-              const int Cc = x - R * (R + 1) / 2;
-              const int i0 = T0 + 4 * R, c0 = T0 + 4 * Cc;
-              double acc[4][4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-              int bi[4], bc[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int ii = min(i0 + u, d - 1), cc2 = min(c0 + u, d - 1);
-                bi[u] = ii * (ii + 1) / 2 + J;
-                bc[u] = cc2 * (cc2 + 1) / 2 + J;
-              }
-              for (int t = 0; t < JB; ++t) {
-                double li[4], lc[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) { li[u] = Mp[bi[u] + t]; lc[u] = Mp[bc[u] + t]; }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                  for (int v = 0; v < 4; ++v) acc[u][v] = fma(li[u], lc[v], acc[u][v]);
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                  const int ii = i0 + u, cc2 = c0 + v;
-                  if (ii < d && cc2 <= ii) Mp[pidx(ii, cc2)] -= acc[u][v];
-                }
-            }
-          }
-          __syncthreads();
-        }
+        // d > 66: 8-column panels, trailing update on the FP64 tensor cores
+        if (!chol_tiled(Mp, d, rdiag, &sm.flg[5])) fail = 1;
       }
       IPM_MARK(4);
       if (!fail) {
@@ -741,7 +809,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
 
 size_t ipm_smem_bytes(int k) {
   const int d = k * (k + 1) / 2, kk = k * k;
-  size_t doubles = 9 * kk + 11 * d + 32 + 64 + (d <= SMEM_D ? d * (d + 1) / 2 : 0);
+  size_t doubles = 9 * kk + 13 * d + 32 + 64 + (d <= SMEM_D ? d * (d + 1) / 2 : 0);
   return doubles * sizeof(double) + 1200 + 16 * sizeof(int) + 64;
 }
 

@@ -21,11 +21,17 @@ enum WsSlot {
   WS_RED = 21,
   WS_IPM = 30,
   WS_BOOK = 40,
+  WS_BOOK_T = 41,
+  WS_BOOK_W = 42,
+  WS_BOOK_G = 43,
 };
 
 void launch_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y);
 void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int64_t ldv, int k,
                  double* Y, int64_t ldy);
+void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,
+                      double* Y, int64_t ldy);
+void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, double* tval);
 // out (ka x kb, row-major, dev) = A^T B for row-major n x ka A and n x kb B;
 // sym: out = 0.5 (G + G^T) (requires ka == kb)
 void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B,

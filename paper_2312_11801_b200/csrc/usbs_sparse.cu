@@ -661,7 +661,32 @@ void launch_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y) {
 
 void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int64_t ldv, int k,
                  double* Y, int64_t ldy) {
-  const double* val = which ? p->zval : p->cval;
+  launch_spmm_vals(ctx, p, which ? p->zval : p->cval, V, ldv, k, Y, ldy);
+}
+
+// T = A*(w) on the merged pattern: tval[s] = sum_{e in slot s} w[idx[e]] val[e]
+__global__ void k_adjoint_values(int64_t nnz, const int* __restrict__ aptr, const int* __restrict__ aent,
+                                 const int* __restrict__ eidx, const double* __restrict__ eval,
+                                 const double* __restrict__ w, double* __restrict__ tval) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int t = aptr[s]; t < aptr[s + 1]; ++t) {
+      const int e = aent[t];
+      acc += w[eidx[e]] * eval[e];
+    }
+    tval[s] = acc;
+  }
+}
+
+void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, double* tval) {
+  int th = 256, bl = (int)std::min<int64_t>((p->nnz + th - 1) / th, 8 * ctx->num_sms);
+  k_adjoint_values<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->nnz, p->aptr, p->aent, p->e_idx, p->e_val, w, tval);
+  check_launch(ctx);
+}
+
+void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,
+                      double* Y, int64_t ldy) {
   double* partial = nullptr;
   if (p->n_split_items) partial = (double*)ctx->ws.get(WS_SPMM_PARTIAL, (size_t)p->n_split_items * k * sizeof(double));
   const int th = 256;

@@ -127,6 +127,13 @@ def main(which):
             r = subproblem.ipm_quad(q)
         dt = (time.perf_counter() - t0) / 3
         print("ipm d=210", r.value, r.newton_iters, f"{dt * 1e3:.3f} ms/solve (incl. host copies)")
+        if os.environ.get("USBS_IPM_PROF"):
+            out = (C.c_uint64 * 10)()
+            rt.lib.usbs_ipm_profile(rt.h, out, 1)
+            tot = sum(out[:9])
+            nn = 4 * r.newton_iters
+            for nm, v in zip(names, out[:9]):
+                print(f"  {nm:14s} {v / 1e3 / nn:8.2f} us/newton  {100 * v / max(tot, 1):5.1f}%")
     elif which == "spmm":
         p = inst.baseline_config("C4").problem
         dp = DeviceProblem(p)
