@@ -212,6 +212,18 @@ usbs_status usbs_svec(usbs_ctx* ctx, int k, const double* a_dev, double scale, d
 usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* g_dev, double drop_tol,
                          int* perm_dev, double* rinv_dev, double* info_dev);
 
+/* ---- rounding -------------------------------------- */
+/* maxcut_round (rounding.py:34-51): for every column j of the factor U
+ * (n x r, dev, row-major, ld >= r, r <= 64) the cut value of
+ * x = sign(U[:, j]) (zero signs to +1), 0.25 x^T L x = sum_e w_e [x_u != x_v]
+ * over the graph's edges (dev: eu < ev int32, ew double, ne of them) --
+ * exact, hence equal to the reference bit for bit, for integer weights.
+ * Outputs: vals (host, r), *best (host, first maximum, the reference's
+ * strict '>'), x_dev (dev int32, n) = the assignment of the best column. */
+usbs_status usbs_maxcut_round(usbs_ctx* ctx, int64_t n, int64_t ne, const int32_t* eu_dev,
+                              const int32_t* ev_dev, const double* ew_dev, const double* u_dev,
+                              int64_t ldu, int r, double* vals, int* best, int32_t* x_dev);
+
 #ifdef __cplusplus
 }
 #endif

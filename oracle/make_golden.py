@@ -21,6 +21,7 @@ Fixtures:
   sketch.npz         sketch_update / reconstruct outputs
   traj_*.npz         per-iteration solve() trajectories of small problems
   lockstep_c1.npz    C1 state snapshot at t=10 and reference iteration 11
+  rounding.npz       maxcut_round / qap_round (rounding.py) on seeded factors
 """
 from __future__ import annotations
 
@@ -317,11 +318,49 @@ def lockstep():
         n_rel_infeas=nx[9], n_lam_cand=nx[10])
 
 
+def rounding_cases():
+    """maxcut_round (rounding.py:34-51) and qap_round (rounding.py:72-93) of
+    the unmodified reference on seeded factors (with exact zeros, which sign
+    to +1)."""
+    from conftest import random_graph, random_qap
+    from specbundle import rounding as sbr
+    data = {}
+    graphs = {
+        "er": random_graph(300, 0.05, 3),
+        "torus": sbp.GraphInstance.from_edges(
+            400, [(20 * i + j, 20 * ((i + 1) % 20) + j, 1.0 if k % 3 else -1.0)
+                  for k, (i, j) in enumerate((i, j) for i in range(20) for j in range(20))] +
+            [(20 * i + j, 20 * i + (j + 1) % 20, 1.0) for i in range(20) for j in range(20)]),
+    }
+    for name, g in graphs.items():
+        rng = np.random.default_rng(11)
+        u = rng.standard_normal((g.n, 7))
+        u[rng.random(u.shape) < 0.05] = 0.0
+        res = sbr.maxcut_round(u, g)
+        data[f"{name}/eu"], data[f"{name}/ev"], data[f"{name}/ew"] = g.edges_u, g.edges_v, g.edges_w
+        data[f"{name}/u"] = u
+        data[f"{name}/x"] = res.assignment
+        data[f"{name}/value"] = np.array([res.value])
+        data[f"{name}/all"] = np.array([0.25 * float(np.where(u[:, j] >= 0, 1.0, -1.0) @ (
+            g.laplacian() @ np.where(u[:, j] >= 0, 1.0, -1.0))) for j in range(u.shape[1])])
+    for size, seed in ((4, 1), (6, 2)):
+        q = random_qap(size, seed)
+        rng = np.random.default_rng(5 + size)
+        u = rng.standard_normal((size * size + 1, 5))
+        res = sbr.qap_round(u, q)
+        key = f"qap{size}"
+        data[f"{key}/W"], data[f"{key}/D"], data[f"{key}/u"] = q.weights, q.distances, u
+        data[f"{key}/perm"] = res.perm
+        data[f"{key}/objective"] = np.array([res.objective])
+    np.savez_compressed(OUT / "rounding.npz", **data)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    which = sys.argv[1:] or ["builders", "quad", "lanczos", "ipm", "cons", "sketch", "traj", "lockstep"]
+    which = sys.argv[1:] or ["builders", "quad", "lanczos", "ipm", "cons", "sketch", "traj", "lockstep", "rounding"]
     fn = {"builders": builders, "quad": quad_oracle, "lanczos": lanczos_cases, "ipm": ipm_cases,
-          "cons": cons_cases, "sketch": sketch_cases, "traj": trajectories, "lockstep": lockstep}
+          "cons": cons_cases, "sketch": sketch_cases, "traj": trajectories, "lockstep": lockstep,
+          "rounding": rounding_cases}
     for w in which:
         fn[w]()
         print("wrote", w)

@@ -39,6 +39,8 @@ _LAZY = {
     "DeviceProblem": ("runtime", "DeviceProblem"),
     "ipm_quad": ("subproblem", "ipm_quad"),
     "ipm_eval": ("subproblem", "ipm_eval"),
+    "maxcut_round": ("rounding", "maxcut_round"),
+    "qap_round": ("rounding", "qap_round"),
 }
 
 

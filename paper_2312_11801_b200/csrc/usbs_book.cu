@@ -555,6 +555,50 @@ __global__ void __launch_bounds__(256) k_pivchol(int c, const double* __restrict
   }
 }
 
+// ---------------------------------------------------------- cut rounding
+// maxcut_round (rounding.py:34-51): x = sign(U[:, j]) (zero -> +1) and
+// 0.25 x^T L x = sum_e w_e [x_u != x_v] (each undirected edge counted once:
+// x^T L x = sum_e w_e (x_u - x_v)^2).  Exact for integer weights, so the
+// value equals the reference's bit for bit in that case.
+__global__ void k_cut_partial(int64_t ne, const int* __restrict__ eu, const int* __restrict__ ev,
+                              const double* __restrict__ ew, const double* __restrict__ U, int64_t ldu,
+                              double* __restrict__ part) {
+  __shared__ double red[32];
+  const int j = blockIdx.y;
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const bool su = U[(int64_t)eu[e] * ldu + j] >= 0.0, sv = U[(int64_t)ev[e] * ldu + j] >= 0.0;
+    if (su != sv) acc += ew[e];
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) part[(int64_t)j * gridDim.x + blockIdx.x] = acc;
+}
+
+__global__ void k_cut_final(int nb, int r, const double* __restrict__ part, double* __restrict__ vals,
+                            int* __restrict__ best) {
+  __shared__ double v[64];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[(int64_t)j * nb + b];
+    v[j] = s;
+    vals[j] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int bj = 0;
+    for (int j = 1; j < r; ++j)
+      if (v[j] > v[bj]) bj = j;  // first maximum, as the reference's strict '>'
+    best[0] = bj;
+  }
+}
+
+__global__ void k_cut_assign(int64_t n, const double* __restrict__ U, int64_t ldu, const int* __restrict__ best,
+                             int* __restrict__ x) {
+  const int j = best[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = U[i * ldu + j] >= 0.0 ? 1 : -1;
+}
+
 }  // namespace usbs
 
 using namespace usbs;
@@ -734,6 +778,29 @@ usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* G, double drop_tol,
   if (c < 1 || c > 40) fail(USBS_ERR_SHAPE, "pivchol: 1 <= c <= 40");
   k_pivchol<<<1, 256, 0, ctx->stream>>>(c, G, drop_tol, perm, Rinv, info);
   check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_maxcut_round(usbs_ctx* ctx, int64_t n, int64_t ne, const int32_t* eu, const int32_t* ev,
+                              const double* ew, const double* U, int64_t ldu, int r, double* vals, int* best,
+                              int32_t* x) {
+  USBS_API_BEGIN
+  if (n < 1 || r < 1 || r > 64 || ldu < r) fail(USBS_ERR_SHAPE, "factor must be a nonempty n x r matrix, r <= 64");
+  const int nbx = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, (ne + 255) / 256));
+  double* part = (double*)ctx->ws.get(WS_RED + 50, (size_t)nbx * r * sizeof(double) + 64 * sizeof(double) + 64);
+  double* dv = part + (size_t)nbx * r;
+  int* db = (int*)(dv + 64);
+  k_cut_partial<<<dim3(nbx, r), 256, 0, ctx->stream>>>(ne, eu, ev, ew, U, ldu, part);
+  check_launch(ctx);
+  k_cut_final<<<1, 64, 0, ctx->stream>>>(nbx, r, part, dv, db);
+  check_launch(ctx);
+  k_cut_assign<<<nblocks(ctx, n), 256, 0, ctx->stream>>>(n, U, ldu, db, x);
+  check_launch(ctx);
+  USBS_CUDA(cudaMemcpyAsync(ctx->pinned, dv, r * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  USBS_CUDA(cudaMemcpyAsync(ctx->pinned_i, db, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  USBS_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int j = 0; j < r; ++j) vals[j] = ctx->pinned[j];
+  *best = ctx->pinned_i[0];
   USBS_API_END
 }
 

@@ -13,7 +13,9 @@ from .runtime import DeviceProblem, Runtime
 
 
 def _p(t):
-    return C.c_void_p(ptr(t)) if t is not None else None
+    # device tensors only: the raw address goes straight into ctypes (the
+    # c_void_p argtype converts ints in C; no per-argument wrapper objects)
+    return None if t is None else t.data_ptr()
 
 
 class Engine:
