@@ -212,6 +212,12 @@ usbs_status usbs_svec(usbs_ctx* ctx, int k, const double* a_dev, double scale, d
 usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* g_dev, double drop_tol,
                          int* perm_dev, double* rinv_dev, double* info_dev);
 
+/* dst[i] = src[idx[i]] for i < n (dev): the ghost-dual refresh of an
+ * entry-family row shard (the mirrored Z slots of constraints owned by
+ * another rank read these copies; dist.EntryShardPlan). */
+usbs_status usbs_gather(usbs_ctx* ctx, int64_t n, const int64_t* idx_dev, const double* src_dev,
+                        double* dst_dev);
+
 /* ---- rounding -------------------------------------- */
 /* maxcut_round (rounding.py:34-51): for every column j of the factor U
  * (n x r, dev, row-major, ld >= r, r <= 64) the cut value of

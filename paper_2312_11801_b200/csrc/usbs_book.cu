@@ -599,6 +599,12 @@ __global__ void k_cut_assign(int64_t n, const double* __restrict__ U, int64_t ld
     x[i] = U[i * ldu + j] >= 0.0 ? 1 : -1;
 }
 
+__global__ void k_gather(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                         double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
 }  // namespace usbs
 
 using namespace usbs;
@@ -801,6 +807,16 @@ usbs_status usbs_maxcut_round(usbs_ctx* ctx, int64_t n, int64_t ne, const int32_
   USBS_CUDA(cudaStreamSynchronize(ctx->stream));
   for (int j = 0; j < r; ++j) vals[j] = ctx->pinned[j];
   *best = ctx->pinned_i[0];
+  USBS_API_END
+}
+
+usbs_status usbs_gather(usbs_ctx* ctx, int64_t n, const int64_t* idx, const double* src, double* dst) {
+  USBS_API_BEGIN
+  if (n < 0) fail(USBS_ERR_SHAPE, "gather: n < 0");
+  if (n > 0) {
+    k_gather<<<nblocks(ctx, n), 256, 0, ctx->stream>>>(n, idx, src, dst);
+    check_launch(ctx);
+  }
   USBS_API_END
 }
 

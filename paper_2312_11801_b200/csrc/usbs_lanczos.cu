@@ -649,6 +649,22 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
     Qs[(size_t)t * R + i] = a.Q[qidx(r0 + i, t, M1)];
   }
   for (int i = tid; i <= nloc; i += nth) rp[i] = a.rowptr[r0 + i];
+  __syncthreads();
+  // SpMV operand cache (thread-per-row path): the CTA's nonzeros as value +
+  // 16-bit column in the Rayleigh-Ritz scratch (Ys .. ts.Z, 4 m^2 doubles),
+  // which is free between Rayleigh-Ritz calls; reloaded after each restart
+  const int nz0 = rp[0], nnz_loc = rp[nloc] - nz0;
+  const bool use_cache = LG == 1 && a.n <= 65536 && (int64_t)nnz_loc * 10 <= (int64_t)m * m * 32;
+  double* cv = Ys;
+  unsigned short* cc = (unsigned short*)(Ys + nnz_loc);
+  auto load_cache = [&]() {
+    if (!use_cache) return;
+    for (int z = tid; z < nnz_loc; z += nth) {
+      cv[z] = a.val[nz0 + z];
+      cc[z] = (unsigned short)a.col[nz0 + z];
+    }
+  };
+  load_cache();
   cluster.sync();
 
   int cycle = a.cycle0, ell = a.ell0, jstart = a.j0, restarts = a.restarts0, nhist = a.nhist0;
@@ -696,12 +712,23 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
             int c1[U], c2[U];
             double v1[U], v2[U], x1[U], x2[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const bool o1 = z1 + u < e1, o2 = z2 + u < e2;
-              c1[u] = o1 ? a.col[z1 + u] : -1;
-              v1[u] = o1 ? a.val[z1 + u] : 0.0;
-              c2[u] = o2 ? a.col[z2 + u] : -1;
-              v2[u] = o2 ? a.val[z2 + u] : 0.0;
+            if (use_cache) {
+              for (int u = 0; u < U; ++u) {
+                const bool o1 = z1 + u < e1, o2 = z2 + u < e2;
+                c1[u] = o1 ? (int)cc[z1 + u - nz0] : -1;
+                v1[u] = o1 ? cv[z1 + u - nz0] : 0.0;
+                c2[u] = o2 ? (int)cc[z2 + u - nz0] : -1;
+                v2[u] = o2 ? cv[z2 + u - nz0] : 0.0;
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const bool o1 = z1 + u < e1, o2 = z2 + u < e2;
+                c1[u] = o1 ? a.col[z1 + u] : -1;
+                v1[u] = o1 ? a.val[z1 + u] : 0.0;
+                c2[u] = o2 ? a.col[z2 + u] : -1;
+                v2[u] = o2 ? a.val[z2 + u] : 0.0;
+              }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -910,6 +937,8 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
       for (int u = 0; u < ell; ++u) Qs[(size_t)u * R + il] = qrow_dot(qrow, u);
       Qs[(size_t)ell * R + il] = Qs[(size_t)m * R + il];
     }
+    __syncthreads();  // Ys (the restart's Y) is read; the operand cache may return
+    load_cache();
     ++restarts;
     jstart = ell;
     from_q = true;

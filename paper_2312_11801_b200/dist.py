@@ -4,14 +4,20 @@ GPU p owns a contiguous row block [r_p, r_{p+1}) of Z = C - A*(y) (balanced
 on nnz + rows, for power-law degree sequences), of the basis V, of the
 Lanczos basis Q, of F, Psi and P, and -- for diagonal constraints (MaxCut,
 the sharded configs C4) -- of the m = n constraint vectors (y, nu, A Xbar,
-a_x, b).  Everything k x k / d x d (Grams, IPM, Rayleigh-Ritz) is computed
+a_x, b).  Entry-family constraints (C5) are owned by the owner of their
+smallest row (EntryShardPlan): the owner keeps y_i, nu_i, b_i and the image;
+a constraint that also touches another rank's rows is a ghost there, whose
+mirrored Z slot reads a copy of y_i refreshed at every assembly; images and
+compressed rows of the owned constraints read an allgathered V.
+Everything k x k / d x d (Grams, IPM, Rayleigh-Ritz) is computed
 redundantly on every rank from allreduced inputs, so all ranks take the same
 branches.  Collectives (torch.distributed: NCCL on GPUs, gloo in the CPU
 tests):
   * per SpMV (each Lanczos step, each SpMM): allgather of the input block;
   * per Lanczos step: allreduce of Q^T w twice (<= 33 doubles) and ||w||^2;
   * per outer iteration: allreduce of the k x k / d x d Grams, d-vectors and
-    residual scalars.
+    residual scalars; for entry families an allgather of the owned duals per
+    assembly and of V per image / compressed-row evaluation.
 Reductions run in a fixed order for a fixed communicator, so runs are
 reproducible; parity with the single-GPU path is to rounding, not bitwise.
 """
@@ -110,14 +116,82 @@ class Comm:
         return out
 
 
+def _allgather_var(comm, local, counts, out):
+    """out = concatenation of every rank's local vector (lengths counts)."""
+    if comm.world == 1:
+        out.copy_(local)
+        return out
+    import torch
+    d = comm._dist()
+    mx = int(max(counts))
+    buf = torch.zeros(max(mx, 1), dtype=local.dtype, device=local.device)
+    buf[: local.numel()].copy_(local.reshape(-1))
+    parts = [torch.empty_like(buf) for _ in range(comm.world)]
+    d.all_gather(parts, buf, group=comm.group)
+    off = 0
+    for q in range(comm.world):
+        out[off: off + counts[q]].copy_(parts[q][: counts[q]])
+        off += counts[q]
+    return out
+
+
+class EntryShardPlan:
+    """Constraint ownership for an entry-family problem (C5) on `shard`.
+
+    owner(i) = the rank holding row min_e rows[e] over constraint i's entries
+    (rows <= cols).  ext = [owned | ghost] indexes the rank's dual copy: the
+    directed entries of the local rows (both mirrored halves of an
+    off-diagonal entry land on the rows' owners) refer to it, and the ghost
+    values are gathered from the concatenation of all ranks' owned duals
+    (rank order) at every assembly."""
+
+    def __init__(self, prob, shard: Shard):
+        cons = prob.constraints
+        idx, rows, cols, vals = (np.asarray(cons.idx, np.int64), np.asarray(cons.rows, np.int64),
+                                 np.asarray(cons.cols, np.int64), np.asarray(cons.vals, float))
+        m = int(prob.m)
+        minrow = np.full(m, np.iinfo(np.int64).max, dtype=np.int64)
+        np.minimum.at(minrow, idx, rows)
+        if np.any(minrow == np.iinfo(np.int64).max):
+            raise ValueError("every constraint needs at least one entry")
+        owner = np.searchsorted(shard.bounds, minrow, side="right") - 1
+        self.counts = np.bincount(owner, minlength=shard.world).astype(np.int64)
+        offsets = np.concatenate([[0], np.cumsum(self.counts)])
+        order = np.argsort(owner, kind="stable")  # concatenated owned lists, rank order
+        pos = np.empty(m, dtype=np.int64)
+        pos[order] = np.arange(m)
+        self.owned = np.flatnonzero(owner == shard.rank)
+        r0, r1 = shard.r0, shard.r1
+        lr = (rows >= r0) & (rows < r1)
+        lc = (cols >= r0) & (cols < r1) & (rows != cols)
+        d_row = np.concatenate([rows[lr] - r0, cols[lc] - r0])
+        d_col = np.concatenate([cols[lr], rows[lc]])
+        d_con = np.concatenate([idx[lr], idx[lc]])
+        d_val = np.concatenate([vals[lr], vals[lc]])
+        touched = np.unique(d_con)
+        self.ghost = np.setdiff1d(touched, self.owned, assume_unique=True)
+        ext = np.concatenate([self.owned, self.ghost])
+        ext_of = np.full(m, -1, dtype=np.int64)
+        ext_of[ext] = np.arange(ext.size)
+        self.m_own, self.m_ext = int(self.owned.size), int(ext.size)
+        self.d_rows, self.d_cols, self.d_idx, self.d_vals = d_row, d_col, ext_of[d_con], d_val
+        self.ghost_pos = pos[self.ghost]  # where each ghost sits in the concatenated owned duals
+        own_of = np.full(m, -1, dtype=np.int64)
+        own_of[self.owned] = np.arange(self.owned.size)
+        sel = own_of[idx] >= 0
+        self.o_idx, self.o_rows, self.o_cols, self.o_vals = own_of[idx[sel]], rows[sel], cols[sel], vals[sel]
+        self.b = np.asarray(prob.b, dtype=float)[self.owned]
+        self.ineq = np.asarray(prob.ineq_mask, dtype=bool)[self.owned]
+        self.m_total = m
+
+
 def shard_maxcut(prob, shard: Shard):
     """Local arrays of a diagonal-constraint problem (MaxCut) for one rank:
     CSR rows [r0, r1) of C with global columns, the directed diagonal
     entries (i, i, r0 + i, 1.0), b and the inequality mask slices."""
     cons = prob.constraints
     if hasattr(cons, "idx"):
-        raise NotImplementedError("row sharding currently covers diagonal constraints (MaxCut, C4); "
-                                  "entry-family sharding (C5) is listed in DESIGN.md as next")
+        raise ValueError("entry-family problems shard through EntryShardPlan")
     c = prob.cost.tocsr()
     r0, r1 = shard.r0, shard.r1
     loc = c[r0:r1]
@@ -134,7 +208,9 @@ def shard_maxcut(prob, shard: Shard):
 class ShardedDeviceProblem:
     """The rank's row block of an SdpProblem on its GPU (C-ABI shard problem:
     local rows, global columns).  Same methods as runtime.DeviceProblem; the
-    operator apply gathers the input block from all ranks first."""
+    operator apply gathers the input block from all ranks first.  Entry
+    families also get an image problem: the rank's owned constraints over the
+    full n, evaluated on the allgathered basis (`image_operands`)."""
 
     def __init__(self, prob, shard: Shard, comm: Comm, rt=None):
         import ctypes as C
@@ -144,39 +220,111 @@ class ShardedDeviceProblem:
 
         self.rt = rt or runtime()
         self.prob, self.shard, self.comm = prob, shard, comm
-        a = shard_maxcut(prob, shard)
         self.n = shard.rows
-        self.m = shard.rows
         self.n_global = shard.n
-        h = C.c_void_p()
-        check(self.rt.lib.usbs_problem_create_shard(
-            self.rt.h, self.n, shard.n, self.m, C.c_void_p(a["indptr"].ctypes.data),
-            C.c_void_p(a["indices"].ctypes.data), C.c_void_p(a["data"].ctypes.data), self.n,
-            C.c_void_p(a["e_idx"].ctypes.data), C.c_void_p(a["e_rows"].ctypes.data),
-            C.c_void_p(a["e_cols"].ctypes.data), C.c_void_p(a["e_vals"].ctypes.data), 1, C.byref(h)),
-            "problem_create_shard")
-        self.h = h
-        self.diag_only = True
-        self.b = self.rt.upload(a["b"])
-        self.ineq_mask = a["ineq"]
+        self.entries = hasattr(prob.constraints, "idx")
+        self.h_img = None
+        lib = self.rt.lib
+        if not self.entries:
+            a = shard_maxcut(prob, shard)
+            self.m = shard.rows
+            h = C.c_void_p()
+            check(lib.usbs_problem_create_shard(
+                self.rt.h, self.n, shard.n, self.m, C.c_void_p(a["indptr"].ctypes.data),
+                C.c_void_p(a["indices"].ctypes.data), C.c_void_p(a["data"].ctypes.data), self.n,
+                C.c_void_p(a["e_idx"].ctypes.data), C.c_void_p(a["e_rows"].ctypes.data),
+                C.c_void_p(a["e_cols"].ctypes.data), C.c_void_p(a["e_vals"].ctypes.data), 1, C.byref(h)),
+                "problem_create_shard")
+            self.h = h
+            self.diag_only = True
+            b, ineq = a["b"], a["ineq"]
+        else:
+            plan = EntryShardPlan(prob, shard)
+            self.plan = plan
+            self.m = plan.m_own
+            c = prob.cost.tocsr()[shard.r0:shard.r1]
+            ip = np.ascontiguousarray(c.indptr, dtype=np.int64)
+            ix = np.ascontiguousarray(c.indices, dtype=np.int32)
+            dt = np.ascontiguousarray(c.data, dtype=np.float64)
+            e = [np.ascontiguousarray(x, dtype=np.int64) for x in (plan.d_idx, plan.d_rows, plan.d_cols)]
+            ev = np.ascontiguousarray(plan.d_vals, dtype=np.float64)
+            h = C.c_void_p()
+            check(lib.usbs_problem_create_shard(
+                self.rt.h, self.n, shard.n, max(plan.m_ext, 1), C.c_void_p(ip.ctypes.data), C.c_void_p(ix.ctypes.data),
+                C.c_void_p(dt.ctypes.data), int(ev.size), C.c_void_p(e[0].ctypes.data), C.c_void_p(e[1].ctypes.data),
+                C.c_void_p(e[2].ctypes.data), C.c_void_p(ev.ctypes.data), 0, C.byref(h)), "problem_create_shard")
+            self.h = h
+            # the owned constraints over the full n (no cost entries)
+            z_ip = np.zeros(shard.n + 1, dtype=np.int64)
+            z_ix = np.zeros(1, dtype=np.int32)
+            z_dt = np.zeros(1, dtype=np.float64)
+            o = [np.ascontiguousarray(x, dtype=np.int64) for x in (plan.o_idx, plan.o_rows, plan.o_cols)]
+            ov = np.ascontiguousarray(plan.o_vals, dtype=np.float64)
+            hi = C.c_void_p()
+            check(lib.usbs_problem_create(
+                self.rt.h, shard.n, max(plan.m_own, 1), C.c_void_p(z_ip.ctypes.data), C.c_void_p(z_ix.ctypes.data),
+                C.c_void_p(z_dt.ctypes.data), int(ov.size), C.c_void_p(o[0].ctypes.data),
+                C.c_void_p(o[1].ctypes.data), C.c_void_p(o[2].ctypes.data), C.c_void_p(ov.ctypes.data), 0,
+                C.byref(hi)), "problem_create(image)")
+            self.h_img = hi
+            self.diag_only = False
+            torch = self.rt.torch
+            self.y_ext = self.rt.zeros(max(plan.m_ext, 1))
+            self.y_cat = self.rt.zeros(max(plan.m_total, 1))
+            self.ghost_pos = torch.as_tensor(plan.ghost_pos, dtype=torch.int64, device=self.rt.device)
+            b, ineq = plan.b, plan.ineq
+        self.b = self.rt.upload(b)
+        self.ineq_mask = ineq
         self.has_ineq = bool(np.asarray(prob.ineq_mask, dtype=bool).any())
-        self.ineq = self.rt.upload(a["ineq"].astype(np.float64))
+        self.ineq = self.rt.upload(ineq.astype(np.float64))
         self.alpha = float(prob.alpha)
         self._xfull = {}
 
     def __del__(self):
         try:
-            if getattr(self, "h", None) is not None:
-                self.rt.lib.usbs_problem_destroy(self.h)
-                self.h = None
+            for nm in ("h", "h_img"):
+                if getattr(self, nm, None) is not None:
+                    self.rt.lib.usbs_problem_destroy(getattr(self, nm))
+                    setattr(self, nm, None)
         except Exception:
             pass
 
     def assemble(self, y_dev):
+        """Z = C - A*(y) on the local rows; y_dev are the rank's owned duals
+        (entry families: the ghost copies are refreshed first)."""
         import ctypes as C
 
         from ._native import check, ptr
-        check(self.rt.lib.usbs_slack_assemble(self.rt.h, self.h, C.c_void_p(ptr(y_dev))), "slack_assemble")
+        y_use = y_dev
+        if self.entries:
+            plan = self.plan
+            _allgather_var(self.comm, y_dev, plan.counts, self.y_cat)
+            self.y_ext[: plan.m_own].copy_(y_dev)
+            ng = int(plan.ghost.size)
+            if ng:
+                check(self.rt.lib.usbs_gather(self.rt.h, ng, C.c_void_p(self.ghost_pos.data_ptr()),
+                                              C.c_void_p(ptr(self.y_cat)),
+                                              C.c_void_p(ptr(self.y_ext) + 8 * plan.m_own)), "gather")
+            y_use = self.y_ext
+        check(self.rt.lib.usbs_slack_assemble(self.rt.h, self.h, C.c_void_p(ptr(y_use))), "slack_assemble")
+
+    def full_rows(self, V):
+        """The allgathered n x k basis (cached buffer per k)."""
+        k = V.shape[1]
+        xfull = self._xfull.get(("img", k))
+        if xfull is None:
+            xfull = self.rt.empty(self.n_global, k)
+            self._xfull[("img", k)] = xfull
+        self.comm.allgather_rows(V.contiguous() if V.stride(1) != 1 else V, xfull, self.shard)
+        return xfull
+
+    def image_operands(self, V):
+        """(problem handle, basis) for the constraint kernels: the owned
+        constraints over the full n and the allgathered V (entry families),
+        or the shard itself and the local V (diagonal constraints)."""
+        if not self.entries:
+            return self.h, V
+        return self.h_img, self.full_rows(V)
 
     def apply(self, which, V, out=None, gram=None, xfull=None):
         import ctypes as C

@@ -98,15 +98,21 @@ class Engine:
             return self.dp.apply(which, V, out=out, gram=gram, h=self.h)
         return self.dp.apply(which, V, out=out, gram=gram)
 
+    def _cons_operands(self, V):
+        f = getattr(self.dp, "image_operands", None)
+        return f(V) if f is not None else (self.dp.h, V)
+
     def image(self, V, S, out, s_is_diag=False, s_scale=1.0, beta=0.0, beta_dev=None, base=None):
-        check(self.lib.usbs_cons_image(self.h, self.dp.h, _p(V), V.stride(0), V.shape[1], _p(S),
+        hp, V = self._cons_operands(V)
+        check(self.lib.usbs_cons_image(self.h, hp, _p(V), V.stride(0), V.shape[1], _p(S),
                                        1 if s_is_diag else 0, float(s_scale), _p(beta_dev), float(beta), _p(base),
                                        _p(out)), "cons_image")
         return out
 
     def compressed(self, V, scale_gram=0.0, gram_out=None, a=None, scale_a=0.0, a_out=None, w=None, scale_w=0.0,
                    w_out=None):
-        check(self.lib.usbs_cons_compressed(self.h, self.dp.h, _p(V), V.stride(0), V.shape[1], float(scale_gram),
+        hp, V = self._cons_operands(V)
+        check(self.lib.usbs_cons_compressed(self.h, hp, _p(V), V.stride(0), V.shape[1], float(scale_gram),
                                             _p(gram_out), _p(a), float(scale_a), _p(a_out), _p(w), float(scale_w),
                                             _p(w_out)), "cons_compressed")
         if self.comm is not None:

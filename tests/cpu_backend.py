@@ -17,7 +17,8 @@ import torch
 
 from oracle import usbs_cpu as O
 from paper_2312_11801_b200 import _native as N
-from paper_2312_11801_b200.dist import Comm, Shard, shard_maxcut
+from paper_2312_11801_b200 import instances as inst
+from paper_2312_11801_b200.dist import Comm, EntryShardPlan, Shard, _allgather_var, shard_maxcut
 
 
 class CpuRuntime:
@@ -48,22 +49,46 @@ class CpuRuntime:
 class CpuShardProblem:
     def __init__(self, prob, shard: Shard, comm: Comm, rt: CpuRuntime):
         self.rt, self.prob, self.shard, self.comm = rt, prob, shard, comm
-        a = shard_maxcut(prob, shard)
-        self.n = self.m = shard.rows
+        self.n = shard.rows
         self.n_global = shard.n
-        self.C = sp.csr_matrix((a["data"], a["indices"], a["indptr"]), shape=(self.n, shard.n))
+        self.entries = hasattr(prob.constraints, "idx")
+        c = prob.cost.tocsr()[shard.r0:shard.r1]
+        self.C = sp.csr_matrix((c.data, c.indices, c.indptr), shape=(self.n, shard.n))
         self.Z = self.C.copy()
-        self.b = rt.upload(a["b"])
-        self.ineq_mask = a["ineq"]
+        if self.entries:
+            self.plan = pl = EntryShardPlan(prob, shard)
+            self.m = pl.m_own
+            b, ineq = pl.b, pl.ineq
+            self.owned_family = inst.EntryFamilies(shard.n, max(pl.m_own, 1), pl.o_idx, pl.o_rows, pl.o_cols,
+                                                   pl.o_vals)
+        else:
+            a = shard_maxcut(prob, shard)
+            self.m = shard.rows
+            b, ineq = a["b"], a["ineq"]
+        self.b = rt.upload(b)
+        self.ineq_mask = ineq
         self.has_ineq = bool(np.asarray(prob.ineq_mask).any())
-        self.ineq = rt.upload(a["ineq"].astype(float))
+        self.ineq = rt.upload(ineq.astype(float))
         self.alpha = float(prob.alpha)
-        self.diag_only = True
+        self.diag_only = not self.entries
 
     def assemble(self, y):
-        d = sp.csr_matrix((y.numpy().copy(), (np.arange(self.n), self.shard.r0 + np.arange(self.n))),
-                          shape=(self.n, self.shard.n))
+        if not self.entries:
+            d = sp.csr_matrix((y.numpy().copy(), (np.arange(self.n), self.shard.r0 + np.arange(self.n))),
+                              shape=(self.n, self.shard.n))
+        else:
+            pl = self.plan
+            cat = torch.zeros(pl.m_total, dtype=torch.float64)
+            _allgather_var(self.comm, y, pl.counts, cat)
+            y_ext = np.concatenate([y.numpy(), cat.numpy()[pl.ghost_pos]])
+            d = sp.coo_matrix((y_ext[pl.d_idx] * pl.d_vals, (pl.d_rows, pl.d_cols)),
+                              shape=(self.n, self.shard.n)).tocsr()
         self.Z = (self.C - d).tocsr()
+
+    def full_rows(self, V):
+        full = torch.empty(self.shard.n, V.shape[1], dtype=torch.float64)
+        self.comm.allgather_rows(V, full, self.shard)
+        return full
 
     def apply(self, which, V, out=None, gram=None, xfull=None):
         if V.dim() == 1:
@@ -212,10 +237,19 @@ class CpuEngine:
         return self.dp.apply(which, V, out=out, gram=gram)
 
     def image(self, V, S, out, s_is_diag=False, s_scale=1.0, beta=0.0, beta_dev=None, base=None):
-        v = V.numpy()
-        if s_is_diag:
+        if self.dp.entries:  # owned constraints on the allgathered basis
+            v, fam = self.dp.full_rows(V).numpy(), self.dp.owned_family
+            k = v.shape[1]
+            if s_is_diag:
+                img = O.image_factor(fam, v, s_scale * S.numpy().reshape(-1)[:k])
+            else:
+                img = O.image_lowrank(fam, v, s_scale * S.numpy())
+            img = img[: self.m]
+        elif s_is_diag:
+            v = V.numpy()
             img = (v * v) @ (s_scale * S.numpy().reshape(-1)[: v.shape[1]])
         else:
+            v = V.numpy()
             img = np.einsum("ij,jk,ik->i", v, s_scale * S.numpy(), v)
         bt = beta * (float(beta_dev[0]) if beta_dev is not None else 1.0)
         res = img + (bt * base.numpy() if base is not None else 0.0)
@@ -224,7 +258,10 @@ class CpuEngine:
 
     def compressed(self, V, scale_gram=0.0, gram_out=None, a=None, scale_a=0.0, a_out=None, w=None, scale_w=0.0,
                    w_out=None):
-        cm = O.compressed(object(), V.numpy())  # diagonal family: rows svec(v_i v_i^T)
+        if self.dp.entries:  # rows of the owned constraints, allgathered basis
+            cm = O.compressed(self.dp.owned_family, self.dp.full_rows(V).numpy())[: self.m]
+        else:
+            cm = O.compressed(object(), V.numpy())  # diagonal family: rows svec(v_i v_i^T)
         if gram_out is not None:
             gram_out.copy_(torch.from_numpy(scale_gram * cm.T @ cm))
             self._ar(gram_out)

@@ -29,8 +29,17 @@ def _free_port():
     return port
 
 
-def _problem():
+def _problem(kind="maxcut"):
+    if kind == "entries":  # correlation SDP: diag equalities + edge inequalities (C5 family)
+        return inst.correlation_problem(*inst.knn_correlation(n=90, clusters=6, dim=8, knn=5, seed=4))
     return inst.maxcut_problem(random_graph(120, 0.08, 3))
+
+
+def _minrow(p):
+    c = p.constraints
+    mr = np.full(p.m, np.iinfo(np.int64).max, dtype=np.int64)
+    np.minimum.at(mr, np.asarray(c.idx), np.asarray(c.rows))
+    return mr
 
 
 def _worker(rank, world, port, outdir, what):
@@ -44,7 +53,7 @@ def _worker(rank, world, port, outdir, what):
         from paper_2312_11801_b200.dist import Comm, Shard, lanczos_sharded
         from paper_2312_11801_b200.solver import DeviceSolver, SolverConfig
 
-        p = _problem()
+        p = _problem("entries" if what == "solve_entries" else "maxcut")
         shard = Shard.balanced(p.cost.indptr, world, rank)
         comm = Comm(world)
         rt = CpuRuntime()
@@ -63,8 +72,17 @@ def _worker(rank, world, port, outdir, what):
             ds = DeviceSolver(p, cfg, dprob=dp, comm=comm, engine=eng)
             rec = []
             st, out = ds.solve(callback=rec.append)
-            yfull = torch.empty(p.n, 1, dtype=torch.float64)
-            comm.allgather_rows(st.y_dev.view(-1, 1), yfull, shard)
+            if what == "solve_entries":  # owned duals back to global constraint order
+                from paper_2312_11801_b200.dist import _allgather_var
+                cat = torch.zeros(p.m, dtype=torch.float64)
+                _allgather_var(comm, st.y_dev, dp.plan.counts, cat)
+                order = np.argsort(np.searchsorted(shard.bounds, _minrow(p), side="right") - 1, kind="stable")
+                yg = np.empty(p.m)
+                yg[order] = cat.numpy()
+                yfull = torch.from_numpy(yg).view(-1, 1)
+            else:
+                yfull = torch.empty(p.n, 1, dtype=torch.float64)
+                comm.allgather_rows(st.y_dev.view(-1, 1), yfull, shard)
             np.savez(os.path.join(outdir, f"r{rank}.npz"), f_y=np.array([r.f_y for r in rec]),
                      f_cand=np.array([r.f_cand for r in rec]), model_val=np.array([r.model_val for r in rec]),
                      steps=np.array([r.step == "descent" for r in rec]), y=yfull.numpy().ravel(), lams=out.lams,
@@ -115,4 +133,41 @@ def test_sharded_solve_gloo_world2():
         assert len(r["f_y"]) == len(f_y)
         np.testing.assert_allclose(r["f_y"][-1], f_y[-1], rtol=1e-3)
     np.testing.assert_array_equal(res[0]["f_y"], res[1]["f_y"])  # every rank took the same decisions
+    np.testing.assert_array_equal(res[0]["y"], res[1]["y"])
+
+
+def test_entry_shard_plan_covers_every_entry():
+    """Every entry lands on the owners of its rows exactly once per half, the
+    owned sets partition the constraints, ghosts point at their owners."""
+    from paper_2312_11801_b200.dist import EntryShardPlan, Shard
+    p = _problem("entries")
+    c = p.constraints
+    world = 3
+    plans = [EntryShardPlan(p, Shard.balanced(p.cost.indptr, world, r)) for r in range(world)]
+    owned = np.concatenate([pl.owned for pl in plans])
+    assert np.array_equal(np.sort(owned), np.arange(p.m))
+    halves = sum(pl.d_vals.size for pl in plans)
+    assert halves == c.vals.size + int(np.sum(np.asarray(c.rows) != np.asarray(c.cols)))
+    cat = np.concatenate([pl.owned for pl in plans])
+    for pl in plans:
+        np.testing.assert_array_equal(cat[pl.ghost_pos], pl.ghost)
+        assert pl.o_vals.size == int(np.isin(np.asarray(c.idx), pl.owned).sum())
+
+
+def test_sharded_entry_solve_gloo_world2():
+    """C5-family (entry constraints with inequalities) row-sharded over two
+    gloo ranks: the first iterations match the single-process oracle, all
+    decisions identical, both ranks bit-identical."""
+    res = _run("solve_entries")
+    p = _problem("entries")
+    rec = []
+    ost, oout = O.solve(p, O.Config(sketch_rank=5, max_iters=8, seed=0), callback=rec.append)
+    f_y = np.array([r.f_y for r in rec])
+    for r in res:
+        np.testing.assert_allclose(r["f_y"][:4], f_y[:4], rtol=1e-8)
+        np.testing.assert_array_equal(r["steps"], [x.step == "descent" for x in rec])
+        assert len(r["f_y"]) == len(f_y)
+        np.testing.assert_allclose(r["f_y"][-1], f_y[-1], rtol=1e-6)
+        np.testing.assert_allclose(r["y"], ost.y, rtol=1e-5, atol=1e-8 * np.abs(ost.y).max())
+    np.testing.assert_array_equal(res[0]["f_y"], res[1]["f_y"])
     np.testing.assert_array_equal(res[0]["y"], res[1]["y"])
