@@ -57,6 +57,19 @@ def main(name="C2", iters=30, skip=10):
     if cur_e is not None:
         busy += cur_e - cur_s
     print(f"{iters} iterations: wall {wall * 1e3 / iters:.3f} ms/it, GPU busy (union) {busy / 1e3 / iters:.3f} ms/it")
+    # idle gaps between consecutive kernels (main + aux streams merged),
+    # attributed to the (previous -> next) kernel pair
+    evs = sorted(((e.time_range.start, e.time_range.end, e.name.split("(")[0]) for e in ev), key=lambda x: x[0])
+    gaps, last_end, last_name = {}, None, None
+    for st_, en_, nm in evs:
+        if last_end is not None and st_ > last_end:
+            key = (last_name[-28:], nm[-28:])
+            gaps[key] = gaps.get(key, 0.0) + (st_ - last_end)
+        if last_end is None or en_ > last_end:
+            last_end, last_name = en_, nm
+    print("  largest idle gaps (us/it): previous kernel -> next kernel")
+    for (a_, b_), g in sorted(gaps.items(), key=lambda x: -x[1])[:12]:
+        print(f"    {g / iters:8.1f}  {a_:>28s} -> {b_}")
     for nm, t in sorted(tot.items(), key=lambda x: -x[1])[:20]:
         print(f"  {t / 1e3 / iters:8.3f} ms/it  {nm}")
 

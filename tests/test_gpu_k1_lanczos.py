@@ -271,3 +271,55 @@ def test_small_eigh_matches_lapack(k):
     np.testing.assert_allclose(vals, lv, atol=1e-13 * max(1, np.abs(lv).max()))
     np.testing.assert_allclose(vecs @ np.diag(vals) @ vecs.T, 0.5 * (a + a.T), atol=1e-12 * np.abs(a).max())
     np.testing.assert_allclose(vecs.T @ vecs, np.eye(k), atol=1e-13)
+
+
+def _star_problem(n=6000, hubs=(0, 2500), seed=9):
+    """Graph with hub rows far above the SpMV tile (1024) and the grid-Lanczos
+    segment (4096) sizes plus a random sparse rest: exercises the block-per-row
+    paths of the fused SpMV and of the grid kernel's segments."""
+    rng = np.random.default_rng(seed)
+    eu, ev = [], []
+    for h in hubs:
+        leaves = rng.choice(n, size=4500, replace=False)
+        leaves = leaves[leaves != h]
+        eu += [h] * leaves.size
+        ev += list(leaves)
+    m = 20000
+    a, b = rng.integers(0, n, m), rng.integers(0, n, m)
+    eu += list(a)
+    ev += list(b)
+    g = inst.Graph.from_arrays(n, np.array(eu), np.array(ev), rng.choice([-1.0, 1.0], len(eu)))
+    return inst.maxcut_problem(g)
+
+
+@pytest.mark.parametrize("k", [1, 3, 11])
+def test_op_apply_hub_rows(k):
+    eigen, runtime = dev()
+    p = _star_problem()
+    assert np.diff(p.cost.indptr).max() > 4096
+    rng = np.random.default_rng(2)
+    y = rng.standard_normal(p.m) * 1e-3
+    v, _ = np.linalg.qr(rng.standard_normal((p.n, k)))
+    dp = runtime.DeviceProblem(p)
+    dp.assemble(dp.rt.upload(y))
+    out = dp.rt.download(dp.apply(1, dp.rt.upload(v)))
+    z = (p.cost - O.adjoint_csr(p.constraints, y, p.n)).tocsr()
+    bound_check(out, z @ v, abs(z), np.abs(v), np.diff(z.indptr))
+
+
+@pytest.mark.parametrize("cluster", [True, False])
+def test_lanczos_hub_rows(cluster, monkeypatch):
+    """Grid kernel (hub rows above one segment, split across the nonzero
+    partition) and cluster kernel against the oracle."""
+    eigen, runtime = dev()
+    if not cluster:
+        monkeypatch.setenv("USBS_LZ_CLUSTER", "0")
+    p = _star_problem()
+    y = np.random.default_rng(4).standard_normal(p.m) * 1e-3
+    dp = runtime.DeviceProblem(p)
+    assert (dp.lanczos_plan(32)[0] > 0) == cluster
+    r = eigen.lanczos_top(eigen.dual_slack_operator(dp, y), 8, seed=0)
+    ro = O.lanczos(O.slack_op(p, y), 8, seed=0)
+    assert abs(r.eigenvalues[0] - ro.eigenvalues[0]) <= 1e-10 * abs(ro.eigenvalues[0])
+    assert r.restarts == ro.restarts and r.matvecs == ro.matvecs
+    np.testing.assert_allclose(r.eigenvalues, ro.eigenvalues, rtol=1e-7, atol=1e-10)
