@@ -211,6 +211,11 @@ usbs_status usbs_svec(usbs_ctx* ctx, int k, const double* a_dev, double scale, d
  * info (dev, 3) = [rank, min selected residual ratio, max column norm]. */
 usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* g_dev, double drop_tol,
                          int* perm_dev, double* rinv_dev, double* info_dev);
+/* B (c x c, dev) with B[perm[i], j] = Rinv[i, j] for i, j < r = info[0] and
+ * zero elsewhere: orthonormalize's first CholQR factor built on the device
+ * from usbs_pivchol's outputs, so the host reads the rank only once. */
+usbs_status usbs_perm_rows(usbs_ctx* ctx, int c, const int32_t* perm_dev, const double* rinv_dev,
+                           const double* info_dev, double* out_dev);
 
 /* dst[i] = src[idx[i]] for i < n (dev): the ghost-dual refresh of an
  * entry-family row shard (the mirrored Z slots of constraints owned by

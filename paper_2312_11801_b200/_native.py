@@ -64,6 +64,7 @@ PROTOS = {
     "usbs_pivchol": (_i32, [_p, _i32, _p, C.c_double, _p, _p, _p]),
     "usbs_svec": (_i32, [_p, _i32, _p, C.c_double, _p]),
     "usbs_gather": (_i32, [_p, _i64, _p, _p, _p]),
+    "usbs_perm_rows": (_i32, [_p, _i32, _p, _p, _p, _p]),
     "usbs_maxcut_round": (_i32, [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i32, _pd, _pi, _p]),
 }
 

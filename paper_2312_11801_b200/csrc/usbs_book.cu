@@ -605,6 +605,19 @@ __global__ void k_gather(int64_t n, const int64_t* __restrict__ idx, const doubl
     dst[i] = src[idx[i]];
 }
 
+// orthonormalize's first CholQR factor: B[perm[i], j] = Rinv[i, j] for
+// i, j < r (r = info[0], the pivoted Cholesky rank), zero elsewhere
+__global__ void k_perm_rows(int c, const int* __restrict__ perm, const double* __restrict__ rinv,
+                            const double* __restrict__ info, double* __restrict__ out) {
+  const int r = (int)info[0];
+  for (int x = threadIdx.x; x < c * c; x += blockDim.x) out[x] = 0.0;
+  __syncthreads();
+  for (int x = threadIdx.x; x < c * c; x += blockDim.x) {
+    const int i = x / c, j = x % c;
+    if (i < r && j < r) out[perm[i] * c + j] = rinv[i * c + j];
+  }
+}
+
 }  // namespace usbs
 
 using namespace usbs;
@@ -817,6 +830,15 @@ usbs_status usbs_gather(usbs_ctx* ctx, int64_t n, const int64_t* idx, const doub
     k_gather<<<nblocks(ctx, n), 256, 0, ctx->stream>>>(n, idx, src, dst);
     check_launch(ctx);
   }
+  USBS_API_END
+}
+
+usbs_status usbs_perm_rows(usbs_ctx* ctx, int c, const int32_t* perm, const double* rinv, const double* info,
+                           double* out) {
+  USBS_API_BEGIN
+  if (c < 1 || c > 64) fail(USBS_ERR_SHAPE, "perm_rows: 1 <= c <= 64");
+  k_perm_rows<<<1, 256, 0, ctx->stream>>>(c, perm, rinv, info, out);
+  check_launch(ctx);
   USBS_API_END
 }
 

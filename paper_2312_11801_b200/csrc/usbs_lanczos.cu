@@ -1320,6 +1320,7 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
     return USBS_OK;
   }
   if (m > 64) fail(USBS_ERR_CONFIG, "Lanczos basis size m > 64 is not supported");
+  if (max_restarts > 3900) fail(USBS_ERR_CONFIG, "max_restarts > 3900 is not supported");
   const int NH = m <= 32 ? 1 : 2;
   const int G = p->lz_blocks;
   const int64_t ldq = (n + 31) / 32 * 32;
@@ -1372,7 +1373,12 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
     if (clp.cs > 0) lz_cl_launch(ctx, a, clp);
     else if (NH == 1) lz_dispatch<1>(ctx, a, G, p->spmv_group, smem);
     else lz_dispatch<2>(ctx, a, G, p->spmv_group, smem);
+    // flags and (speculatively) the results in one round trip
     USBS_CUDA(cudaMemcpyAsync(hf, flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    USBS_CUDA(cudaMemcpyAsync(ctx->pinned, a.theta, (size_t)k_c * sizeof(double), cudaMemcpyDeviceToHost, st));
+    USBS_CUDA(cudaMemcpyAsync(ctx->pinned + 64, a.res, (size_t)k_c * sizeof(double), cudaMemcpyDeviceToHost, st));
+    USBS_CUDA(cudaMemcpyAsync(ctx->pinned + 128, a.hist, (size_t)(max_restarts + 1) * sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
     USBS_CUDA(cudaStreamSynchronize(st));
     if (hf[F_EXIT] == EXIT_NONFINITE) fail(USBS_ERR_NONFINITE, "matvec returned non-finite values");
     if (hf[F_EXIT] == EXIT_DONE) break;
@@ -1425,11 +1431,7 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
     USBS_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), st));
   }
   const int nh = hf[F_NHIST];
-  double* ho = ctx->pinned;
-  USBS_CUDA(cudaMemcpyAsync(ho, a.theta, (size_t)k_c * sizeof(double), cudaMemcpyDeviceToHost, st));
-  USBS_CUDA(cudaMemcpyAsync(ho + 64, a.res, (size_t)k_c * sizeof(double), cudaMemcpyDeviceToHost, st));
-  USBS_CUDA(cudaMemcpyAsync(ho + 128, a.hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, st));
-  USBS_CUDA(cudaStreamSynchronize(st));
+  const double* ho = ctx->pinned;
   for (int u = 0; u < k_c; ++u) {
     vals[u] = ho[u];
     res[u] = ho[64 + u];

@@ -82,6 +82,10 @@ class Engine:
         check(self.lib.usbs_pivchol(self.h, G.shape[0], _p(G), float(drop_tol), _p(perm), _p(rinv), _p(info)),
               "pivchol")
 
+    def perm_rows(self, perm, rinv, info, out):
+        check(self.lib.usbs_perm_rows(self.h, out.shape[0], _p(perm), _p(rinv), _p(info), _p(out)), "perm_rows")
+        return out
+
     def svec(self, A, out, scale=1.0):
         check(self.lib.usbs_svec(self.h, A.shape[0], _p(A), float(scale), _p(out)), "svec")
         return out

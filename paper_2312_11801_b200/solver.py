@@ -435,7 +435,18 @@ class DeviceSolver:
         rinv = rt.zeros(c, c)
         info = rt.zeros(3)
         eng.pivchol(G, 1e-12, perm, rinv, info)
-        info_h, perm_h, rinv_h = self._fetch(info, perm, rinv)
+        # speculate full rank: the second CholQR pass is issued before the
+        # host reads the rank, so the common case costs one round trip
+        B = eng.perm_rows(perm, rinv, info, rt.empty(c, c))
+        Y = eng.rowgemm(A, B, rt.empty(self.n, c))
+        G2 = rt.empty(c, c)
+        eng.gram(Y, Y, G2)
+        perm2 = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
+        rinv2 = rt.zeros(c, c)
+        info2 = rt.zeros(3)
+        eng.pivchol(G2, -1.0, perm2, rinv2, info2)
+        Q = eng.rowgemm(Y, rinv2, rt.empty(self.n, c))
+        info_h = self._fetch(info)[0]
         r = int(info_h[0])
         if info_h[2] == 0.0:
             raise EmptyBasisError("all input columns are zero")
@@ -443,15 +454,15 @@ class DeviceSolver:
             raise EmptyBasisError("all input columns are numerically dependent")
         if info_h[1] < 1e-6:
             return self._gs_exact(A)
-        B = np.zeros((c, r))
-        B[perm_h[:r].astype(np.int64), :] = rinv_h[:r, :r]
-        Y = eng.rowgemm(A, rt.upload(B), rt.empty(self.n, r))
+        if r == c:
+            return Q
+        # rank-deficient input: the second pass on the r selected columns
+        Yr = Y[:, :r].contiguous()
         G2 = rt.empty(r, r)
-        eng.gram(Y, Y, G2)
+        eng.gram(Yr, Yr, G2)
         rinv2 = rt.zeros(r, r)
-        eng.pivchol(G2, -1.0, perm, rinv2, info)
-        Q = eng.rowgemm(Y, rinv2, rt.empty(self.n, r))
-        return Q
+        eng.pivchol(G2, -1.0, perm2, rinv2, info2)
+        return eng.rowgemm(Yr, rinv2, rt.empty(self.n, r))
 
     def _gs_exact(self, A):
         """Column-pivoted two-pass Gram-Schmidt on device primitives."""

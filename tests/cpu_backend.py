@@ -229,6 +229,15 @@ class CpuEngine:
         perm.copy_(torch.from_numpy(p))
         info.copy_(torch.tensor([float(r), minratio, mx], dtype=torch.float64))
 
+    def perm_rows(self, perm, rinv, info, out):
+        c = out.shape[0]
+        r = int(info[0])
+        b = np.zeros((c, c))
+        p = perm.numpy().astype(np.int64)
+        b[p[:r], :r] = rinv.numpy().reshape(-1)[: c * c].reshape(c, c)[:r, :r]
+        out.copy_(torch.from_numpy(b))
+        return out
+
     def dense_update(self, X, eta, F, lams):
         raise NotImplementedError
 
