@@ -15,7 +15,8 @@
 //     every iterate) instead of an LU inverse; it is symmetrised the same way.
 //   * The reduced Newton matrix M (d x d, d = k(k+1)/2) lives packed-lower in
 //     shared memory (d <= 210, i.e. k <= 20; larger k spills M to global) and
-//     is factorised by a right-looking Cholesky that fails exactly on a
+//     is factorised by a blocked right-looking Cholesky (8-column panels,
+//     trailing tiles on the FP64 tensor cores) that fails exactly on a
 //     non-positive or NaN pivot, like LAPACK potrf.
 #include <algorithm>
 #include <cmath>
@@ -61,7 +62,6 @@ __host__ __device__ inline int state_len(int k) { return 2 * k * k + 7; }
 
 constexpr int IPM_THREADS = 512;
 constexpr int SMEM_D = 210;
-constexpr int CHOL_REG_D = 66;  // register-resident Cholesky up to d = 66 (k = 11)
 constexpr int KMAX = 32;
 
 __device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }  // packed lower, i >= j
@@ -521,100 +521,11 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       }
       __syncthreads();
       IPM_MARK(3);
-      // Blocked Cholesky of M (potrf semantics: fails on a pivot <= 0 or NaN).
-      // Panels of CB columns are factorised by warp 0 (lanes over rows,
-      // __syncwarp only); the trailing update is a SYRK over 4x4 register
-      // tiles by the whole block.  rdiag keeps 1 / L_jj for the solves.
-      double* rdiag = sm.f1;  // f1 is dead once rhs is formed
-      if (d <= CHOL_REG_D) {
-        // d <= 66: right-looking with the matrix in REGISTERS (each thread
-        // owns <= 5 packed entries), one barrier per column; the column being
-        // eliminated is published to a double-buffered smem vector.  Entries
-        // are numbered in the reversed packed order (i', c') = (d-1-c, d-1-i),
-        // so the entries still active at column j (c >= j) are exactly the
-        // prefix x < (d-j)(d-j+1)/2: idle threads and slots drop out as the
-        // trailing matrix shrinks.
-        constexpr int EPT = 5;
-        const int np = d * (d + 1) / 2;
-        double val[EPT];
-        short ri[EPT], ci[EPT];
-        // two columns per barrier: the pre-update columns j and j+1 are
-        // published (A/B buffers, double-buffered), every thread forms the
-        // 2x2 pivot block itself and applies both rank-1 updates
-        double* pA[2] = {sm.tmp, sm.ds};    // column j   (tmp free until E ds, ds until the solves)
-        double* pB[2] = {sm.cb0, sm.cb1};   // column j+1
-#pragma unroll
-        for (int u = 0; u < EPT; ++u) {
-          const int x = tid + u * nth;
-          ri[u] = -1;
-          ci[u] = 0;
-          val[u] = 0.0;
-          if (x < np) {
-            int ip = (int)((sqrtf(8.0f * x + 1.0f) - 1.0f) * 0.5f);
-            while (ip * (ip + 1) / 2 > x) --ip;
-            while ((ip + 1) * (ip + 2) / 2 <= x) ++ip;
-            const int cp = x - ip * (ip + 1) / 2;
-            const int r = d - 1 - cp, c = d - 1 - ip;  // r >= c
-            ri[u] = (short)r;
-            ci[u] = (short)c;
-            val[u] = Mp[pidx(r, c)];
-            if (c == 0) pA[0][r] = val[u];
-            if (c == 1) pB[0][r] = val[u];
-          }
-        }
-        __syncthreads();
-        int buf = 0;
-        for (int j = 0; j < d; j += 2) {
-          const double* ca = pA[buf];
-          const double* cb = pB[buf];
-          double* na = pA[buf ^ 1];
-          double* nb = pB[buf ^ 1];
-          const bool two = j + 1 < d;
-          const double p0 = ca[j];
-          if (!(p0 > 0.0)) { fail = 1; break; }  // uniform
-          const double r0 = rsqrt(p0);
-          double l1 = 0.0, p1 = 1.0, r1 = 0.0;
-          if (two) {
-            l1 = ca[j + 1] * r0;
-            p1 = cb[j + 1] - l1 * l1;
-            if (!(p1 > 0.0)) { fail = 1; break; }
-            r1 = rsqrt(p1);
-          }
-          const int act = (d - j) * (d - j + 1) / 2;  // active entries: x < act
-#pragma unroll
-          for (int u = 0; u < EPT; ++u) {
-            if (tid + u * nth >= act) break;
-            const int i = ri[u], c = ci[u];
-            const double lij = ca[i] * r0;
-            if (c == j) {
-              val[u] = (i == j) ? p0 * r0 : lij;
-            } else if (c == j + 1) {
-              val[u] = (i == j + 1) ? p1 * r1 : (cb[i] - lij * l1) * r1;
-            } else {
-              const double lcj = ca[c] * r0;
-              const double li1 = (cb[i] - lij * l1) * r1, lc1 = (cb[c] - lcj * l1) * r1;
-              val[u] -= lij * lcj + li1 * lc1;
-              if (c == j + 2) na[i] = val[u];
-              if (c == j + 3) nb[i] = val[u];
-            }
-          }
-          if (tid == 0) {
-            rdiag[j] = r0;
-            if (two) rdiag[j + 1] = r1;
-          }
-          buf ^= 1;
-          __syncthreads();
-        }
-        if (!fail) {
-#pragma unroll
-          for (int u = 0; u < EPT; ++u)
-            if (ri[u] >= 0) Mp[pidx(ri[u], ci[u])] = val[u];
-        }
-        __syncthreads();
-      } else {
-        // d > 66: 8-column panels, trailing update on the FP64 tensor cores
-        if (!chol_tiled(Mp, d, rdiag, &sm.flg[5])) fail = 1;
-      }
+      // Cholesky of M (potrf semantics: fails on a pivot <= 0 or NaN) in
+      // 8-column panels with the trailing update on the FP64 tensor cores;
+      // rdiag keeps 1 / L_jj for the solves (f1 is dead once rhs is formed)
+      double* rdiag = sm.f1;
+      if (!chol_tiled(Mp, d, rdiag, &sm.flg[5])) fail = 1;
       IPM_MARK(4);
       if (!fail) {
         // blocked triangular solves: the 32-row diagonal triangles by warp 0
