@@ -216,58 +216,82 @@ __device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, doub
                : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
+// 8 x 8 diagonal block J by one warp: lane l owns entries (l >> 3, l & 7) and
+// (4 + (l >> 3), l & 7) (row i, column t, t <= i); per column the pivot and
+// the two column values each update needs arrive by shuffle, so the chain is
+// shfl -> rsqrt -> shfl -> fma.  Writes L and rdiag; lane 0 sets *flag.
+__device__ __forceinline__ void chol_diag8(double* __restrict__ Mp, int d, int J, double* __restrict__ rdiag,
+                                           int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = J * 8, jb = min(8, d - j0);
+  const int t = lane & 7, ia = lane >> 3, ib = 4 + (lane >> 3);
+  double ea = (ia < jb && t <= ia) ? Mp[pidx(j0 + ia, j0 + t)] : 0.0;
+  double eb = (ib < jb && t <= ib) ? Mp[pidx(j0 + ib, j0 + t)] : 0.0;
+  int ok = 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < jb) {
+      const double pv = __shfl_sync(0xffffffffu, c < 4 ? ea : eb, (c & 3) * 8 + c);
+      if (!(pv > 0.0)) ok = 0;
+      const double r = ok ? rsqrt(pv) : 0.0;
+      if (t == c) {
+        if (ia > c) ea *= r; else if (ia == c) ea = pv * r;
+        if (ib > c) eb *= r; else if (ib == c) eb = pv * r;
+      }
+      if (lane == 0) rdiag[j0 + c] = r;
+      const double lia = __shfl_sync(0xffffffffu, ea, (ia & 3) * 8 + c);  // L(ia, c), ia < 4
+      const double lib = __shfl_sync(0xffffffffu, eb, (ib & 3) * 8 + c);  // L(ib, c)
+      const double lta_a = __shfl_sync(0xffffffffu, ea, (t & 3) * 8 + c);
+      const double lta_b = __shfl_sync(0xffffffffu, eb, (t & 3) * 8 + c);
+      const double lta = t < 4 ? lta_a : lta_b;  // L(t, c)
+      if (t > c) {
+        if (t <= ia) ea -= lia * lta;
+        if (t <= ib) eb -= lib * lta;
+      }
+    }
+  }
+  if (ia < jb && t <= ia) Mp[pidx(j0 + ia, j0 + t)] = ea;
+  if (ib < jb && t <= ib) Mp[pidx(j0 + ib, j0 + t)] = eb;
+  if (lane == 0) *flag = ok;
+}
+
+// C_IK -= L_IJ L_KJ^T for one 8 x 8 tile pair (I, K tile rows/cols, absolute)
+__device__ __forceinline__ void chol_tile_update(double* __restrict__ Mp, int d, int j0, int jb, int I, int K) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int ra = I * 8 + g, rb = K * 8 + g;
+  const int oa = ra < d ? pidx(ra, 0) : 0;
+  const int ob = rb < d ? pidx(rb, 0) : 0;
+  const double a0 = (ra < d && q < jb) ? -Mp[oa + j0 + q] : 0.0;
+  const double a1 = (ra < d && q + 4 < jb) ? -Mp[oa + j0 + 4 + q] : 0.0;
+  const double b0 = (rb < d && q < jb) ? Mp[ob + j0 + q] : 0.0;
+  const double b1 = (rb < d && q + 4 < jb) ? Mp[ob + j0 + 4 + q] : 0.0;
+  const int cc = K * 8 + 2 * q;
+  const bool v0 = ra < d && cc <= ra, v1 = ra < d && cc + 1 <= ra;
+  double c0 = v0 ? Mp[oa + cc] : 0.0, c1 = v1 ? Mp[oa + cc + 1] : 0.0;
+  double d0, d1;
+  dmma8x8x4(d0, d1, a0, b0, c0, c1);
+  dmma8x8x4(d0, d1, a1, b1, d0, d1);
+  if (v0) Mp[oa + cc] = d0;
+  if (v1) Mp[oa + cc + 1] = d1;
+}
+
 // Blocked right-looking Cholesky of the packed lower matrix M (d x d) by
-// 8-column panels: (1) the 8 x 8 diagonal block by one warp (potrf: fails on
-// a pivot <= 0 or NaN), (2) the panel below it by forward substitution, a
-// thread per row, (3) the trailing update C_IK -= L_IJ L_KJ^T per 8 x 8 tile
-// pair with two DMMA m8n8k4 per tile, warps over tile pairs.  rdiag[j] =
-// 1 / L_jj.  Returns 0 on failure (uniform).
+// 8-column panels with look-ahead: per panel J, (a) the rows below block J
+// by forward substitution, a thread per row; (b) the trailing update
+// C_IK -= L_IJ L_KJ^T per 8 x 8 tile pair, two DMMA m8n8k4 per tile, while
+// warp 0 first updates the next diagonal block and factorises it (potrf
+// semantics: fails on a pivot <= 0 or NaN), so the diagonal chain overlaps
+// the tensor-core update.  Two barriers per panel.  rdiag[j] = 1 / L_jj.
+// Returns 0 on failure (uniform).
 __device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ rdiag, int* flag) {
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwp = nth >> 5;
+  const int tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, nwp = nth >> 5;
   const int T = (d + 7) >> 3;
+  if (warp == 0) chol_diag8(Mp, d, 0, rdiag, flag);
+  __syncthreads();
+  if (!*flag) return 0;
   for (int J = 0; J < T; ++J) {
     const int j0 = J * 8, jb = min(8, d - j0);
-    // (1) diagonal block by warp 0: lane l owns entries (l >> 3, l & 7) and
-    // (4 + (l >> 3), l & 7) of the 8 x 8 block (row i, column t, t <= i);
-    // per column: the pivot and the two column values each update needs
-    // arrive by shuffle, so the chain is shfl -> rsqrt -> shfl -> fma
-    if (warp == 0) {
-      const int t = lane & 7, ia = lane >> 3, ib = 4 + (lane >> 3);
-      double ea = (ia < jb && t <= ia) ? Mp[pidx(j0 + ia, j0 + t)] : 0.0;
-      double eb = (ib < jb && t <= ib) ? Mp[pidx(j0 + ib, j0 + t)] : 0.0;
-      int ok = 1;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c < jb) {
-          // pivot (c, c): lane (c & 3) * 8 + c, entry a if c < 4 else b
-          const double pv = __shfl_sync(0xffffffffu, c < 4 ? ea : eb, (c & 3) * 8 + c);
-          if (!(pv > 0.0)) ok = 0;
-          const double r = ok ? rsqrt(pv) : 0.0;
-          // column c: entries (i, c) for i >= c live on lanes (i & 3) * 8 + c
-          if (t == c) {
-            if (ia > c) ea *= r; else if (ia == c) ea = pv * r;
-            if (ib > c) eb *= r; else if (ib == c) eb = pv * r;
-          }
-          if (lane == 0) rdiag[j0 + c] = r;
-          // trailing: e(i, t) -= L(i, c) L(t, c) for c < t <= i
-          const double lia = __shfl_sync(0xffffffffu, ea, (ia & 3) * 8 + c);  // L(ia, c), ia < 4
-          const double lib = __shfl_sync(0xffffffffu, eb, (ib & 3) * 8 + c);  // L(ib, c)
-          const double lta_a = __shfl_sync(0xffffffffu, ea, (t & 3) * 8 + c);
-          const double lta_b = __shfl_sync(0xffffffffu, eb, (t & 3) * 8 + c);
-          const double lta = t < 4 ? lta_a : lta_b;  // L(t, c)
-          if (t > c) {
-            if (t <= ia) ea -= lia * lta;
-            if (t <= ib) eb -= lib * lta;
-          }
-        }
-      }
-      if (ia < jb && t <= ia) Mp[pidx(j0 + ia, j0 + t)] = ea;
-      if (ib < jb && t <= ib) Mp[pidx(j0 + ib, j0 + t)] = eb;
-      if (lane == 0) *flag = ok;
-    }
-    __syncthreads();
-    if (!*flag) return 0;
-    // (2) panel rows below: x = a L_JJ^{-T}
+    // (a) panel rows below: x = a L_JJ^{-T}
     for (int i = j0 + jb + tid; i < d; i += nth) {
       double* ri = Mp + pidx(i, j0);
       double x[8];
@@ -282,33 +306,27 @@ __device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ r
       }
     }
     __syncthreads();
-    // (3) trailing tiles K <= I, both > J: tile pairs dealt round-robin to
-    // the warps in row-major order (balanced), (I, K) advanced incrementally
+    // (b) trailing tile pairs (I, K), J < K <= I; pair 0 = the next diagonal
+    // block goes to warp 0 (update + factorisation), the rest round-robin
     const int R = T - J - 1, npairs = R * (R + 1) / 2;
-    const int g = lane >> 2, q = lane & 3;
-    int I = 0, K = warp;
-    while (K > I) { K -= I + 1; ++I; }
-    for (int pq = warp; pq < npairs; pq += nwp) {
-      const int i0 = (J + 1 + I) * 8, ra = i0 + g;
-      const int oa = ra < d ? pidx(ra, 0) : 0;
-      const double a0 = (ra < d && q < jb) ? -Mp[oa + j0 + q] : 0.0;
-      const double a1 = (ra < d && q + 4 < jb) ? -Mp[oa + j0 + 4 + q] : 0.0;
-      const int k0 = (J + 1 + K) * 8, rb = k0 + g;
-      const int ob = rb < d ? pidx(rb, 0) : 0;
-      const double b0 = (rb < d && q < jb) ? Mp[ob + j0 + q] : 0.0;
-      const double b1 = (rb < d && q + 4 < jb) ? Mp[ob + j0 + 4 + q] : 0.0;
-      const int cc = k0 + 2 * q;
-      const bool v0 = ra < d && cc <= ra, v1 = ra < d && cc + 1 <= ra;
-      double c0 = v0 ? Mp[oa + cc] : 0.0, c1 = v1 ? Mp[oa + cc + 1] : 0.0;
-      double d0, d1;
-      dmma8x8x4(d0, d1, a0, b0, c0, c1);
-      dmma8x8x4(d0, d1, a1, b1, d0, d1);
-      if (v0) Mp[oa + cc] = d0;
-      if (v1) Mp[oa + cc + 1] = d1;
-      K += nwp;
+    if (warp == 0) {
+      if (R > 0) {
+        chol_tile_update(Mp, d, j0, jb, J + 1, J + 1);
+        __syncwarp();
+        chol_diag8(Mp, d, J + 1, rdiag, flag);
+      }
+    } else {
+      const int nw1 = nwp - 1;
+      int I = 0, K = warp;  // pair index pq = warp (>= 1)
       while (K > I) { K -= I + 1; ++I; }
+      for (int pq = warp; pq < npairs; pq += nw1) {
+        chol_tile_update(Mp, d, j0, jb, J + 1 + I, J + 1 + K);
+        K += nw1;
+        while (K > I) { K -= I + 1; ++I; }
+      }
     }
     __syncthreads();
+    if (R > 0 && !*flag) return 0;
   }
   return 1;
 }
