@@ -122,6 +122,13 @@ struct usbs_problem {
   int* blk_seg = nullptr;  // Lanczos block b's SpMV segments [blk_seg[b], blk_seg[b+1])
   int* seg_r0 = nullptr;   // segment rows [seg_r0, seg_r1): <= LZT_NNZ nonzeros or one row
   int* seg_r1 = nullptr;
+  int lz_npieces = 0;             // pieces of rows above LZT_NNZ nonzeros
+  int* lz_piece_z0 = nullptr;     //   nonzero range of each piece
+  int* lz_piece_z1 = nullptr;
+  int* lz_blk_split = nullptr;    // row block b's split rows [lz_blk_split[b], [b+1])
+  int* lz_split_row = nullptr;    //   row, first piece, piece count
+  int* lz_split_first = nullptr;
+  int* lz_split_cnt = nullptr;
   std::vector<void*> owned;
 };
 

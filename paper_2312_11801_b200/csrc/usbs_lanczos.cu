@@ -55,7 +55,14 @@ struct LzArgs {
   const int* blk_row;  // block b owns rows [blk_row[b], blk_row[b+1]) (Q passes)
   const int* blk_seg;  // ... and SpMV segments [blk_seg[b], blk_seg[b+1]) (nnz-balanced)
   const int* seg_r0;   // segment: rows [seg_r0, seg_r1), <= LZT_NNZ nonzeros,
-  const int* seg_r1;   //   or a single row with more (block-wide sum)
+  const int* seg_r1;   //   or (seg_r1 < 0) piece -seg_r1-1 of a longer row
+  const int* piece_z0;  // nonzero range of each piece
+  const int* piece_z1;
+  double* piece_sum;    // partial sum of each piece
+  const int* blk_split;  // row block b's split rows [blk_split[b], blk_split[b+1])
+  const int* split_row;
+  const int* split_first;
+  const int* split_cnt;
   double* Q;
   double* W0;
   double* W1;
@@ -263,8 +270,9 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       // one); a row above LZT_NNZ nonzeros is summed by the whole block.
       for (int e = e0; e < e1; ++e) {
         const int t0 = a.seg_r0[e], t1 = a.seg_r1[e];
-        const int base = a.rowptr[t0], cnt = a.rowptr[t1] - base;
-        if (cnt > LZT_NNZ) {
+        if (t1 < 0) {  // a piece of a long row: block-wide partial sum
+          const int pc = -t1 - 1;
+          const int base = a.piece_z0[pc], cnt = a.piece_z1[pc] - base;
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
           for (int z0 = 0; z0 < cnt; z0 += nth * 8) {
             int cc[8];
@@ -280,9 +288,10 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
               if (cc[u] >= 0) acc[u & 3] = fma(vv[u], (from_q ? a.Q[qidx(cc[u], j, M1)] : Wprev[cc[u]]) * xs, acc[u & 3]);
           }
           const double tot = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), red);
-          if (tid == 0) Wcur[t0] = tot;
+          if (tid == 0) a.piece_sum[pc] = tot;
           continue;  // block_sum ends with a barrier
         }
+        const int base = a.rowptr[t0], cnt = a.rowptr[t1] - base;
         constexpr int PER = LZT_NNZ / (NH == 1 ? 512 : 256);
         int cc[PER];
         double vv[PER];
@@ -329,6 +338,14 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       // every W row must be final before the column sums
       grid.sync();
       BW_START();
+      // rows cut into pieces: their owner adds the partial sums in order
+      for (int x = a.blk_split[b] + tid; x < a.blk_split[b + 1]; x += nth) {
+        double tot = 0.0;
+        const int f = a.split_first[x], c = a.split_cnt[x];
+        for (int u = 0; u < c; ++u) tot += a.piece_sum[f + u];
+        Wcur[a.split_row[x]] = tot;
+      }
+      if (a.blk_split[b + 1] > a.blk_split[b]) __syncthreads();
       ++matvecs;
       {
         int bad = 0;
@@ -1344,6 +1361,10 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   a.tol = tol < 0 ? 1e-9 : tol;
   a.rowptr = p->rowptr; a.col = p->col; a.val = val;
   a.blk_row = p->blk_row; a.blk_seg = p->blk_seg; a.seg_r0 = p->seg_r0; a.seg_r1 = p->seg_r1;
+  a.piece_z0 = p->lz_piece_z0; a.piece_z1 = p->lz_piece_z1;
+  a.piece_sum = (double*)ctx->ws.get(WS_LZ_SPLIT, (size_t)std::max(1, p->lz_npieces) * sizeof(double));
+  a.blk_split = p->lz_blk_split; a.split_row = p->lz_split_row; a.split_first = p->lz_split_first;
+  a.split_cnt = p->lz_split_cnt;
   a.Q = Q; a.W0 = W; a.W1 = W + ldq; a.H = H;
   a.P1 = P; a.P2 = P + G * 64; a.P3 = P + 2 * G * 64;
   a.flags = flags;

@@ -490,28 +490,58 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     for (int bb = 1; bb < G; ++bb) blk_row[bb] = (int32_t)std::min<int64_t>(n, (blk_row[bb] + 31) / 32 * 32);
     for (int bb = 1; bb <= G; ++bb) blk_row[bb] = std::max(blk_row[bb], blk_row[bb - 1]);
     // SpMV segments over the whole matrix: <= LZT_NNZ nonzeros and
-    // <= LZT_ROWS rows, or one row with more
+    // <= LZT_ROWS rows; a row with more is cut into LZT_NNZ-nonzero pieces
+    // (segment r1 = -(piece + 1)) whose partial sums its row owner adds up
+    std::vector<int32_t> pz0, pz1, srow, sfirst, scnt;
     int64_t i = 0;
     while (i < n) {
       const int64_t s0 = i;
       if (rp32[i + 1] - rp32[i] > LZT_NNZ) {
+        srow.push_back((int32_t)i);
+        sfirst.push_back((int32_t)pz0.size());
+        int c = 0;
+        for (int32_t z = rp32[i]; z < rp32[i + 1]; z += LZT_NNZ, ++c) {
+          seg_r0.push_back((int32_t)i);
+          seg_r1.push_back(-(int32_t)pz0.size() - 1);
+          pz0.push_back(z);
+          pz1.push_back(std::min(rp32[i + 1], z + LZT_NNZ));
+        }
+        scnt.push_back(c);
         ++i;
-      } else {
-        while (i < n && i - s0 < LZT_ROWS && rp32[i + 1] - rp32[i] <= LZT_NNZ && rp32[i + 1] - rp32[s0] <= LZT_NNZ)
-          ++i;
+        continue;
       }
+      while (i < n && i - s0 < LZT_ROWS && rp32[i + 1] - rp32[i] <= LZT_NNZ && rp32[i + 1] - rp32[s0] <= LZT_NNZ)
+        ++i;
       seg_r0.push_back((int32_t)s0);
       seg_r1.push_back((int32_t)i);
     }
+    p->lz_npieces = (int)pz0.size();
+    p->lz_piece_z0 = dev_upload(p, pz0.data(), pz0.size());
+    p->lz_piece_z1 = dev_upload(p, pz1.data(), pz1.size());
+    // split rows per row block (both lists ascend in row order)
+    std::vector<int32_t> blk_sp(G + 1, 0);
+    for (int bb = 0; bb <= G; ++bb)
+      blk_sp[bb] = (int32_t)(std::lower_bound(srow.begin(), srow.end(), blk_row[bb]) - srow.begin());
+    p->lz_blk_split = dev_upload(p, blk_sp.data(), blk_sp.size());
+    p->lz_split_row = dev_upload(p, srow.data(), srow.size());
+    p->lz_split_first = dev_upload(p, sfirst.data(), sfirst.size());
+    p->lz_split_cnt = dev_upload(p, scnt.data(), scnt.size());
     // contiguous segment ranges per block, balanced on nonzeros + 2 per row
     const int64_t ns = (int64_t)seg_r0.size();
+    auto seg_cost = [&](int64_t e) -> double {
+      if (seg_r1[e] < 0) {
+        const int pc = -seg_r1[e] - 1;
+        return (double)(pz1[pc] - pz0[pc]);
+      }
+      return (rp32[seg_r1[e]] - rp32[seg_r0[e]]) + 2.0 * (seg_r1[e] - seg_r0[e]);
+    };
     double stot = 0.0;
-    for (int64_t e = 0; e < ns; ++e) stot += (rp32[seg_r1[e]] - rp32[seg_r0[e]]) + 2.0 * (seg_r1[e] - seg_r0[e]);
+    for (int64_t e = 0; e < ns; ++e) stot += seg_cost(e);
     double sacc = 0.0;
     int sb = 0;
     blk_seg[0] = 0;
     for (int64_t e = 0; e < ns && sb + 1 < G; ++e) {
-      sacc += (rp32[seg_r1[e]] - rp32[seg_r0[e]]) + 2.0 * (seg_r1[e] - seg_r0[e]);
+      sacc += seg_cost(e);
       if (sacc >= stot * (sb + 1) / G) blk_seg[++sb] = (int32_t)(e + 1);
     }
     for (int bb = sb + 1; bb <= G; ++bb) blk_seg[bb] = (int32_t)ns;
