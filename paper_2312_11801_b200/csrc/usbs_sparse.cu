@@ -599,8 +599,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     // CSR-stream tiles: maximal runs of at most ST_ROWS consecutive rows with
     // at most ST_NNZ nonzeros in total; longer rows get a block of their own
     {
-      const char* te = getenv("USBS_SPMV_TILE");
-      const int ST_NNZ = (te && atoi(te) == 2048) ? 2048 : (te && atoi(te) == 4096) ? 4096 : 1024;
+      const int ST_NNZ = 1024;  // the tile size k_spmv_fused is instantiated for
       p->st_nnz = ST_NNZ;
       std::vector<int32_t> t0, t1, hr;
       int64_t i = 0;
@@ -723,15 +722,9 @@ void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const d
   if (k == 1) {
     const int64_t nb = (int64_t)p->n_huge_rows + p->n_stiles;
     if (nb > 0) {
-#define USBS_SPMV_ARGS p->n_huge_rows, p->huge_rows, p->n_stiles, p->stile_r0, p->stile_r1, p->rowptr, p->col, \
-                       val, V, ldv, Y, ldy
-      if (p->st_nnz == 2048)
-        k_spmv_fused<2048, 512, 3><<<(unsigned)nb, 512, 0, ctx->stream>>>(USBS_SPMV_ARGS);
-      else if (p->st_nnz == 4096)
-        k_spmv_fused<4096, 512, 2><<<(unsigned)nb, 512, 0, ctx->stream>>>(USBS_SPMV_ARGS);
-      else
-        k_spmv_fused<1024, 256, 6><<<(unsigned)nb, 256, 0, ctx->stream>>>(USBS_SPMV_ARGS);
-#undef USBS_SPMV_ARGS
+k_spmv_fused<1024, 256, 6><<<(unsigned)nb, 256, 0, ctx->stream>>>(
+          p->n_huge_rows, p->huge_rows, p->n_stiles, p->stile_r0, p->stile_r1, p->rowptr, p->col, val, V, ldv, Y,
+          ldy);
       check_launch(ctx);
     }
     return;
