@@ -572,9 +572,16 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           __syncthreads();
           for (int i = J + JB + tid; i < d; i += nth) {
             const int base = i * (i + 1) / 2 + J;
-            double s = 0.0;
-            for (int jj = 0; jj < JB; ++jj) s = fma(Mp[base + jj], sm.rhs[J + jj], s);
-            sm.rhs[i] -= s;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int jj = 0;
+            for (; jj + 3 < JB; jj += 4) {
+              s0 = fma(Mp[base + jj], sm.rhs[J + jj], s0);
+              s1 = fma(Mp[base + jj + 1], sm.rhs[J + jj + 1], s1);
+              s2 = fma(Mp[base + jj + 2], sm.rhs[J + jj + 2], s2);
+              s3 = fma(Mp[base + jj + 3], sm.rhs[J + jj + 3], s3);
+            }
+            for (; jj < JB; ++jj) s0 = fma(Mp[base + jj], sm.rhs[J + jj], s0);
+            sm.rhs[i] -= (s0 + s1) + (s2 + s3);
           }
           __syncthreads();
         }
@@ -598,9 +605,16 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           }
           __syncthreads();
           for (int i = tid; i < J; i += nth) {
-            double s = 0.0;
-            for (int jj = 0; jj < JB; ++jj) s = fma(Mp[pidx(J + jj, i)], sm.ds[J + jj], s);
-            sm.rhs[i] -= s;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int jj = 0;
+            for (; jj + 3 < JB; jj += 4) {
+              s0 = fma(Mp[pidx(J + jj, i)], sm.ds[J + jj], s0);
+              s1 = fma(Mp[pidx(J + jj + 1, i)], sm.ds[J + jj + 1], s1);
+              s2 = fma(Mp[pidx(J + jj + 2, i)], sm.ds[J + jj + 2], s2);
+              s3 = fma(Mp[pidx(J + jj + 3, i)], sm.ds[J + jj + 3], s3);
+            }
+            for (; jj < JB; ++jj) s0 = fma(Mp[pidx(J + jj, i)], sm.ds[J + jj], s0);
+            sm.rhs[i] -= (s0 + s1) + (s2 + s3);
           }
           __syncthreads();
         }
