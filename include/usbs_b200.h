@@ -217,6 +217,31 @@ usbs_status usbs_pivchol(usbs_ctx* ctx, int c, const double* g_dev, double drop_
 usbs_status usbs_perm_rows(usbs_ctx* ctx, int c, const int32_t* perm_dev, const double* rinv_dev,
                            const double* info_dev, double* out_dev);
 
+/* ---- the constraint-bundle duck type (problem.py:144-243) ------------------
+ * Device halves of DiagonalConstraints / SparseConstraintFamilies for an
+ * unsharded problem (the Python shim constraints.DeviceConstraints returns
+ * numpy on demand). */
+/* Y = A*(y) V (n x k, dev), optionally gram = sym(V^T Y): adjoint_matvec /
+ * adjoint_inner_lowrank (problem.py:163-167, 222-227). */
+usbs_status usbs_cons_adjoint_apply(usbs_ctx* ctx, usbs_problem* p, const double* y_dev,
+                                    const double* v_dev, int64_t ldv, int k, double* y_out_dev,
+                                    int64_t ldy, double* gram_dev);
+/* A*(y) on the problem's merged pattern (nnz values, dev) and that pattern
+ * (host: rowptr int64 n+1, col int32 nnz, nent int32 nnz = constraint
+ * entries per slot, zero for slots that only hold cost entries):
+ * adjoint_matrix (problem.py:160-161, 214-220). */
+usbs_status usbs_cons_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* y_dev,
+                                     double* vals_dev);
+usbs_status usbs_problem_pattern(usbs_problem* p, int64_t* rowptr, int32_t* col, int32_t* nent);
+/* out (m, dev) = A(X) for a dense n x n X (dev, ld): primal_image_dense
+ * (problem.py:157-158, 210-212). */
+usbs_status usbs_cons_image_dense(usbs_ctx* ctx, usbs_problem* p, const double* x_dev, int64_t ldx,
+                                  double* out_dev);
+/* out (m x d, dev, ld >= d) = rows svec(V^T A_i V): compressed_rows
+ * (problem.py:169-173, 229-239); the solver itself never materialises it. */
+usbs_status usbs_cons_compressed_rows(usbs_ctx* ctx, usbs_problem* p, const double* v_dev,
+                                      int64_t ldv, int k, double* out_dev, int64_t ldo);
+
 /* dst[i] = src[idx[i]] for i < n (dev): the ghost-dual refresh of an
  * entry-family row shard (the mirrored Z slots of constraints owned by
  * another rank read these copies; dist.EntryShardPlan). */

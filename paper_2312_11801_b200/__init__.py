@@ -40,6 +40,8 @@ _LAZY = {
     "ipm_quad": ("subproblem", "ipm_quad"),
     "ipm_eval": ("subproblem", "ipm_eval"),
     "maxcut_round": ("rounding", "maxcut_round"),
+    "DeviceConstraints": ("constraints", "DeviceConstraints"),
+    "device_constraints": ("constraints", "device_constraints"),
     "qap_round": ("rounding", "qap_round"),
 }
 

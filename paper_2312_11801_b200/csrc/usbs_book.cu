@@ -618,6 +618,55 @@ __global__ void k_perm_rows(int c, const int* __restrict__ perm, const double* _
   }
 }
 
+// --------------------------------------------- constraint-bundle surface
+// primal_image_dense (problem.py:157-158, 210-212): sum over constraint i's
+// entries of (2 - [r == c]) val X[r, c]; diagonal family: X[i, i]
+__global__ void __launch_bounds__(256) k_image_dense(int64_t m, int diag_only, const int* __restrict__ cptr,
+                                                     const int* __restrict__ cent, const int* __restrict__ erow,
+                                                     const int* __restrict__ ecol, const double* __restrict__ eval,
+                                                     const double* __restrict__ X, int64_t ldx,
+                                                     double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, gw = lane >> 3, t = lane & 7;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wb = wid * 4; wb < m; wb += nwarps * 4) {
+    const int64_t i = wb + gw;
+    double acc = 0.0;
+    if (i < m) {
+      if (diag_only) {
+        if (t == 0) acc = X[i * ldx + i];
+      } else {
+        for (int q = cptr[i] + t; q < cptr[i + 1]; q += 8) {
+          const int e = cent[q];
+          const int r = erow[e], c = ecol[e];
+          acc = fma(X[(int64_t)r * ldx + c], (r == c) ? eval[e] : 2.0 * eval[e], acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, 8);
+    if (i < m && t == 0) out[i] = acc;
+  }
+}
+
+// compressed_rows (problem.py:169-173, 229-239): row i = svec(V^T A_i V),
+// column-major lower-triangle order with sqrt(2) off the diagonal
+__global__ void k_compressed_rows(int64_t m, int diag_only, const int* __restrict__ cptr,
+                                  const int* __restrict__ cent, const int* __restrict__ erow,
+                                  const int* __restrict__ ecol, const double* __restrict__ eval,
+                                  const double* __restrict__ V, int64_t ldv, int k, double* __restrict__ out,
+                                  int64_t ldo) {
+  const int d = k * (k + 1) / 2;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < m * d; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / d;
+    int rem = (int)(x % d), j = 0;
+    while (rem >= k - j) { rem -= k - j; ++j; }
+    const int a = j + rem, bcol = j;  // svec position -> (row a, column b), a >= b
+    out[i * ldo + (x % d)] = crow_entry(diag_only, i, a, bcol, a == bcol ? 1.0 : 1.4142135623730951, cptr, cent,
+                                        erow, ecol, eval, V, ldv);
+  }
+}
+
 }  // namespace usbs
 
 using namespace usbs;
@@ -838,6 +887,55 @@ usbs_status usbs_perm_rows(usbs_ctx* ctx, int c, const int32_t* perm, const doub
   USBS_API_BEGIN
   if (c < 1 || c > 64) fail(USBS_ERR_SHAPE, "perm_rows: 1 <= c <= 64");
   k_perm_rows<<<1, 256, 0, ctx->stream>>>(c, perm, rinv, info, out);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_cons_adjoint_apply(usbs_ctx* ctx, usbs_problem* p, const double* y, const double* V, int64_t ldv,
+                                    int k, double* Y, int64_t ldy, double* gram) {
+  USBS_API_BEGIN
+  if (p->n_cols != p->n) fail(USBS_ERR_SHAPE, "cons_adjoint_apply needs an unsharded problem");
+  if (k < 1 || ldv < k || ldy < k) fail(USBS_ERR_SHAPE, "cons_adjoint_apply: bad k / leading dimension");
+  double* tval = (double*)ctx->ws.get(WS_BOOK_T, (size_t)p->nnz * sizeof(double));
+  launch_adjoint_values(ctx, p, y, tval);
+  launch_spmm_vals(ctx, p, tval, V, ldv, k, Y, ldy);
+  if (gram) launch_gram_tn(ctx, p->n, V, ldv, k, Y, ldy, k, gram, true);
+  USBS_API_END
+}
+
+usbs_status usbs_cons_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* y, double* vals) {
+  USBS_API_BEGIN
+  launch_adjoint_values(ctx, p, y, vals);
+  USBS_API_END
+}
+
+usbs_status usbs_problem_pattern(usbs_problem* p, int64_t* rowptr, int32_t* col, int32_t* nent) {
+  USBS_API_BEGIN
+  std::vector<int32_t> rp(p->n + 1), ap(p->nnz + 1);
+  USBS_CUDA(cudaMemcpy(rp.data(), p->rowptr, (p->n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  USBS_CUDA(cudaMemcpy(col, p->col, p->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  USBS_CUDA(cudaMemcpy(ap.data(), p->aptr, (p->nnz + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i <= p->n; ++i) rowptr[i] = rp[i];
+  for (int64_t s = 0; s < p->nnz; ++s) nent[s] = ap[s + 1] - ap[s];
+  USBS_API_END
+}
+
+usbs_status usbs_cons_image_dense(usbs_ctx* ctx, usbs_problem* p, const double* X, int64_t ldx, double* out) {
+  USBS_API_BEGIN
+  if (p->n_cols != p->n) fail(USBS_ERR_SHAPE, "cons_image_dense needs an unsharded problem");
+  k_image_dense<<<nblocks(ctx, (p->m + 3) / 4 * 32), 256, 0, ctx->stream>>>(
+      p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row, p->e_col, p->e_val, X, ldx, out);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+usbs_status usbs_cons_compressed_rows(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k,
+                                      double* out, int64_t ldo) {
+  USBS_API_BEGIN
+  if (k < 1 || k > 64 || ldo < k * (k + 1) / 2) fail(USBS_ERR_SHAPE, "cons_compressed_rows: bad k / ldo");
+  const int64_t tot = p->m * (int64_t)(k * (k + 1) / 2);
+  k_compressed_rows<<<nblocks(ctx, tot), 256, 0, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent,
+                                                                p->e_row, p->e_col, p->e_val, V, ldv, k, out, ldo);
   check_launch(ctx);
   USBS_API_END
 }
