@@ -41,6 +41,10 @@ _LAZY = {
     "ipm_eval": ("subproblem", "ipm_eval"),
     "maxcut_round": ("rounding", "maxcut_round"),
     "DeviceConstraints": ("constraints", "DeviceConstraints"),
+    "orthonormalize": ("linalg", "orthonormalize"),
+    "sketch_init": ("linalg", "sketch_init"),
+    "sketch_update": ("linalg", "sketch_update"),
+    "reconstruct": ("linalg", "reconstruct"),
     "device_constraints": ("constraints", "device_constraints"),
     "qap_round": ("rounding", "qap_round"),
 }

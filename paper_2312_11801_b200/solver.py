@@ -304,6 +304,92 @@ class PrimalOutput:
 S_Q22, S_LINETA, S_EQ22, S_ELINETA, S_DNU, S_CQS, S_BYC, S_RES, S_BY, S_MINI, S_CFIP = 0, 1, 2, 3, 4, 6, 8, 10, 12, 14, 16
 
 
+def orthonormalize_dev(eng: Engine, A, drop_tol: float = 1e-12):
+    """symlin.orthonormalize (symlin.py:148-190) on device tensors: pivot order
+    and drop rule from a pivoted Cholesky of the Gram, then CholQR2 (the
+    second pass speculatively issued for full rank, so the common case costs
+    one round trip).  Falls back to the exact column-pivoted Gram-Schmidt when
+    a selected residual is below 1e-6 of the largest column or a column is
+    dropped: there a Gram cannot resolve the drop rule."""
+    rt = eng.rt
+    n, c = A.shape
+    G = rt.empty(c, c)
+    eng.gram(A, A, G)
+    perm = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
+    rinv = rt.zeros(c, c)
+    info = rt.zeros(3)
+    eng.pivchol(G, drop_tol, perm, rinv, info)
+    B = eng.perm_rows(perm, rinv, info, rt.empty(c, c))
+    Y = eng.rowgemm(A, B, rt.empty(n, c))
+    G2 = rt.empty(c, c)
+    eng.gram(Y, Y, G2)
+    perm2 = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
+    rinv2 = rt.zeros(c, c)
+    info2 = rt.zeros(3)
+    eng.pivchol(G2, -1.0, perm2, rinv2, info2)
+    Q = eng.rowgemm(Y, rinv2, rt.empty(n, c))
+    info_h = info.cpu().numpy()
+    r = int(info_h[0])
+    if info_h[2] == 0.0:
+        raise EmptyBasisError("all input columns are zero")
+    if r == 0:
+        raise EmptyBasisError("all input columns are numerically dependent")
+    if info_h[1] < 1e-6 or r < c:
+        # a selected residual below what a Gram resolves, or dropped columns
+        # (whose true residual the Gram cannot tell from the 1e-12 rule)
+        return _gs_exact_dev(eng, A, drop_tol)
+    return Q
+
+
+def _gs_exact_dev(eng: Engine, A, drop_tol: float = 1e-12):
+    """Column-pivoted two-pass Gram-Schmidt on device primitives."""
+    rt = eng.rt
+    n, c = A.shape
+    ident = rt.upload(np.eye(c))
+    work = rt.empty(n, c)
+    eng.rowgemm(A, ident, work)
+    G = rt.empty(c, c)
+    eng.gram(work, work, G)
+    norms = np.sqrt(np.maximum(np.diag(G.cpu().numpy()), 0.0))
+    thresh = drop_tol * float(norms.max())
+    alive = list(range(c))
+    basis = rt.empty(n, c)
+    nb = 0
+    coef = rt.empty(c, c)
+    red = rt.zeros(2)
+    while alive:
+        eng.gram(work, work, G)
+        g = G.cpu().numpy()
+        nr = np.sqrt(np.maximum(np.array([g[j, j] for j in alive]), 0.0))
+        pick = int(np.argmax(nr))
+        if nr[pick] <= thresh:
+            break
+        piv = alive.pop(pick)
+        q = rt.empty(n, 1)
+        eng.rowgemm(work[:, piv:piv + 1], ident[:1, :1], q)
+        if nb:
+            Bm = basis[:, :nb]
+            cv = coef.view(-1)[:nb].view(nb, 1)  # gram writes a contiguous block
+            eng.gram(Bm, q, cv)
+            eng.rowgemm(Bm, cv, q, alpha=-1.0, beta=1.0, Y0=q)
+        eng.dot_into(q.view(-1), q.view(-1), red)
+        nq = math.sqrt(float(red[0].item()))
+        if nq <= thresh:
+            continue
+        eng.rowgemm(q, ident[:1, :1], basis[:, nb:nb + 1], alpha=1.0 / nq)
+        qb = basis[:, nb:nb + 1]
+        nb += 1
+        for j in alive:
+            col = work[:, j:j + 1]
+            eng.gram(qb, col, coef[:1, :1])
+            eng.rowgemm(qb, coef[:1, :1], col, alpha=-1.0, beta=1.0, Y0=col)
+    if nb == 0:
+        raise EmptyBasisError("all input columns are numerically dependent")
+    out = rt.empty(n, nb)
+    eng.rowgemm(basis[:, :nb], ident[:nb, :nb], out)
+    return out
+
+
 class DeviceSolver:
     """Holds the uploaded problem and scratch buffers for one solve."""
 
@@ -423,93 +509,8 @@ class DeviceSolver:
         return out
 
     def orthonormalize(self, A):
-        """symlin.orthonormalize (symlin.py:148-190): pivot order and drop rule
-        from a pivoted Cholesky of the Gram, then CholQR2.  Falls back to the
-        exact column-pivoted Gram-Schmidt when a selected residual is below
-        1e-6 of the largest column (where a Gram cannot resolve the 1e-12 rule)."""
-        rt, eng = self.rt, self.eng
-        c = A.shape[1]
-        G = rt.empty(c, c)
-        eng.gram(A, A, G)
-        perm = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
-        rinv = rt.zeros(c, c)
-        info = rt.zeros(3)
-        eng.pivchol(G, 1e-12, perm, rinv, info)
-        # speculate full rank: the second CholQR pass is issued before the
-        # host reads the rank, so the common case costs one round trip
-        B = eng.perm_rows(perm, rinv, info, rt.empty(c, c))
-        Y = eng.rowgemm(A, B, rt.empty(self.n, c))
-        G2 = rt.empty(c, c)
-        eng.gram(Y, Y, G2)
-        perm2 = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
-        rinv2 = rt.zeros(c, c)
-        info2 = rt.zeros(3)
-        eng.pivchol(G2, -1.0, perm2, rinv2, info2)
-        Q = eng.rowgemm(Y, rinv2, rt.empty(self.n, c))
-        info_h = self._fetch(info)[0]
-        r = int(info_h[0])
-        if info_h[2] == 0.0:
-            raise EmptyBasisError("all input columns are zero")
-        if r == 0:
-            raise EmptyBasisError("all input columns are numerically dependent")
-        if info_h[1] < 1e-6:
-            return self._gs_exact(A)
-        if r == c:
-            return Q
-        # rank-deficient input: the second pass on the r selected columns
-        Yr = Y[:, :r].contiguous()
-        G2 = rt.empty(r, r)
-        eng.gram(Yr, Yr, G2)
-        rinv2 = rt.zeros(r, r)
-        eng.pivchol(G2, -1.0, perm2, rinv2, info2)
-        return eng.rowgemm(Yr, rinv2, rt.empty(self.n, r))
-
-    def _gs_exact(self, A):
-        """Column-pivoted two-pass Gram-Schmidt on device primitives."""
-        rt, eng, n = self.rt, self.eng, self.n
-        c = A.shape[1]
-        work = rt.empty(n, c)
-        eng.rowgemm(A, self.ident[:c, :c], work)
-        G = rt.empty(c, c)
-        eng.gram(work, work, G)
-        norms = np.sqrt(np.maximum(np.diag(G.cpu().numpy()), 0.0))
-        thresh = 1e-12 * float(norms.max())
-        alive = list(range(c))
-        basis = rt.empty(n, c)
-        nb = 0
-        coef = rt.empty(c, c)
-        red = rt.zeros(2)
-        while alive:
-            eng.gram(work, work, G)
-            g = G.cpu().numpy()
-            nr = np.sqrt(np.maximum(np.array([g[j, j] for j in alive]), 0.0))
-            pick = int(np.argmax(nr))
-            if nr[pick] <= thresh:
-                break
-            piv = alive.pop(pick)
-            q = rt.empty(n, 1)
-            eng.rowgemm(work[:, piv:piv + 1], self.ident[:1, :1], q)
-            if nb:
-                B = basis[:, :nb]
-                cv = coef.view(-1)[:nb].view(nb, 1)  # gram writes a contiguous block
-                eng.gram(B, q, cv)
-                eng.rowgemm(B, cv, q, alpha=-1.0, beta=1.0, Y0=q)
-            eng.dot_into(q.view(-1), q.view(-1), red)
-            nq = math.sqrt(float(red[0].item()))
-            if nq <= thresh:
-                continue
-            eng.rowgemm(q, self.ident[:1, :1], basis[:, nb:nb + 1], alpha=1.0 / nq)
-            qb = basis[:, nb:nb + 1]
-            nb += 1
-            for j in alive:
-                col = work[:, j:j + 1]
-                eng.gram(qb, col, coef[:1, :1])
-                eng.rowgemm(qb, coef[:1, :1], col, alpha=-1.0, beta=1.0, Y0=col)
-        if nb == 0:
-            raise EmptyBasisError("all input columns are numerically dependent")
-        out = rt.empty(n, nb)
-        eng.rowgemm(basis[:, :nb], self.ident[:nb, :nb], out)
-        return out
+        """symlin.orthonormalize (symlin.py:148-190) on the device."""
+        return orthonormalize_dev(self.eng, A)
 
     # ------------------------------------------------------------ cold start
     def cold_start(self) -> SolverState:
