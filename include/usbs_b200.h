@@ -248,6 +248,14 @@ usbs_status usbs_cons_compressed_rows(usbs_ctx* ctx, usbs_problem* p, const doub
 usbs_status usbs_gather(usbs_ctx* ctx, int64_t n, const int64_t* idx_dev, const double* src_dev,
                         double* dst_dev);
 
+/* dst[i, :k] = src[idx[i], :k] for i < n (dev, row-major, leading dimensions
+ * lds, ldd >= k); a zero row where idx[i] < 0.  warm_start_pad's embedding of
+ * the dual vectors, basis and primal factor into a larger problem
+ * (bundle.py:781-792: y[cmap] = prev.y, basis[vmap] = model.basis, ...),
+ * evaluated through the inverse map. */
+usbs_status usbs_gather_rows(usbs_ctx* ctx, int64_t n, int k, const int64_t* idx_dev, const double* src_dev,
+                             int64_t lds, double* dst_dev, int64_t ldd);
+
 /* ---- rounding -------------------------------------- */
 /* maxcut_round (rounding.py:34-51): for every column j of the factor U
  * (n x r, dev, row-major, ld >= r, r <= 64) the cut value of

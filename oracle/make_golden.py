@@ -22,6 +22,8 @@ Fixtures:
   traj_*.npz         per-iteration solve() trajectories of small problems
   lockstep_c1.npz    C1 state snapshot at t=10 and reference iteration 11
   rounding.npz       maxcut_round / qap_round (rounding.py) on seeded factors
+  state.npz          USBS v1 state-file bytes (save_state) of solved states,
+                     warm_start_pad outputs and the warm-started trajectory
 """
 from __future__ import annotations
 
@@ -355,12 +357,52 @@ def rounding_cases():
     np.savez_compressed(OUT / "rounding.npz", **data)
 
 
+def state_cases():
+    """save_state bytes (bundle.py:578-622) of solved states, warm_start_pad
+    (bundle.py:754-817) into a graph with one more vertex (the reference's
+    test_bundle.py:373-394 construction), and the solve warm-started from it."""
+    import tempfile
+    from conftest import make_k3, random_graph
+    data = {}
+
+    def state_bytes(st, prob):
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "s.bin")
+            sbb.save_state(path, st, prob)
+            return np.frombuffer(open(path, "rb").read(), dtype=np.uint8).copy()
+
+    k3p = sbp.build_maxcut(make_k3())
+    st, _ = sbb.solve(k3p, sbb.SolverConfig(eps=1e-3, max_iters=200, seed=0, sketch_rank=2))
+    data["k3_sketch/bin"] = state_bytes(st, k3p)
+    g_small = random_graph(9, 0.5, 60)
+    edges = list(zip(g_small.edges_u, g_small.edges_v, g_small.edges_w))
+    edges.append((0, 9, 1.0))
+    g_big = sbp.GraphInstance.from_edges(10, [(int(a), int(b), float(c)) for a, b, c in edges])
+    data["big/eu"], data["big/ev"], data["big/ew"] = g_big.edges_u, g_big.edges_v, g_big.edges_w
+    data["small/eu"], data["small/ev"], data["small/ew"] = g_small.edges_u, g_small.edges_v, g_small.edges_w
+    p_small, p_big = sbp.build_maxcut(g_small), sbp.build_maxcut(g_big)
+    for name, rank, seed in (("dense", 0, None), ("sketch", 3, 5)):
+        cfg = sbb.SolverConfig(k_c=4, k_p=1, eps=1e-3, max_iters=500, seed=0, sketch_rank=rank)
+        st, _ = sbb.solve(p_small, cfg)
+        data[f"{name}/bin"] = state_bytes(st, p_small)
+        padded = sbb.warm_start_pad(st, p_big, sbb.Mapping(np.arange(9), np.arange(9)), sketch_seed=seed)
+        data[f"{name}/pad_bin"] = state_bytes(padded, p_big)
+        fs = []
+        cfg2 = sbb.SolverConfig(k_c=4, k_p=1, eps=1e-3, max_iters=500, seed=0, sketch_rank=rank)
+        st2, _ = sbb.solve(p_big, cfg2, init=padded, callback=lambda i: fs.append((i.f_y, i.step == "descent")))
+        data[f"{name}/warm_f"] = np.array([f for f, _ in fs])
+        data[f"{name}/warm_step"] = np.array([d for _, d in fs], dtype=np.int8)
+        data[f"{name}/warm_status"] = np.array([st2.status == "converged", st2.iterations, st2.descent_steps])
+        print(f"state {name}: warm {st2.status} in {st2.iterations} its")
+    np.savez_compressed(OUT / "state.npz", **data)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    which = sys.argv[1:] or ["builders", "quad", "lanczos", "ipm", "cons", "sketch", "traj", "lockstep", "rounding"]
+    which = sys.argv[1:] or ["builders", "quad", "lanczos", "ipm", "cons", "sketch", "traj", "lockstep", "rounding", "state"]
     fn = {"builders": builders, "quad": quad_oracle, "lanczos": lanczos_cases, "ipm": ipm_cases,
           "cons": cons_cases, "sketch": sketch_cases, "traj": trajectories, "lockstep": lockstep,
-          "rounding": rounding_cases}
+          "rounding": rounding_cases, "state": state_cases}
     for w in which:
         fn[w]()
         print("wrote", w)

@@ -10,7 +10,7 @@ host-side (``instances``) and bit-exact with the reference builders.
 Device modules import lazily so that the host layer (builders, errors) is
 usable without a GPU; the device path itself has no CPU fallback.
 """
-from .errors import ConditioningError, EmptyBasisError, NumericError, StepFailureError
+from .errors import ConditioningError, EmptyBasisError, FingerprintMismatch, NumericError, StepFailureError
 from .instances import (
     DiagonalFamily,
     EntryFamilies,
@@ -47,6 +47,14 @@ _LAZY = {
     "reconstruct": ("linalg", "reconstruct"),
     "device_constraints": ("constraints", "device_constraints"),
     "qap_round": ("rounding", "qap_round"),
+    "save_state": ("state", "save_state"),
+    "load_state": ("state", "load_state"),
+    "state_from_record": ("state", "state_from_record"),
+    "record_to_state": ("state", "record_to_state"),
+    "warm_start_pad": ("state", "warm_start_pad"),
+    "fingerprint_of": ("state", "fingerprint_of"),
+    "Mapping": ("state", "Mapping"),
+    "StateRecord": ("state", "StateRecord"),
 }
 
 

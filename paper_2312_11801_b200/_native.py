@@ -64,6 +64,7 @@ PROTOS = {
     "usbs_pivchol": (_i32, [_p, _i32, _p, C.c_double, _p, _p, _p]),
     "usbs_svec": (_i32, [_p, _i32, _p, C.c_double, _p]),
     "usbs_gather": (_i32, [_p, _i64, _p, _p, _p]),
+    "usbs_gather_rows": (_i32, [_p, _i64, _i32, _p, _p, _i64, _p, _i64]),
     "usbs_cons_adjoint_apply": (_i32, [_p, _p, _p, _p, _i64, _i32, _p, _i64, _p]),
     "usbs_cons_adjoint_values": (_i32, [_p, _p, _p, _p]),
     "usbs_problem_pattern": (_i32, [_p, _p, _p, _p]),

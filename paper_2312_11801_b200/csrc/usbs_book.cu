@@ -605,6 +605,20 @@ __global__ void k_gather(int64_t n, const int64_t* __restrict__ idx, const doubl
     dst[i] = src[idx[i]];
 }
 
+// dst[i, :k] = src[idx[i], :k] (row-major), a zero row where idx[i] < 0:
+// the embedding scatter of warm_start_pad (bundle.py:781-792) as a gather
+// through the inverse map
+__global__ void k_gather_rows(int64_t n, int k, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                              int64_t lds, double* __restrict__ dst, int64_t ldd) {
+  const int64_t tot = n * k;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = x / k;
+    const int j = (int)(x - i * k);
+    const int64_t s = idx[i];
+    dst[i * ldd + j] = s >= 0 ? src[s * lds + j] : 0.0;
+  }
+}
+
 // orthonormalize's first CholQR factor: B[perm[i], j] = Rinv[i, j] for
 // i, j < r (r = info[0], the pivoted Cholesky rank), zero elsewhere
 __global__ void k_perm_rows(int c, const int* __restrict__ perm, const double* __restrict__ rinv,
@@ -877,6 +891,17 @@ usbs_status usbs_gather(usbs_ctx* ctx, int64_t n, const int64_t* idx, const doub
   if (n < 0) fail(USBS_ERR_SHAPE, "gather: n < 0");
   if (n > 0) {
     k_gather<<<nblocks(ctx, n), 256, 0, ctx->stream>>>(n, idx, src, dst);
+    check_launch(ctx);
+  }
+  USBS_API_END
+}
+
+usbs_status usbs_gather_rows(usbs_ctx* ctx, int64_t n, int k, const int64_t* idx, const double* src, int64_t lds,
+                             double* dst, int64_t ldd) {
+  USBS_API_BEGIN
+  if (n < 0 || k < 1 || lds < k || ldd < k) fail(USBS_ERR_SHAPE, "gather_rows: n >= 0, k >= 1, ld >= k");
+  if (n > 0) {
+    k_gather_rows<<<nblocks(ctx, n * k), 256, 0, ctx->stream>>>(n, k, idx, src, lds, dst, ldd);
     check_launch(ctx);
   }
   USBS_API_END

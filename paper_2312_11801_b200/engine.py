@@ -86,6 +86,13 @@ class Engine:
         check(self.lib.usbs_perm_rows(self.h, out.shape[0], _p(perm), _p(rinv), _p(info), _p(out)), "perm_rows")
         return out
 
+    def gather_rows(self, idx, src, out):
+        """out[i] = src[idx[i]] row-wise, zero rows where idx[i] < 0."""
+        k = out.shape[1]
+        check(self.lib.usbs_gather_rows(self.h, out.shape[0], k, _p(idx), _p(src), src.stride(0), _p(out),
+                                        out.stride(0)), "gather_rows")
+        return out
+
     def svec(self, A, out, scale=1.0):
         check(self.lib.usbs_svec(self.h, A.shape[0], _p(A), float(scale), _p(out)), "svec")
         return out

@@ -17,3 +17,7 @@ class EmptyBasisError(ValueError):
 
 class StepFailureError(RuntimeError):
     """No strictly feasible step length found above the minimum."""
+
+
+class FingerprintMismatch(RuntimeError):
+    """A serialized state does not belong to this problem (bundle.py:60-61)."""

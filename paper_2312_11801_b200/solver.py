@@ -14,6 +14,7 @@ Configuration objects are duck-typed: a reference ``SolverConfig`` (with
 """
 from __future__ import annotations
 
+import dataclasses
 import math
 import time
 from dataclasses import dataclass, field
@@ -247,6 +248,7 @@ class SolverState:
     scale_c: float = 1.0
     best_rel_infeas: float = np.inf
     best_rel_subopt: float = np.inf
+    device_problem: Optional[object] = field(default=None, repr=False, compare=False)
 
     @property
     def y(self) -> np.ndarray:
@@ -531,12 +533,13 @@ class DeviceSolver:
                            scale_x=float(self.prob.scale_x), scale_c=float(self.prob.scale_c))
 
     def state_from_arrays(self, y, nu, f_y, lam_y, basis, trace, cost_ip, image, xbar=None, sketch=None,
-                          descent=0, null=0, last_primal=None) -> SolverState:
+                          descent=0, null=0, last_primal=None, psi_seed=None) -> SolverState:
         """Device state from host arrays (a reference SolverState's fields or
         a loaded USBS state record), e.g. for warm starts and lock-step replay."""
         rt = self.rt
         if sketch is not None:
-            sketch_seed = int(np.random.SeedSequence(self.seed).generate_state(2)[0])
+            sketch_seed = (int(np.random.SeedSequence(self.seed).generate_state(2)[0]) if psi_seed is None
+                           else int(psi_seed))
             store = DeviceSketchStore(self.eng, self.n, sketch.shape[1], sketch_seed)
             store.P.copy_(rt.upload(sketch))
         elif xbar is not None:
@@ -792,5 +795,19 @@ class DeviceSolver:
 def solve(prob, cfg, init: Optional[SolverState] = None, callback: Optional[Callable] = None):
     """Drop-in for specbundle.solve (bundle.py:426-529): same arguments and
     return value (SolverState, PrimalOutput); arrays of the state live on the
-    GPU and convert to numpy on attribute access."""
-    return DeviceSolver(prob, cfg).solve(init=init, callback=callback)
+    GPU and convert to numpy on attribute access.  ``init`` may be a device
+    state (cold start, ``state.warm_start_pad`` / ``state_from_record``) or a
+    host one with the reference's attribute names; as in the reference, the
+    state's own k_c / k_p drive the iteration."""
+    dprob = None
+    if init is not None:
+        if not hasattr(init, "y_dev"):
+            from .state import state_from_host
+            init = state_from_host(init)
+        dp = getattr(init, "device_problem", None)
+        if dp is not None and dp.prob is prob:
+            dprob = dp
+        kc, kp = int(init.model.k_c), int(init.model.k_p)
+        if (kc, kp) != (min(cfg.k_c, int(prob.n)), min(cfg.k_p, int(prob.n) - min(cfg.k_c, int(prob.n)))):
+            cfg = dataclasses.replace(cfg, k_c=kc, k_p=kp)
+    return DeviceSolver(prob, cfg, dprob=dprob).solve(init=init, callback=callback)
