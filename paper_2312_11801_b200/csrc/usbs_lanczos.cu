@@ -585,6 +585,12 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
 // costs 3 cluster barriers (~0.2 us) instead of 3 grid barriers (~1.6 us)
 // and no L2 round trips for Q.  Breakdown exits spill Q to global so the
 // host can reseed exactly as in the grid variant.
+// leading dimension of the CTA's Q slice: R rounded up to 2 (mod 4), so
+// column reads with 128-bit loads (two rows per lane) are conflict-free for
+// lane = column (8 lanes cover all banks) and every column starts 16-byte
+// aligned; the padding rows stay zero
+__host__ __device__ inline int lz_ldq(int R) { return ((R + 1) & 3) == 2 ? R + 1 : R + 3; }
+
 template <int LG>
 __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -593,17 +599,18 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   const int tid = threadIdx.x, nth = blockDim.x, nw = nth >> 5, lane = tid & 31, warp = tid >> 5;
   const int b = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
   const int r0 = min(a.n, b * R), r1 = min(a.n, r0 + R), nloc = r1 - r0;
+  const int LDQ = lz_ldq(R), npair = (nloc + 1) >> 1;
 
-  double* Qs = (double*)smem_raw;   // M1 * R, column-major (ld R), local rows
-  double* W0s = Qs + (size_t)M1 * R;  // R
-  double* W1s = W0s + R;             // R
+  double* Qs = (double*)smem_raw;   // M1 * LDQ, column-major (ld LDQ), local rows
+  double* W0s = Qs + (size_t)M1 * LDQ;  // LDQ
+  double* W1s = W0s + LDQ;           // LDQ
   // partial-sum exchange: every CTA pushes its 32 column partials (and its
   // ||w''||^2 share) into slot [rank] of EVERY CTA's buffer before the
   // barrier, so the sums after it are local, fixed-order reads
-  double* XA = W1s + R;              // 16 * 32  Q^T w partials
+  double* XA = W1s + LDQ;              // 16 * 32  Q^T w partials
   double* XB = XA + 16 * 32;         // 16 * 32  Q^T w' partials
-  double* XC = XB + 16 * 32;         // 16       ||w''||^2 partials
-  double* wred = XC + 16;            // nw * 32
+  double* XC = XB + 16 * 32;         // 16 * 16  ||w''||^2 partials (CTA, warp)
+  double* wred = XC + 16 * 16;       // nw * 32  (also each warp's copy of c / c')
   double* cvec = wred + nw * 32;     // 64
   double* c2vec = cvec + 64;         // 64
   double* red = c2vec + 64;          // 64
@@ -626,29 +633,62 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   const unsigned rmagic = (unsigned)((0x100000000ull + (unsigned)R - 1) / (unsigned)R);
 
   // sum over the own rows of Q[:, lane] * x for lane <= j: warp w takes a
-  // contiguous block of rows, four independent FMA chains (R is odd, so the
-  // 32 lanes' column reads are bank-conflict free)
+  // contiguous block of row pairs, 128-bit loads (LDQ = 2 mod 4: the 32
+  // lanes' column reads are bank-conflict free), four independent FMA chains
   auto colsum = [&](const double* x, int j) -> double {
-    const int rpw = (nloc + nw - 1) / nw;
-    const int i0 = min(nloc, warp * rpw), i1 = min(nloc, i0 + rpw);
+    const int ppw = (npair + nw - 1) / nw;
+    const int p0 = min(npair, warp * ppw), p1 = min(npair, p0 + ppw);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (lane <= j) {
-      const double* qc = Qs + (size_t)lane * R;
-      int i = i0;
-      for (; i + 3 < i1; i += 4) {
-        a0 = fma(qc[i], x[i], a0);
-        a1 = fma(qc[i + 1], x[i + 1], a1);
-        a2 = fma(qc[i + 2], x[i + 2], a2);
-        a3 = fma(qc[i + 3], x[i + 3], a3);
+      const double2* qc = reinterpret_cast<const double2*>(Qs + (size_t)lane * LDQ);
+      const double2* x2 = reinterpret_cast<const double2*>(x);
+      int p = p0;
+      for (; p + 1 < p1; p += 2) {
+        const double2 q0 = qc[p], q1 = qc[p + 1], y0 = x2[p], y1 = x2[p + 1];
+        a0 = fma(q0.x, y0.x, a0);
+        a1 = fma(q0.y, y0.y, a1);
+        a2 = fma(q1.x, y1.x, a2);
+        a3 = fma(q1.y, y1.y, a3);
       }
-      for (; i < i1; ++i) a0 = fma(qc[i], x[i], a0);
+      if (p < p1) {
+        const double2 q0 = qc[p], y0 = x2[p];
+        a0 = fma(q0.x, y0.x, a0);
+        a1 = fma(q0.y, y0.y, a1);
+      }
     }
     return (a0 + a1) + (a2 + a3);
+  };
+  // (Q c)[rows 2pp, 2pp+1] over columns 0..j (c in smem, broadcast within the
+  // warp): columns in chunks of eight whose loads are all issued before the
+  // chunk's FMAs (a branch per chunk, not per column); c is zero above j
+  // (the column sums of unused columns are zero), so the chunk's tail
+  // columns add exact zeros
+  auto pair_sub = [&](int pp, const double* cv, int j) -> double2 {
+    const double2* q2 = reinterpret_cast<const double2*>(Qs) + pp;
+    const int ld2 = LDQ >> 1;
+    double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+    for (int t0 = 0; t0 <= j; t0 += 8) {
+      double2 q[8];
+      double c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        q[u] = q2[(t0 + u) * ld2];
+        c[u] = cv[t0 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        s0 = fma(q[u].x, c[u], s0);
+        s1 = fma(q[u].y, c[u], s1);
+        u0 = fma(q[u + 1].x, c[u + 1], u0);
+        u1 = fma(q[u + 1].y, c[u + 1], u1);
+      }
+    }
+    return make_double2(s0 + u0, s1 + u1);
   };
   // row il of Q (m <= 32 columns) into registers, and its product with Y[:, u]
   auto load_qrow = [&](int il, double (&q)[32]) {
 #pragma unroll
-    for (int t = 0; t < 32; ++t) q[t] = t < m ? Qs[(size_t)t * R + il] : 0.0;
+    for (int t = 0; t < 32; ++t) q[t] = t < m ? Qs[(size_t)t * LDQ + il] : 0.0;
   };
   auto qrow_dot = [&](const double (&q)[32], int u) -> double {
     double s0 = 0.0, s1 = 0.0;
@@ -660,10 +700,13 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
     return s0 + s1;
   };
 
-  // Q for the own rows from global (start vector / restart state / reseed)
+  // Q for the own rows from global (start vector / restart state / reseed);
+  // the padding rows of Q and of both w buffers are zero for good
+  for (int x = tid; x < (M1 + 2) * LDQ; x += nth) Qs[x] = 0.0;
+  __syncthreads();
   for (int x = tid; x < M1 * nloc; x += nth) {
     const int t = x / nloc, i = x % nloc;
-    Qs[(size_t)t * R + i] = a.Q[qidx(r0 + i, t, M1)];
+    Qs[(size_t)t * LDQ + i] = a.Q[qidx(r0 + i, t, M1)];
   }
   for (int i = tid; i <= nloc; i += nth) rp[i] = a.rowptr[r0 + i];
   __syncthreads();
@@ -698,10 +741,10 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
       double* Wprev = wb ? W1s : W0s;
       double* Wcur = wb ? W0s : W1s;
       // ------------------------------------------------------------ phase A
-      const double* xloc = from_q ? Qs + (size_t)j * R : Wprev;
+      const double* xloc = from_q ? Qs + (size_t)j * LDQ : Wprev;
       const double xs = from_q ? 1.0 : 1.0 / beta;
       if (!from_q) {
-        for (int i = tid; i < nloc; i += nth) Qs[(size_t)j * R + i] = Wprev[i] * xs;
+        for (int i = tid; i < nloc; i += nth) Qs[(size_t)j * LDQ + i] = Wprev[i] * xs;
         if (b == 0 && tid == 0) {
           a.H[j * M1 + (j - 1)] = beta;
           a.H[(j - 1) * M1 + j] = beta;
@@ -796,14 +839,12 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
       cluster.sync();
       LZ_MARK(1);
       // ------------------------------------------------------------ phase B
-      if (warp == 0) {  // c = sum over CTAs in rank order (identical everywhere)
-        double s = 0.0;
-        for (int src = 0; src < CS; ++src) s += XA[src * 32 + lane];
-        cvec[lane] = s;
-      }
-      __syncthreads();
+      // c = sum over CTAs in rank order, formed by every warp (identical
+      // everywhere, no block barrier); the warp's copy goes to its wred row
+      double cl = 0.0;
+      for (int src = 0; src < CS; ++src) cl += XA[src * 32 + lane];
       // a non-finite w entry makes every column sum non-finite (inf * 0 = NaN)
-      if (!isfinite(cvec[0])) {
+      if (!isfinite(__shfl_sync(0xffffffffu, cl, 0))) {
         if (b == 0 && tid == 0) {
           atomicOr(&a.flags[F_NONFINITE], 1);
           a.flags[F_EXIT] = EXIT_NONFINITE;
@@ -812,17 +853,18 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
         cluster.sync();
         return;
       }
+      double* cw = wred + warp * 32;
+      cw[lane] = cl;
+      __syncwarp();
       {
-        // w' = w - Q c (lane = row), then partial Q^T w' (lane = column)
-        for (int il = tid; il < nloc; il += nth) {
-          double s0 = 0.0, s1 = 0.0;
-          int t = 0;
-          for (; t + 1 <= j; t += 2) {
-            s0 = fma(Qs[(size_t)t * R + il], cvec[t], s0);
-            s1 = fma(Qs[(size_t)(t + 1) * R + il], cvec[t + 1], s1);
-          }
-          if (t <= j) s0 = fma(Qs[(size_t)t * R + il], cvec[t], s0);
-          Wcur[il] -= s0 + s1;
+        // w' = w - Q c (lane = row pair), then partial Q^T w' (lane = column)
+        for (int pp = tid; pp < npair; pp += nth) {
+          const double2 qc = pair_sub(pp, cw, j);
+          double2* w2 = reinterpret_cast<double2*>(Wcur) + pp;
+          double2 w = *w2;
+          w.x -= qc.x;
+          w.y -= qc.y;
+          *w2 = w;
         }
         __syncthreads();
         const double acc = colsum(Wcur, j);
@@ -838,57 +880,50 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
       cluster.sync();
       LZ_MARK(1);
       // ------------------------------------------------------------ phase C
-      if (warp == 0) {
-        double s = 0.0;
-        for (int src = 0; src < CS; ++src) s += XB[src * 32 + lane];
-        c2vec[lane] = s;
-        // H column j = c + c' and the breakdown scale max(1, max|c + c'|)
-        const double ct = cvec[lane] + s;
-        cvec[lane] = ct;
-        const double mx = warp_max(lane <= j ? fabs(ct) : 0.0);
-        if (lane == 0) misc[0] = fmax(1.0, mx);
-      }
-      __syncthreads();
+      // c' per warp as above; H column j = c + c' and the breakdown scale
+      // max(1, max |c + c'|) in registers
+      double c2l = 0.0;
+      for (int src = 0; src < CS; ++src) c2l += XB[src * 32 + lane];
+      const double ctl = cl + c2l;
+      const double scale = fmax(1.0, warp_max(lane <= j ? fabs(ctl) : 0.0));
+      cw[lane] = c2l;
+      __syncwarp();
       {
         double ss = 0.0;
-        for (int il = tid; il < nloc; il += nth) {
-          double s0 = 0.0, s1 = 0.0;
-          int t = 0;
-          for (; t + 1 <= j; t += 2) {
-            s0 = fma(Qs[(size_t)t * R + il], c2vec[t], s0);
-            s1 = fma(Qs[(size_t)(t + 1) * R + il], c2vec[t + 1], s1);
-          }
-          if (t <= j) s0 = fma(Qs[(size_t)t * R + il], c2vec[t], s0);
-          const double w = Wcur[il] - (s0 + s1);
-          Wcur[il] = w;
-          ss = fma(w, w, ss);
+        for (int pp = tid; pp < npair; pp += nth) {
+          const double2 qc = pair_sub(pp, cw, j);
+          double2* w2 = reinterpret_cast<double2*>(Wcur) + pp;
+          double2 w = *w2;
+          w.x -= qc.x;
+          w.y -= qc.y;
+          *w2 = w;
+          ss = fma(w.x, w.x, ss);
+          ss = fma(w.y, w.y, ss);
         }
-        ss = block_sum(ss, red);
-        if (tid < CS) cluster.map_shared_rank(XC, tid)[b] = ss;
+        // warp partials straight into slot [rank][warp] of every CTA
+        ss = warp_sum(ss);
+        if (lane < CS) cluster.map_shared_rank(XC, lane)[b * nw + warp] = ss;
       }
-      if (b == 0)
-        for (int t = tid; t <= j; t += nth) {
-          a.H[t * M1 + j] = cvec[t];
-          a.H[j * M1 + t] = cvec[t];
-        }
+      if (b == 0 && warp == 0 && lane <= j) {
+        a.H[lane * M1 + j] = ctl;
+        a.H[j * M1 + lane] = ctl;
+      }
       LZ_MARK(3);
       cluster.sync();
       LZ_MARK(1);
-      if (warp == 0) {
-        double s = lane < CS ? XC[lane] : 0.0;
-        s = warp_sum(s);
-        if (lane == 0) misc[1] = sqrt(s);
+      {
+        const int nx = CS * nw;
+        double s = 0.0;
+        for (int x = lane; x < nx; x += 32) s += XC[x];
+        beta = sqrt(warp_sum(s));
       }
-      __syncthreads();
-      beta = misc[1];
-      const double scale = misc[0];
       wb ^= 1;
       from_q = false;
       if (beta <= 1e-13 * scale) {
         // spill Q for the host reseed (the host uses columns 0..j)
         for (int x = tid; x < M1 * nloc; x += nth) {
           const int t = x / nloc, i = x % nloc;
-          a.Q[qidx(r0 + i, t, M1)] = Qs[(size_t)t * R + i];
+          a.Q[qidx(r0 + i, t, M1)] = Qs[(size_t)t * LDQ + i];
         }
         if (b == 0 && tid == 0) {
           a.flags[F_EXIT] = EXIT_BREAKDOWN;
@@ -912,7 +947,7 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
     if (pending) {
       double* Wprev = wb ? W1s : W0s;
       const double xs = 1.0 / beta;
-      for (int i = tid; i < nloc; i += nth) Qs[(size_t)m * R + i] = Wprev[i] * xs;
+      for (int i = tid; i < nloc; i += nth) Qs[(size_t)m * LDQ + i] = Wprev[i] * xs;
       if (b == 0 && tid == 0) {
         a.H[m * M1 + (m - 1)] = beta;
         a.H[(m - 1) * M1 + m] = beta;
@@ -951,8 +986,8 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
     for (int il = tid; il < nloc; il += nth) {
       double qrow[32];
       load_qrow(il, qrow);
-      for (int u = 0; u < ell; ++u) Qs[(size_t)u * R + il] = qrow_dot(qrow, u);
-      Qs[(size_t)ell * R + il] = Qs[(size_t)m * R + il];
+      for (int u = 0; u < ell; ++u) Qs[(size_t)u * LDQ + il] = qrow_dot(qrow, u);
+      Qs[(size_t)ell * LDQ + il] = Qs[(size_t)m * LDQ + il];
     }
     __syncthreads();  // Ys (the restart's Y) is read; the operand cache may return
     load_cache();
@@ -986,8 +1021,8 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
 }
 
 static size_t lz_cl_smem(int m, int R, int nth) {
-  const int M1 = m + 1, nw = nth / 32;
-  return (size_t)((size_t)M1 * R + 2 * R + 16 * 32 * 2 + 16 + nw * 32 + 64 * 3 + 8 + 64 + 4 * m * m + 6 * 64) *
+  const int M1 = m + 1, nw = nth / 32, LDQ = lz_ldq(R);
+  return (size_t)((size_t)M1 * LDQ + 2 * LDQ + 16 * 32 * 2 + 16 * 16 + nw * 32 + 64 * 3 + 8 + 64 + 4 * m * m + 6 * 64) *
              sizeof(double) + (128 + R + 1) * sizeof(int) + 64;
 }
 

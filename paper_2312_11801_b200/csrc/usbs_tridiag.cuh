@@ -95,27 +95,49 @@ __device__ __forceinline__ void pow2_rescale(double& p, double& pm) {
 __device__ inline int sturm_arrow(int N, int ell, const double* d, const double* sq, double sigma, double pivmin) {
   int cnt = 0;
   double pa = 1.0, pb = 0.0;
-  for (int k = 0; k < ell; ++k) {
-    double f = d[k] - sigma;
+  // rows in blocks of four with the block's d / sq loaded up front, so the
+  // shared-memory latency stays off the dependent FMA chain; the power-of-two
+  // rescale falls on every block's last row
+  auto arrow_row = [&](double f, double s2) {
     if (fabs(f) < pivmin) f = -pivmin;
     cnt += f < 0.0;
-    pb = fma(pb, f, sq[k] * pa);
+    pb = fma(pb, f, s2 * pa);
     pa *= f;
-    if ((k & 3) == 3) pow2_rescale(pa, pb);
+  };
+  int k = 0;
+  for (; k + 3 < ell; k += 4) {
+    const double f0 = d[k] - sigma, f1 = d[k + 1] - sigma, f2 = d[k + 2] - sigma, f3 = d[k + 3] - sigma;
+    const double q0 = sq[k], q1 = sq[k + 1], q2 = sq[k + 2], q3 = sq[k + 3];
+    arrow_row(f0, q0);
+    arrow_row(f1, q1);
+    arrow_row(f2, q2);
+    arrow_row(f3, q3);
+    pow2_rescale(pa, pb);
   }
+  for (; k < ell; ++k) arrow_row(d[k] - sigma, sq[k]);
   double pm = pa;
   double p = fma(d[ell] - sigma, pa, -pb);
   if (fabs(p) < pivmin * fabs(pm)) p = -pivmin * pm;
   cnt += (p < 0.0) != (pm < 0.0);
   pow2_rescale(p, pm);
-  for (int i = ell + 1; i < N; ++i) {
-    double pn = fma(d[i] - sigma, p, -sq[i - 1] * pm);
+  auto tri_row = [&](double f, double s2) {
+    double pn = fma(f, p, -s2 * pm);
     if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;
     cnt += (pn < 0.0) != (p < 0.0);
     pm = p;
     p = pn;
-    if (((i - ell) & 3) == 0) pow2_rescale(p, pm);
+  };
+  int i = ell + 1;
+  for (; i + 3 < N; i += 4) {
+    const double f0 = d[i] - sigma, f1 = d[i + 1] - sigma, f2 = d[i + 2] - sigma, f3 = d[i + 3] - sigma;
+    const double q0 = sq[i - 1], q1 = sq[i], q2 = sq[i + 1], q3 = sq[i + 2];
+    tri_row(f0, q0);
+    tri_row(f1, q1);
+    tri_row(f2, q2);
+    tri_row(f3, q3);
+    pow2_rescale(p, pm);  // row i + 3 = ell + 4 (mod 4)
   }
+  for (; i < N; ++i) tri_row(d[i] - sigma, sq[i - 1]);
   return cnt;
 }
 
@@ -228,15 +250,15 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
     // columns still to come are mu * b_c (scaled by each swap), A_ell at
     // column ell and mu * e_ell at column ell + 1
     double mu = 1.0, aell = s.dd[ell] - lam;
-    for (int k = 0; k < ell; ++k) {
-      const double D = s.dd[k] - lam, ak = mu * s.v[k];
+    auto arrow_col = [&](int k, double dk, double vk) {
+      const double D = dk - lam, ak = mu * vk;
       if (fabs(D) >= fabs(ak)) {
         const double piv = (fabs(D) < tiny) ? copysign(tiny, D == 0.0 ? 1.0 : D) : D;
         const double g = fast_rcp(piv);
         const double l = ak * g;
         U0[k * nw + j] = g;
         LM[k * nw + j] = l;
-        aell = fma(-l, s.v[k], aell);
+        aell = fma(-l, vk, aell);
       } else {
         const double g = fast_rcp(ak);
         const double l = D * g;
@@ -245,14 +267,23 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
         U1[k * nw + j] = aell;
         swp |= 1ull << k;
         mu = -l * mu;
-        aell = fma(-l, aell, s.v[k]);
+        aell = fma(-l, aell, vk);
       }
+    };
+    {
+      int k = 0;
+      for (; k + 3 < ell; k += 4) {
+        const double d0 = s.dd[k], d1 = s.dd[k + 1], d2 = s.dd[k + 2], d3 = s.dd[k + 3];
+        const double v0 = s.v[k], v1 = s.v[k + 1], v2 = s.v[k + 2], v3 = s.v[k + 3];
+        arrow_col(k, d0, v0);
+        arrow_col(k + 1, d1, v1);
+        arrow_col(k + 2, d2, v2);
+        arrow_col(k + 3, d3, v3);
+      }
+      for (; k < ell; ++k) arrow_col(k, s.dd[k], s.v[k]);
     }
     double a0 = aell, c0 = (ell + 1 < N) ? mu * s.ee[ell] : 0.0;
-    for (int i = ell; i < N - 1; ++i) {
-      const double bsub = s.ee[i];
-      const double dn = s.dd[i + 1] - lam;
-      const double cn = (i + 2 < N) ? s.ee[i + 1] : 0.0;
+    auto tri_col = [&](int i, double bsub, double dn, double cn) {
       if (fabs(a0) >= fabs(bsub)) {
         const double piv = (fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0;
         const double rp = fast_rcp(piv);
@@ -272,6 +303,21 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
         a0 = c0 - l * dn;
         c0 = -l * cn;
       }
+    };
+    {
+      int i = ell;
+      for (; i + 3 < N - 1; i += 4) {
+        double b4[4], d4[4], c4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          b4[u] = s.ee[i + u];
+          d4[u] = s.dd[i + u + 1] - lam;
+          c4[u] = (i + u + 2 < N) ? s.ee[i + u + 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tri_col(i + u, b4[u], d4[u], c4[u]);
+      }
+      for (; i < N - 1; ++i) tri_col(i, s.ee[i], s.dd[i + 1] - lam, (i + 2 < N) ? s.ee[i + 1] : 0.0);
     }
     U0[(N - 1) * nw + j] = fast_rcp((fabs(a0) < tiny) ? copysign(tiny, a0 == 0.0 ? 1.0 : a0) : a0);
     // deterministic pseudo-random start vector in (-0.5, 0.5)
@@ -286,58 +332,137 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
   for (int iter = 0; iter < 2; ++iter) {
     if (tid < nw) {
       const int j = tid;
+      // the sweeps below go in blocks of four rows whose operands are loaded
+      // into registers before any of the block's stores, so the shared-memory
+      // latency overlaps the dependent chain (same arithmetic, same order)
       // arrow forward (row k keeps its rhs, or takes the arrow's on a swap)
       double t = Z[ell * nw + j];
-      for (int k = 0; k < ell; ++k) {
-        const double l = LM[k * nw + j], zk = Z[k * nw + j];
-        if ((swp >> k) & 1ull) {
-          Z[k * nw + j] = t;
-          t = fma(-l, t, zk);
-        } else {
-          t = fma(-l, zk, t);
+      {
+        int k = 0;
+        for (; k + 3 < ell; k += 4) {
+          double l4[4], z4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            l4[u] = LM[(k + u) * nw + j];
+            z4[u] = Z[(k + u) * nw + j];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if ((swp >> (k + u)) & 1ull) {
+              Z[(k + u) * nw + j] = t;
+              t = fma(-l4[u], t, z4[u]);
+            } else {
+              t = fma(-l4[u], z4[u], t);
+            }
+          }
+        }
+        for (; k < ell; ++k) {
+          const double l = LM[k * nw + j], zk = Z[k * nw + j];
+          if ((swp >> k) & 1ull) {
+            Z[k * nw + j] = t;
+            t = fma(-l, t, zk);
+          } else {
+            t = fma(-l, zk, t);
+          }
         }
       }
       // tridiagonal forward: L^-1 with the recorded swaps (z_i carried)
       double zi = t;
-      for (int i = ell; i < N - 1; ++i) {
-        const double zn = Z[(i + 1) * nw + j], l = LM[i * nw + j];
-        if ((swp >> i) & 1ull) {
-          Z[i * nw + j] = zn;
-          zi = fma(-l, zn, zi);
-        } else {
-          Z[i * nw + j] = zi;
-          zi = fma(-l, zi, zn);
+      {
+        int i = ell;
+        for (; i + 3 < N - 1; i += 4) {
+          double l4[4], n4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            n4[u] = Z[(i + u + 1) * nw + j];
+            l4[u] = LM[(i + u) * nw + j];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if ((swp >> (i + u)) & 1ull) {
+              Z[(i + u) * nw + j] = n4[u];
+              zi = fma(-l4[u], n4[u], zi);
+            } else {
+              Z[(i + u) * nw + j] = zi;
+              zi = fma(-l4[u], zi, n4[u]);
+            }
+          }
+        }
+        for (; i < N - 1; ++i) {
+          const double zn = Z[(i + 1) * nw + j], l = LM[i * nw + j];
+          if ((swp >> i) & 1ull) {
+            Z[i * nw + j] = zn;
+            zi = fma(-l, zn, zi);
+          } else {
+            Z[i * nw + j] = zi;
+            zi = fma(-l, zi, zn);
+          }
         }
       }
       Z[(N - 1) * nw + j] = zi;
       // backward: U z = y  (U row i: 1/U0, U1, and e_{i+1} after a swap)
       double z1 = 0.0, z2 = 0.0;
-      for (int i = N - 1; i >= ell; --i) {
-        double tt = Z[i * nw + j];
-        if (i + 1 < N) tt -= U1[i * nw + j] * z1;
-        if (i + 2 < N && ((swp >> i) & 1ull)) tt -= s.ee[i + 1] * z2;
-        const double zi = tt * U0[i * nw + j];
-        Z[i * nw + j] = zi;
-        z2 = z1;
-        z1 = zi;
+      {
+        auto brow = [&](int i, double tt, double u1, double u0, double e1) {
+          if (i + 1 < N) tt -= u1 * z1;
+          if (i + 2 < N && ((swp >> i) & 1ull)) tt -= e1 * z2;
+          const double zz = tt * u0;
+          Z[i * nw + j] = zz;
+          z2 = z1;
+          z1 = zz;
+        };
+        int i = N - 1;
+        for (; i - 3 >= ell; i -= 4) {
+          double t4[4], a4[4], b4[4], e4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int r = i - u;
+            t4[u] = Z[r * nw + j];
+            a4[u] = U1[r * nw + j];
+            b4[u] = U0[r * nw + j];
+            e4[u] = (r + 2 < N) ? s.ee[r + 1] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) brow(i - u, t4[u], a4[u], b4[u], e4[u]);
+        }
+        for (; i >= ell; --i) brow(i, Z[i * nw + j], U1[i * nw + j], U0[i * nw + j], (i + 2 < N) ? s.ee[i + 1] : 0.0);
       }
       // arrow back-substitution; S = sum_{k < c < ell} b_c z_c for the
       // swapped (dense) rows
       const double zl = Z[ell * nw + j], zl1 = (ell + 1 < N) ? Z[(ell + 1) * nw + j] : 0.0;
       double S = 0.0;
-      for (int k = ell - 1; k >= 0; --k) {
-        const double g = U0[k * nw + j], rk = Z[k * nw + j];
-        double y;
-        if ((swp >> k) & 1ull)
-          y = fma(rk - U1[k * nw + j] * zl, g, -(S + s.ee[ell] * zl1) * fast_rcp(s.v[k]));
-        else
-          y = fma(-s.v[k], zl, rk) * g;
-        Z[k * nw + j] = y;
-        S = fma(s.v[k], y, S);
+      {
+        const double eel = s.ee[ell];
+        auto arow = [&](int k, double g, double rk, double vk, double u1) {
+          double y;
+          if ((swp >> k) & 1ull)
+            y = fma(rk - u1 * zl, g, -(S + eel * zl1) * fast_rcp(vk));
+          else
+            y = fma(-vk, zl, rk) * g;
+          Z[k * nw + j] = y;
+          S = fma(vk, y, S);
+        };
+        int k = ell - 1;
+        for (; k - 3 >= 0; k -= 4) {
+          double g4[4], r4[4], v4[4], u4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int r = k - u;
+            g4[u] = U0[r * nw + j];
+            r4[u] = Z[r * nw + j];
+            v4[u] = s.v[r];
+            u4[u] = U1[r * nw + j];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) arow(k - u, g4[u], r4[u], v4[u], u4[u]);
+        }
+        for (; k >= 0; --k) arow(k, U0[k * nw + j], Z[k * nw + j], s.v[k], U1[k * nw + j]);
       }
       double nrm = 0.0;
+#pragma unroll 4
       for (int i = 0; i < N; ++i) nrm = fma(Z[i * nw + j], Z[i * nw + j], nrm);
       const double inv = nrm > 0.0 ? rsqrt(nrm) : 0.0;
+#pragma unroll 4
       for (int i = 0; i < N; ++i) Z[i * nw + j] *= inv;
     }
     __syncthreads();
@@ -364,8 +489,10 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
     if (tid < nw) {
       const int j = tid;
       double nrm = 0.0;
+#pragma unroll 4
       for (int i = 0; i < N; ++i) nrm = fma(Z[i * nw + j], Z[i * nw + j], nrm);
       const double inv = nrm > 0.0 ? rsqrt(nrm) : 0.0;
+#pragma unroll 4
       for (int i = 0; i < N; ++i) Z[i * nw + j] *= inv;
     }
     __syncthreads();
