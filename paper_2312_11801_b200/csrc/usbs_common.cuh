@@ -117,6 +117,7 @@ struct usbs_problem {
   // cached cluster-Lanczos plan (usbs_lanczos.cu): basis size it was made
   // for, cluster size (0 = grid kernel), rows per CTA, dynamic smem bytes
   int lz_cl_m = -1, lz_cl_cs = 0, lz_cl_R = 0, lz_cl_lg = 32;  // lg: SpMV lanes per row
+  int lz_cl_hmax = 0;  // halo slots per CTA (0: DSMEM gathers inside the SpMV)
   size_t lz_cl_smem = 0;
   int* blk_row = nullptr;
   int* blk_seg = nullptr;  // Lanczos block b's SpMV segments [blk_seg[b], blk_seg[b+1])

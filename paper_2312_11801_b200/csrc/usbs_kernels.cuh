@@ -17,6 +17,7 @@ enum WsSlot {
   WS_LZ_OUT = 16,
   WS_LZ_TMP = 17,
   WS_LZ_PROF = 18,
+  WS_LZ_HALO = 19,
   WS_SMALL = 20,
   WS_RED = 21,
   WS_IPM = 30,

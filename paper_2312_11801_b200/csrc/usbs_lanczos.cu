@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
 __host__ __device__ inline int lz_ldq(int R) { return ((R + 1) & 3) == 2 ? R + 1 : R + 3; }
 
 template <int LG>
-__global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
+__global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R, int hmax) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int m = a.m, M1 = m + 1;
@@ -611,10 +611,8 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   double* XB = XA + 16 * 32;         // 16 * 32  Q^T w' partials
   double* XC = XB + 16 * 32;         // 16 * 16  ||w''||^2 partials (CTA, warp)
   double* wred = XC + 16 * 16;       // nw * 32  (also each warp's copy of c / c')
-  double* cvec = wred + nw * 32;     // 64
-  double* c2vec = cvec + 64;         // 64
-  double* red = c2vec + 64;          // 64
-  double* misc = red + 64;           // 8
+  double* hval = wred + nw * 32;     // hmax  halo: remote x entries of this step
+  double* misc = hval + hmax;        // 8
   double* thetaS = misc + 8;         // 64
   double* Ys = thetaS + 64;          // m*m
   TriSmem ts;
@@ -629,6 +627,9 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   ts.red = ts.lam + 64;
   ts.iw = (int*)(ts.red + 64);
   int* rp = ts.iw + 128;  // R + 1 own row pointers
+  // halo slot h fetches x[li] from CTA owner: hsrc[h] = owner << 11 | li
+  unsigned short* hsrc = reinterpret_cast<unsigned short*>(rp + R + 1);
+  int* hcnt = reinterpret_cast<int*>(misc + 3);
   // c / R as a multiply-high: exact for c * R < 2^32 (host checks n * R)
   const unsigned rmagic = (unsigned)((0x100000000ull + (unsigned)R - 1) / (unsigned)R);
 
@@ -715,13 +716,37 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   // which is free between Rayleigh-Ritz calls; reloaded after each restart
   const int nz0 = rp[0], nnz_loc = rp[nloc] - nz0;
   const bool use_cache = LG == 1 && a.n <= 65536 && (int64_t)nnz_loc * 10 <= (int64_t)m * m * 32;
+  // halo mode (hmax > 0, cached operands): the step's remote x entries are
+  // fetched once into hval by all threads, and the cached column of a
+  // nonzero is its local index (own row) or nloc + its halo slot, so the
+  // SpMV itself reads only local shared memory
+  const bool use_halo = use_cache && hmax > 0;
+  int nhalo = 0;
   double* cv = Ys;
   unsigned short* cc = (unsigned short*)(Ys + nnz_loc);
   auto load_cache = [&]() {
     if (!use_cache) return;
+    if (use_halo) {
+      if (tid == 0) *hcnt = 0;
+      __syncthreads();
+    }
     for (int z = tid; z < nnz_loc; z += nth) {
+      const int c = a.col[nz0 + z];
       cv[z] = a.val[nz0 + z];
-      cc[z] = (unsigned short)a.col[nz0 + z];
+      if (!use_halo) {
+        cc[z] = (unsigned short)c;
+      } else if (c >= r0 && c < r1) {
+        cc[z] = (unsigned short)(c - r0);
+      } else {
+        const int h = atomicAdd(hcnt, 1);  // slot order is irrelevant: sums run in nonzero order
+        const int owner = (int)__umulhi((unsigned)c, rmagic);
+        hsrc[h] = (unsigned short)((owner << 11) | (c - owner * R));
+        cc[z] = (unsigned short)(nloc + h);
+      }
+    }
+    if (use_halo) {
+      __syncthreads();
+      nhalo = *hcnt;
     }
   };
   load_cache();
@@ -756,7 +781,25 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
         const double* src = owner == b ? xloc : cluster.map_shared_rank(xloc, owner);
         return src[li];
       };
-      if constexpr (LG == 1) {
+      if (use_halo) {
+        for (int h = tid; h < nhalo; h += nth) {
+          const unsigned sh = hsrc[h];
+          hval[h] = cluster.map_shared_rank(xloc, (int)(sh >> 11))[sh & 2047u];
+        }
+        __syncthreads();
+        // a thread per row; every operand in local shared memory (own row
+        // or halo slot), the products in nonzero order as in the gather path
+        for (int il = tid; il < nloc; il += nth) {
+          const int z1 = rp[il + 1] - nz0;
+          double acc = 0.0;
+          for (int z = rp[il] - nz0; z < z1; ++z) {
+            const int c = cc[z];
+            const double x = c < nloc ? xloc[c] : hval[c - nloc];
+            acc = fma(cv[z], x * xs, acc);
+          }
+          Wcur[il] = acc;
+        }
+      } else if constexpr (LG == 1) {
         // short rows: one thread per row, two rows in flight per thread and
         // the row's loads batched by U so the col -> gather chains overlap
         constexpr int U = 8;
@@ -1020,10 +1063,26 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R) {
   cluster.sync();  // keep smem alive until every remote read is done
 }
 
-static size_t lz_cl_smem(int m, int R, int nth) {
+static size_t lz_cl_smem(int m, int R, int nth, int hmax) {
   const int M1 = m + 1, nw = nth / 32, LDQ = lz_ldq(R);
-  return (size_t)((size_t)M1 * LDQ + 2 * LDQ + 16 * 32 * 2 + 16 * 16 + nw * 32 + 64 * 3 + 8 + 64 + 4 * m * m + 6 * 64) *
-             sizeof(double) + (128 + R + 1) * sizeof(int) + 64;
+  return (size_t)((size_t)M1 * LDQ + 2 * LDQ + 16 * 32 * 2 + 16 * 16 + nw * 32 + hmax + 8 + 64 + 4 * m * m + 6 * 64) *
+             sizeof(double) + (128 + R + 1) * sizeof(int) + ((2 * hmax + 7) & ~7) + 64;
+}
+
+// remote nonzeros of each CTA's row range (halo sizes of the cluster kernel)
+__global__ void k_halo_count(int n, int R, const int* __restrict__ rowptr, const int* __restrict__ col, int* out) {
+  __shared__ int tot;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  const int r0 = min(n, (int)blockIdx.x * R), r1 = min(n, r0 + R);
+  int cnt = 0;
+  for (int z = rowptr[r0] + threadIdx.x; z < rowptr[r1]; z += blockDim.x) {
+    const int c = col[z];
+    cnt += (c < r0 || c >= r1);
+  }
+  atomicAdd(&tot, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = tot;
 }
 
 // ------------------------------------------------------------ small kernels
@@ -1171,7 +1230,7 @@ static void lz_launch(usbs_ctx* ctx, LzArgs& a, int G, size_t smem) {
 
 // Cluster plan for the small-n variant: CS CTAs in one cluster, R rows each.
 struct LzClusterPlan {
-  int cs = 0, R = 0, lg = 32;
+  int cs = 0, R = 0, lg = 32, hmax = 0;
   size_t smem = 0;
 };
 
@@ -1214,7 +1273,8 @@ static int lz_cl_max_clusters_lg(int LG, int cs, size_t smem) {
 
 // Picks the largest cluster (16, else 8) whose per-CTA Q slice fits in shared
 // memory and that the device can schedule; cs = 0 means "use the grid kernel".
-static LzClusterPlan lz_cluster_plan(usbs_ctx* ctx, int64_t n, int64_t nnz, int m, int LG) {
+static LzClusterPlan lz_cluster_plan(usbs_ctx* ctx, usbs_problem* p, int m, int LG) {
+  const int64_t n = p->n, nnz = p->nnz;
   LzClusterPlan pl;
   // short rows (<= 16 nnz on average): thread per row; else the grid
   // kernel's group size
@@ -1228,13 +1288,28 @@ static LzClusterPlan lz_cluster_plan(usbs_ctx* ctx, int64_t n, int64_t nnz, int 
     const int64_t R = ((n + cs - 1) / cs) | 1;  // odd: conflict-free column reads
     if (R < 32) continue;  // tiny operators: one warp-row per CTA at least
     if (n * R >= (int64_t(1) << 32)) continue;  // owner = c / R by multiply-high
-    const size_t sm = lz_cl_smem(m, (int)R, 512);
+    size_t sm = lz_cl_smem(m, (int)R, 512, 0);
     if (sm > (size_t)optin) continue;
     if (lz_cl_max_clusters_lg(LG, cs, sm) < 1) continue;
     pl.cs = cs;
     pl.R = (int)R;
     pl.smem = sm;
     pl.lg = LG;
+    // halo SpMV when the largest per-CTA remote nonzero count fits
+    const char* eh = getenv("USBS_LZ_HALO");
+    if (LG == 1 && R < 2048 && n <= 65536 && !(eh && eh[0] == '0')) {
+      int* dcnt = (int*)ctx->ws.get(WS_LZ_HALO, 16 * sizeof(int));
+      k_halo_count<<<cs, 256, 0, ctx->stream>>>((int)n, (int)R, p->rowptr, p->col, dcnt);
+      USBS_CUDA(cudaMemcpyAsync(ctx->pinned_i, dcnt, cs * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      USBS_CUDA(cudaStreamSynchronize(ctx->stream));
+      int hmax = 0;
+      for (int b = 0; b < cs; ++b) hmax = std::max(hmax, ctx->pinned_i[b]);
+      const size_t smh = lz_cl_smem(m, (int)R, 512, std::max(hmax, 1));
+      if (hmax > 0 && smh <= (size_t)optin && lz_cl_max_clusters_lg(LG, cs, smh) >= 1) {
+        pl.hmax = hmax;
+        pl.smem = smh;
+      }
+    }
     return pl;
   }
   return pl;
@@ -1243,17 +1318,19 @@ static LzClusterPlan lz_cluster_plan(usbs_ctx* ctx, int64_t n, int64_t nnz, int 
 // plan cached per (problem, basis size)
 static LzClusterPlan lz_cached_plan(usbs_ctx* ctx, usbs_problem* p, int m) {
   if (p->lz_cl_m != m) {
-    const LzClusterPlan pl = lz_cluster_plan(ctx, p->n, p->nnz, m, p->spmv_group);
+    const LzClusterPlan pl = lz_cluster_plan(ctx, p, m, p->spmv_group);
     p->lz_cl_m = m;
     p->lz_cl_cs = pl.cs;
     p->lz_cl_R = pl.R;
     p->lz_cl_lg = pl.lg;
+    p->lz_cl_hmax = pl.hmax;
     p->lz_cl_smem = pl.smem;
   }
   LzClusterPlan pl;
   pl.cs = p->lz_cl_cs;
   pl.R = p->lz_cl_R;
   pl.lg = p->lz_cl_lg;
+  pl.hmax = p->lz_cl_hmax;
   pl.smem = p->lz_cl_smem;
   return pl;
 }
@@ -1272,7 +1349,7 @@ static void lz_cl_launch_t(usbs_ctx* ctx, LzArgs& a, const LzClusterPlan& pl) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  USBS_CUDA(cudaLaunchKernelEx(&cfg, k_lanczos_cl<LG>, a, pl.R));
+  USBS_CUDA(cudaLaunchKernelEx(&cfg, k_lanczos_cl<LG>, a, pl.R, pl.hmax));
   check_launch(ctx);
 }
 
