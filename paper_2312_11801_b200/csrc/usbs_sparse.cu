@@ -475,7 +475,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   {
     // rows (the CGS2 passes over Q): balanced on rows; the SpMV runs in its
     // own phase, so its segments are balanced separately on nonzeros
-    const double NNZCOST = 0.02;  // row loop bookkeeping per nonzero, in row units
+    const double NNZCOST = 0.0;  // the Q passes cost per row only (measured, C4)
     double total = (double)n + NNZCOST * (double)p->nnz;
     double acc = 0.0;
     int b = 0;
@@ -526,14 +526,24 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     p->lz_split_row = dev_upload(p, srow.data(), srow.size());
     p->lz_split_first = dev_upload(p, sfirst.data(), sfirst.size());
     p->lz_split_cnt = dev_upload(p, scnt.data(), scnt.size());
-    // contiguous segment ranges per block, balanced on nonzeros + 2 per row
+    // contiguous segment ranges per block, balanced on the measured cost of
+    // each row kind (least-squares fit of the C4 per-block timers, in units
+    // of a short-row nonzero): short rows (a thread per row) 1.0 per nonzero
+    // + 0.36 per row; rows of 33..128 nonzeros (a warp per row, lanes half
+    // idle) 1.5; longer rows 1.15; pieces of rows above LZT_NNZ (a block per
+    // piece) 0.74
     const int64_t ns = (int64_t)seg_r0.size();
     auto seg_cost = [&](int64_t e) -> double {
       if (seg_r1[e] < 0) {
         const int pc = -seg_r1[e] - 1;
-        return (double)(pz1[pc] - pz0[pc]);
+        return 0.74 * (double)(pz1[pc] - pz0[pc]);
       }
-      return (rp32[seg_r1[e]] - rp32[seg_r0[e]]) + 2.0 * (seg_r1[e] - seg_r0[e]);
+      double c = 0.0;
+      for (int32_t r = seg_r0[e]; r < seg_r1[e]; ++r) {
+        const int32_t len = rp32[r + 1] - rp32[r];
+        c += len <= 32 ? len + 0.36 : (len <= 128 ? 1.5 * len : 1.15 * len);
+      }
+      return c;
     };
     double stot = 0.0;
     for (int64_t e = 0; e < ns; ++e) stot += seg_cost(e);
