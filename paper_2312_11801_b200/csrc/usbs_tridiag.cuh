@@ -209,6 +209,24 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
   for (int j = warp; j < nw; j += nwp) {
     const int asc = N - 1 - j;  // ascending index of the j-th largest
     double lo = glo, hi = ghi;
+    if (j < ell) {
+      // after a thick restart the arrow's diagonal holds the kept Ritz values
+      // theta_0 >= theta_1 >= ..., the eigenvalues of a principal submatrix,
+      // so lambda_j >= theta_j (Cauchy interlacing); the first sweep puts its
+      // shifts at theta_j + |H| 10^(k/2 - 15), k = 0..30, and |H|'s upper
+      // bound, which brackets lambda_j within a factor 10^0.5 of its distance
+      // to theta_j (small once the Ritz values settle)
+      const double th = s.dd[j];
+      const double l0 = fmax(glo, th - 8.8e-16 * fabs(th) - pivmin);
+      const double sig = lane < 31 ? l0 + tnorm * exp10(0.5 * lane - 15.0) : ghi;
+      const int cnt0 = sturm_arrow(N, ell, s.dd, s.p, fmin(sig, ghi), pivmin);
+      const unsigned mask = __ballot_sync(0xffffffffu, cnt0 >= asc + 1);
+      const int first = mask ? __ffs(mask) - 1 : 31;
+      const double sf = __shfl_sync(0xffffffffu, fmin(sig, ghi), first);
+      const double sp = __shfl_sync(0xffffffffu, fmin(sig, ghi), first > 0 ? first - 1 : 0);
+      hi = sf;
+      lo = first > 0 ? sp : l0;
+    }
     for (int it = 0; it < 24; ++it) {
       if (hi - lo <= fmax(4.4e-16 * fmax(fabs(lo), fabs(hi)), 2.2e-16 * tnorm) + 1e-300) break;
       const double sig = lo + (hi - lo) * (double)(lane + 1) / 33.0;
