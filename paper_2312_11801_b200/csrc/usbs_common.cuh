@@ -166,6 +166,14 @@ inline void check_launch(usbs_ctx* c) {
 }
 
 // ---------------------------------------------------------------- device utils
+// D = A B + C on the FP64 tensor cores (mma.sync m8n8k4, row.col): lane l
+// holds a = A[l >> 2][l & 3], b = B[l & 3][l >> 2], c/d = C[l >> 2][2 (l & 3) + {0, 1}]
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

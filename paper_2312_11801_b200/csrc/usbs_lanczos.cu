@@ -1026,11 +1026,38 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R, int hmax
     if (misc[2] != 0.0) { converged = 1; break; }
     if (cycle == a.max_restarts) break;
     ell = ell_next;
-    for (int il = tid; il < nloc; il += nth) {
-      double qrow[32];
-      load_qrow(il, qrow);
-      for (int u = 0; u < ell; ++u) Qs[(size_t)u * LDQ + il] = qrow_dot(qrow, u);
-      Qs[(size_t)ell * LDQ + il] = Qs[(size_t)m * LDQ + il];
+    if (m == 32) {
+      // Q[:, :ell] <- Q Y[:, :ell] on the FP64 tensor cores: a warp per block
+      // of 8 rows, m8n8k4 over the 32 columns; the block's Q fragments are in
+      // registers before any of its outputs is stored (row i of the product
+      // depends on row i of Q only)
+      const int g = lane >> 2, q4 = lane & 3, nrb = (nloc + 7) >> 3, ntl = (ell + 7) >> 3;
+      for (int rbk = warp; rbk < nrb; rbk += nw) {
+        const int i0 = rbk * 8, r = i0 + g;
+        double af[8];
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc) af[kc] = Qs[(size_t)(kc * 4 + q4) * LDQ + r];
+        for (int nt2 = 0; nt2 < ntl; ++nt2) {
+          const int n0 = nt2 * 8;
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int kc = 0; kc < 8; ++kc) dmma_m8n8k4(d0, d1, af[kc], Ys[(kc * 4 + q4) * m + n0 + g], d0, d1);
+          const int c0 = n0 + 2 * q4;
+          if (r < nloc) {
+            if (c0 < ell) Qs[(size_t)c0 * LDQ + r] = d0;
+            if (c0 + 1 < ell) Qs[(size_t)(c0 + 1) * LDQ + r] = d1;
+          }
+        }
+      }
+      __syncthreads();  // column ell is an input of every row block above
+      for (int il = tid; il < nloc; il += nth) Qs[(size_t)ell * LDQ + il] = Qs[(size_t)m * LDQ + il];
+    } else {
+      for (int il = tid; il < nloc; il += nth) {
+        double qrow[32];
+        load_qrow(il, qrow);
+        for (int u = 0; u < ell; ++u) Qs[(size_t)u * LDQ + il] = qrow_dot(qrow, u);
+        Qs[(size_t)ell * LDQ + il] = Qs[(size_t)m * LDQ + il];
+      }
     }
     __syncthreads();  // Ys (the restart's Y) is read; the operand cache may return
     load_cache();
