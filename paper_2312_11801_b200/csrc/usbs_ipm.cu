@@ -216,42 +216,41 @@ __device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, doub
                : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
-// 8 x 8 diagonal block J by one warp: lane l owns entries (l >> 3, l & 7) and
-// (4 + (l >> 3), l & 7) (row i, column t, t <= i); per column the pivot and
-// the two column values each update needs arrive by shuffle, so the chain is
-// shfl -> rsqrt -> shfl -> fma.  Writes L and rdiag; lane 0 sets *flag.
+// 8 x 8 diagonal block J by one warp: lane r (< 8) holds row r of the block
+// in registers; per column c the pivot A(c, c) comes by shuffle from lane c,
+// the column is scaled by its rsqrt, and every row updates its entries
+// t <= r with L(t, c) shuffled from lane t (1.6 K cycles per block against
+// 2.3 K for a two-entries-per-lane layout, identical results;
+// profiles/mb/diag8_mb.cu).  Writes L and rdiag; lane 0 sets *flag.
 __device__ __forceinline__ void chol_diag8(double* __restrict__ Mp, int d, int J, double* __restrict__ rdiag,
                                            int* flag) {
   const int lane = threadIdx.x & 31;
   const int j0 = J * 8, jb = min(8, d - j0);
-  const int t = lane & 7, ia = lane >> 3, ib = 4 + (lane >> 3);
-  double ea = (ia < jb && t <= ia) ? Mp[pidx(j0 + ia, j0 + t)] : 0.0;
-  double eb = (ib < jb && t <= ib) ? Mp[pidx(j0 + ib, j0 + t)] : 0.0;
+  const int r = lane & 7;
+  double a[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) a[t] = (r < jb && t <= r) ? Mp[pidx(j0 + r, j0 + t)] : 0.0;
   int ok = 1;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     if (c < jb) {
-      const double pv = __shfl_sync(0xffffffffu, c < 4 ? ea : eb, (c & 3) * 8 + c);
+      const double pv = __shfl_sync(0xffffffffu, a[c], c);
       if (!(pv > 0.0)) ok = 0;
-      const double r = ok ? rsqrt(pv) : 0.0;
-      if (t == c) {
-        if (ia > c) ea *= r; else if (ia == c) ea = pv * r;
-        if (ib > c) eb *= r; else if (ib == c) eb = pv * r;
-      }
-      if (lane == 0) rdiag[j0 + c] = r;
-      const double lia = __shfl_sync(0xffffffffu, ea, (ia & 3) * 8 + c);  // L(ia, c), ia < 4
-      const double lib = __shfl_sync(0xffffffffu, eb, (ib & 3) * 8 + c);  // L(ib, c)
-      const double lta_a = __shfl_sync(0xffffffffu, ea, (t & 3) * 8 + c);
-      const double lta_b = __shfl_sync(0xffffffffu, eb, (t & 3) * 8 + c);
-      const double lta = t < 4 ? lta_a : lta_b;  // L(t, c)
-      if (t > c) {
-        if (t <= ia) ea -= lia * lta;
-        if (t <= ib) eb -= lib * lta;
+      const double rs = ok ? rsqrt(pv) : 0.0;
+      if (lane == 0) rdiag[j0 + c] = rs;
+      a[c] = (r == c) ? pv * rs : a[c] * rs;
+#pragma unroll
+      for (int t = c + 1; t < 8; ++t) {
+        const double ltc = __shfl_sync(0xffffffffu, a[c], t);  // L(t, c)
+        if (t <= r) a[t] -= a[c] * ltc;
       }
     }
   }
-  if (ia < jb && t <= ia) Mp[pidx(j0 + ia, j0 + t)] = ea;
-  if (ib < jb && t <= ib) Mp[pidx(j0 + ib, j0 + t)] = eb;
+  if (lane < 8 && r < jb) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (t <= r) Mp[pidx(j0 + r, j0 + t)] = a[t];
+  }
   if (lane == 0) *flag = ok;
 }
 
@@ -292,18 +291,25 @@ __device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ r
   for (int J = 0; J < T; ++J) {
     const int j0 = J * 8, jb = min(8, d - j0);
     // (a) panel rows below: x = a L_JJ^{-T}
+    // (the row's entries are read first and stored last, so the L_JJ and
+    // rdiag loads are free to issue ahead of the dependent chain)
     for (int i = j0 + jb + tid; i < d; i += nth) {
       double* ri = Mp + pidx(i, j0);
-      double x[8];
+      double v[8], x[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = c < jb ? ri[c] : 0.0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c < jb) {
-          double s = ri[c];
+          double s = v[c];
+#pragma unroll
           for (int t = 0; t < c; ++t) s -= x[t] * Mp[pidx(j0 + c, j0 + t)];
           x[c] = s * rdiag[j0 + c];
-          ri[c] = x[c];
         }
       }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < jb) ri[c] = x[c];
     }
     __syncthreads();
     // (b) trailing tile pairs (I, K), J < K <= I; pair 0 = the next diagonal

@@ -1,0 +1,105 @@
+// Microbenchmark (diagnostic): the IPM Cholesky's 8 x 8 diagonal-block
+// factorisation by one warp (packed lower storage), cycles per call:
+//   v0 the kernel's chol_diag8 (shuffle chain, double rsqrt)
+//   v1 rows in lanes 0..7 (row r in lane r, all 8 entries in registers)
+#include <cstdio>
+__device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
+__device__ __forceinline__ void chol_diag8(double* Mp, int d, int J, double* rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = J * 8, jb = min(8, d - j0);
+  const int t = lane & 7, ia = lane >> 3, ib = 4 + (lane >> 3);
+  double ea = (ia < jb && t <= ia) ? Mp[pidx(j0 + ia, j0 + t)] : 0.0;
+  double eb = (ib < jb && t <= ib) ? Mp[pidx(j0 + ib, j0 + t)] : 0.0;
+  int ok = 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < jb) {
+      const double pv = __shfl_sync(0xffffffffu, c < 4 ? ea : eb, (c & 3) * 8 + c);
+      if (!(pv > 0.0)) ok = 0;
+      const double r = ok ? rsqrt(pv) : 0.0;
+      if (t == c) {
+        if (ia > c) ea *= r; else if (ia == c) ea = pv * r;
+        if (ib > c) eb *= r; else if (ib == c) eb = pv * r;
+      }
+      if (lane == 0) rdiag[j0 + c] = r;
+      const double lia = __shfl_sync(0xffffffffu, ea, (ia & 3) * 8 + c);
+      const double lib = __shfl_sync(0xffffffffu, eb, (ib & 3) * 8 + c);
+      const double lta_a = __shfl_sync(0xffffffffu, ea, (t & 3) * 8 + c);
+      const double lta_b = __shfl_sync(0xffffffffu, eb, (t & 3) * 8 + c);
+      const double lta = t < 4 ? lta_a : lta_b;
+      if (t > c) {
+        if (t <= ia) ea -= lia * lta;
+        if (t <= ib) eb -= lib * lta;
+      }
+    }
+  }
+  if (ia < jb && t <= ia) Mp[pidx(j0 + ia, j0 + t)] = ea;
+  if (ib < jb && t <= ib) Mp[pidx(j0 + ib, j0 + t)] = eb;
+  if (lane == 0) *flag = ok;
+}
+// v1: lane r (< 8) holds row r of the block; per column c the pivot row's
+// entries come by shuffle from lane c (row c, columns <= c are final)
+__device__ __forceinline__ void chol_diag8_v1(double* Mp, int d, int J, double* rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = J * 8, jb = min(8, d - j0);
+  const int r = lane & 7;
+  double a[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) a[t] = (r < jb && t <= r) ? Mp[pidx(j0 + r, j0 + t)] : 0.0;
+  int ok = 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < jb) {
+      const double pv = __shfl_sync(0xffffffffu, a[c], c);   // A(c, c) after the updates so far
+      if (!(pv > 0.0)) ok = 0;
+      const double rs = ok ? rsqrt(pv) : 0.0;
+      if (lane == 0) rdiag[j0 + c] = rs;
+      // column c: L(r, c) = A(r, c) / L(c, c); the diagonal L(c, c) = pv rs
+      a[c] = (r == c) ? pv * rs : a[c] * rs;
+      // trailing update of row r: A(r, t) -= L(r, c) L(t, c), c < t <= r
+#pragma unroll
+      for (int t = c + 1; t < 8; ++t) {
+        const double ltc = __shfl_sync(0xffffffffu, a[c], t);  // L(t, c) from lane t
+        if (t <= r) a[t] -= a[c] * ltc;
+      }
+    }
+  }
+  if (lane < 8 && r < jb) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) if (t <= r) Mp[pidx(j0 + r, j0 + t)] = a[t];
+  }
+  if (lane == 0) *flag = ok;
+}
+__global__ void k(int v, double* g, long long* out) {
+  __shared__ double Mp[64 * 65 / 2];
+  __shared__ double rd[64];
+  __shared__ int flag;
+  const int d = 64;
+  for (int x = threadIdx.x; x < d * (d + 1) / 2; x += blockDim.x) Mp[x] = g[x];
+  __syncthreads();
+  long long t0 = clock64();
+  for (int rep = 0; rep < 50; ++rep) {
+    if (v == 0) chol_diag8(Mp, d, rep & 7, rd, &flag); else chol_diag8_v1(Mp, d, rep & 7, rd, &flag);
+    __syncwarp();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[v] = (t1 - t0) / 50;
+  for (int x = threadIdx.x; x < 64; x += blockDim.x) g[4096 + x] = rd[x];
+}
+int main() {
+  const int d = 64;
+  static double h[8192];
+  for (int i = 0; i < d; ++i) for (int j = 0; j <= i; ++j) h[i * (i + 1) / 2 + j] = (i == j) ? 100.0 + i : 1.0 / (1 + i + j);
+  double* g; long long* o; cudaMalloc(&g, 8192 * 8); cudaMalloc(&o, 64);
+  double rd0[64], rd1[64];
+  for (int v = 0; v < 2; ++v) {
+    cudaMemcpy(g, h, 8192 * 8, cudaMemcpyHostToDevice);
+    k<<<1, 32>>>(v, g, o);
+    cudaDeviceSynchronize();
+    cudaMemcpy(v ? rd1 : rd0, g + 4096, 64 * 8, cudaMemcpyDeviceToHost);
+  }
+  long long c[2]; cudaMemcpy(c, o, 16, cudaMemcpyDeviceToHost);
+  double mx = 0; for (int i = 0; i < 64; ++i) mx = fmax(mx, fabs(rd0[i] - rd1[i]));
+  printf("diag8 v0 %lld cycles, v1 %lld cycles, max |rdiag diff| %.3e\n", c[0], c[1], mx);
+  return 0;
+}
