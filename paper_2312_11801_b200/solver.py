@@ -413,7 +413,12 @@ class DeviceSolver:
         self.ineq = self.dp.ineq
         self.has_ineq = self.dp.has_ineq
         self.b_norm = float(np.linalg.norm(np.asarray(prob.b, dtype=float)))
-        self.sc = self.rt.zeros(64)
+        # the scalars the host reads each iteration live in one buffer, so a
+        # single D2H fetches them (sc 0:64, res_q 64:72, res_e 72:80, a k-vector
+        # slot 80:144, lamc 144:208)
+        self._scratch = self.rt.zeros(208)
+        self._scratch_h = self.rt.torch.empty(208, dtype=self.rt.torch.float64, pin_memory=True)
+        self.sc = self._scratch[:64]
         self.opts = _ipm_opts(cfg)
         lz = getattr(cfg, "lanczos", None) or LanczosSettings()
         self.lz = (int(lz.inner_iters), int(lz.max_restarts), lz.tol)
@@ -444,12 +449,12 @@ class DeviceSolver:
         sl = self.eng.state_len(k)
         self.st_q = rt.zeros(sl)
         self.st_e = rt.zeros(sl)
-        self.res_q = rt.zeros(8)
-        self.res_e = rt.zeros(8)
+        self.res_q = self._scratch[64:72]
+        self.res_e = self._scratch[72:80]
         self.s_act = rt.empty(k, k)
         self.evals = rt.empty(k)
         self.evecs = rt.empty(k, k)
-        self.lamc = rt.empty(max(self.k_c, 1))
+        self.lamc = self._scratch[144:144 + max(self.k_c, 1)] if self.k_c <= 64 else rt.empty(self.k_c)
         self.ident = rt.upload(np.eye(max(k, 1)))
         self.lz_probe = None  # list -> (start, end, restarts, matvecs) per Lanczos call
         # overlap the model-evaluation IPM with the Lanczos kernel (single GPU,
@@ -463,6 +468,14 @@ class DeviceSolver:
     def _fetch(self, *tensors):
         """One synchronising D2H of several small device arrays."""
         return [t.cpu().numpy() for t in tensors]
+
+    def _fetch_scratch(self, upto: int) -> np.ndarray:
+        """The first `upto` entries of the scalar buffer in one synchronising
+        D2H (pinned)."""
+        h = self._scratch_h[:upto]
+        h.copy_(self._scratch[:upto], non_blocking=True)
+        self.rt.stream.synchronize()
+        return h.numpy().copy()
 
     def penalized_lanczos(self, y_dev, which=1, assembled=False):
         """penalized_obj (bundle.py:212-236) minus the <b,y> term (device dot)."""
@@ -710,7 +723,9 @@ class DeviceSolver:
             # s_act = alpha S (original units) for model_update
             S = self.st_q[:k * k].view(k, k)
             eng.vec(N.VOP_AXPBY, k * k, x=S.reshape(-1), s0=a, out=self.s_act.view(-1))
-            sc_h, rq, re_, sdiag = self._fetch(sc[:18], self.res_q, self.res_e, S.diagonal())
+            self._scratch[80:80 + k].copy_(S.diagonal())
+            buf = self._fetch_scratch(80 + k)
+            sc_h, rq, re_, sdiag = buf[:18], buf[64:72], buf[72:80], buf[80:80 + k]
             if self.has_ineq and sc_h[S_MINI + 1] > 0.0:
                 raise ValueError("candidate dual point violates the sign constraints")
             eta_act = (a * float(rq[3]) / tr) if has_eta else 0.0
@@ -772,12 +787,16 @@ class DeviceSolver:
                 red=sc[S_RES:S_RES + 2])
         eng.dot_into(self.b, y, sc[S_BY:S_BY + 1])
         if pending is not None:
-            sc_h, lamc = self._fetch(sc[:18], self.lamc[:model.k_c])
+            if self.lamc.data_ptr() == self._scratch[144:].data_ptr():
+                buf = self._fetch_scratch(144 + model.k_c)
+                sc_h, lamc = buf[:18], buf[144:144 + model.k_c]
+            else:
+                sc_h, lamc = self._fetch(sc[:18], self.lamc[:model.k_c])
             eta, tr_old, cip_old = pending
             model.stats.trace = eta * tr_old + float(lamc.sum())
             model.stats.cost_ip = eta * cip_old + float(sc_h[S_CFIP])
         else:
-            (sc_h,) = self._fetch(sc[:18])
+            sc_h = self._fetch_scratch(18)
         c_x = primal.cost_ip
         rel_infeas = math.sqrt(max(float(sc_h[S_RES]), 0.0)) / (1.0 + self.b_norm)
         linf = float(sc_h[S_RES + 1]) if self.m else 0.0
