@@ -546,7 +546,11 @@ __global__ void __launch_bounds__(256) k_pivchol(int c, const double* __restrict
         X[row * 40 + col] = (row <= col) ? s / R[row * 40 + row] : 0.0;
       }
     __syncthreads();
-    for (int x = tid; x < r * r; x += nth) Rinv[(x / r) * c + (x % r)] = X[(x / r) * 40 + (x % r)];
+    // r x r upper inverse, zero elsewhere (callers may reuse the buffer)
+    for (int x = tid; x < c * c; x += nth) {
+      const int i = x / c, j = x % c;
+      Rinv[x] = (i < r && j < r) ? X[i * 40 + j] : 0.0;
+    }
   }
   if (tid == 0) {
     info[0] = r;

@@ -315,21 +315,26 @@ def orthonormalize_dev(eng: Engine, A, drop_tol: float = 1e-12):
     dropped: there a Gram cannot resolve the drop rule."""
     rt = eng.rt
     n, c = A.shape
-    G = rt.empty(c, c)
+    # scratch reused across calls (usbs_pivchol writes every entry of its
+    # outputs); the result is a fresh tensor (callers keep bases around)
+    cache = eng.__dict__.setdefault("_orth_scratch", {})
+    key = (n, c)
+    if key not in cache:
+        i32 = rt.torch.int32
+        cache[key] = {"G": rt.empty(c, c), "perm": rt.torch.zeros(c, dtype=i32, device=rt.device),
+                      "rinv": rt.zeros(c, c), "info": rt.zeros(3), "B": rt.empty(c, c), "Y": rt.empty(n, c),
+                      "G2": rt.empty(c, c), "perm2": rt.torch.zeros(c, dtype=i32, device=rt.device),
+                      "rinv2": rt.zeros(c, c), "info2": rt.zeros(3)}
+    sc = cache[key]
+    G, perm, rinv, info = sc["G"], sc["perm"], sc["rinv"], sc["info"]
     eng.gram(A, A, G)
-    perm = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
-    rinv = rt.zeros(c, c)
-    info = rt.zeros(3)
     eng.pivchol(G, drop_tol, perm, rinv, info)
-    B = eng.perm_rows(perm, rinv, info, rt.empty(c, c))
-    Y = eng.rowgemm(A, B, rt.empty(n, c))
-    G2 = rt.empty(c, c)
+    B = eng.perm_rows(perm, rinv, info, sc["B"])
+    Y = eng.rowgemm(A, B, sc["Y"])
+    G2 = sc["G2"]
     eng.gram(Y, Y, G2)
-    perm2 = rt.torch.zeros(c, dtype=rt.torch.int32, device=rt.device)
-    rinv2 = rt.zeros(c, c)
-    info2 = rt.zeros(3)
-    eng.pivchol(G2, -1.0, perm2, rinv2, info2)
-    Q = eng.rowgemm(Y, rinv2, rt.empty(n, c))
+    eng.pivchol(G2, -1.0, sc["perm2"], sc["rinv2"], sc["info2"])
+    Q = eng.rowgemm(Y, sc["rinv2"], rt.empty(n, c))
     info_h = info.cpu().numpy()
     r = int(info_h[0])
     if info_h[2] == 0.0:
