@@ -371,14 +371,22 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
         return;
       }
       cross_block_sum(a.P1, G, j + 1, cvec);
+      for (int t = j + 1 + tid; t < 32 * NH; t += nth) cvec[t] = 0.0;  // the row pass reads all 32 NH
       __syncthreads();
       column_reduce<NH>(a, j, r0, r1, wred, red, [&](int i, double (&q)[NH][32]) {
-        double s = 0.0;
+        // four independent chains (q is zero above j)
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int h = 0; h < NH; ++h)
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (h * 32 + t <= j) s = fma(q[h][t], cvec[h * 32 + t], s);
+          for (int t = 0; t < 32; t += 4) {
+            const int tt = h * 32 + t;
+            s0 = fma(q[h][t], cvec[tt], s0);
+            s1 = fma(q[h][t + 1], cvec[tt + 1], s1);
+            s2 = fma(q[h][t + 2], cvec[tt + 2], s2);
+            s3 = fma(q[h][t + 3], cvec[tt + 3], s3);
+          }
+        const double s = (s0 + s1) + (s2 + s3);
         double w = Wcur[i] - s;
         Wcur[i] = w;
         return w;
@@ -391,6 +399,7 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
       BW_START();
       // ------------------------------------------------------------ phase C
       cross_block_sum(a.P2, G, j + 1, c2vec);
+      for (int t = j + 1 + tid; t < 32 * NH; t += nth) c2vec[t] = 0.0;
       __syncthreads();
       {
         // w'' = w' - Q c' with the row's Q entries loaded unrolled (all in
@@ -408,15 +417,21 @@ __global__ void __launch_bounds__(NH == 1 ? 512 : 256, 1) k_lanczos(LzArgs a) {
               const int tt = h * 32 + t;
               q[h][t] = (live && tt <= j) ? __ldcg(a.Q + qidx(i, tt, M1)) : 0.0;
             }
-          double s0 = 0.0, s1 = 0.0;
+          // four independent chains, no per-column predicates (q and c2vec
+          // are zero above j)
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
           for (int h = 0; h < NH; ++h)
 #pragma unroll
-            for (int t = 0; t < 32; t += 2) {
+            for (int t = 0; t < 32; t += 4) {
               const int tt = h * 32 + t;
-              if (tt <= j) s0 = fma(q[h][t], c2vec[tt], s0);
-              if (tt + 1 <= j) s1 = fma(q[h][t + 1], c2vec[tt + 1], s1);
+              s0 = fma(q[h][t], c2vec[tt], s0);
+              s1 = fma(q[h][t + 1], c2vec[tt + 1], s1);
+              s2 = fma(q[h][t + 2], c2vec[tt + 2], s2);
+              s3 = fma(q[h][t + 3], c2vec[tt + 3], s3);
             }
+          s0 += s2;
+          s1 += s3;
           if (live) {
             const double w = Wcur[i] - (s0 + s1);
             Wcur[i] = w;

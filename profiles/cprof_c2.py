@@ -16,4 +16,4 @@ pr.disable()
 torch.cuda.synchronize()
 print("wall per it ms", (time.perf_counter() - t0) / 60 * 1e3)
 ps = pstats.Stats(pr).sort_stats("tottime")
-ps.print_stats(25)
+ps.sort_stats("cumulative").print_stats(40)
