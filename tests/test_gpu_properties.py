@@ -258,3 +258,50 @@ def test_ipm_warm_start_beats_cold_in_aggregate():
                 wins += w.newton_iters <= cold.newton_iters
             warm = w.state
     assert wins / total >= 0.9
+
+
+def test_warm_start_from_subgraph_saves_descent_steps():
+    """Acceptance criterion 7 (test_acceptance.py:320-347): a state solved on
+    the induced subgraph of the first 99 vertices, padded into the full
+    graph, needs no more descent steps than a cold start in >= 4 of 5 runs."""
+    S = _solver()
+    from paper_2312_11801_b200 import state as ST
+    wins = 0
+    for seed in range(5):
+        g = random_graph(100, 0.08, 900 + seed)
+        keep = (g.eu < 99) & (g.ev < 99)
+        sub = inst.Graph.from_arrays(99, g.eu[keep], g.ev[keep], g.ew[keep])
+        prob, sub_prob = inst.maxcut_problem(g), inst.maxcut_problem(sub)
+        cfg = S.SolverConfig(rho=0.01, beta=0.25, k_c=10, k_p=1, eps=1e-3, max_iters=3000, seed=seed)
+        cold, _ = S.solve(prob, cfg)
+        assert cold.status == "converged"
+        sub_state, _ = S.solve(sub_prob, cfg)
+        padded = ST.warm_start_pad(sub_state, prob, ST.Mapping(np.arange(99), np.arange(99)), sketch_seed=seed)
+        warm, _ = S.solve(prob, cfg, init=padded)
+        assert warm.status == "converged"
+        wins += warm.descent_steps <= cold.descent_steps
+    assert wins >= 4
+
+
+def test_diagonal_fast_path_equals_generic_entries():
+    """problem.py's diagonal family and the same constraints written as
+    generic entries give the same device images and adjoints
+    (test_problem.py:228-256)."""
+    from paper_2312_11801_b200.constraints import DeviceConstraints
+    rng = np.random.default_rng(12)
+    n, k = 300, 7
+    ent = SimpleNamespace(idx=np.arange(n), rows=np.arange(n), cols=np.arange(n), vals=np.ones(n))
+    diag = DeviceConstraints(n, n, inst.DiagonalFamily(n))
+    gen = DeviceConstraints(n, n, ent)
+    v = rng.standard_normal((n, k))
+    s = rng.standard_normal((k, k))
+    s = s + s.T
+    y = rng.standard_normal(n)
+    np.testing.assert_allclose(diag.primal_image_lowrank(v, s), gen.primal_image_lowrank(v, s), rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(diag.adjoint_matvec(y, v), gen.adjoint_matvec(y, v), rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(diag.adjoint_inner_lowrank(y, v), gen.adjoint_inner_lowrank(y, v), rtol=1e-12,
+                               atol=1e-12)
+    # adjoint identity <A(X), y> = <X, A*(y)> for X = V S V^T
+    lhs = float(gen.primal_image_lowrank(v, s) @ y)
+    rhs = float(np.sum(s * gen.adjoint_inner_lowrank(y, v)))
+    assert abs(lhs - rhs) <= 1e-10 * (1.0 + abs(lhs))
