@@ -59,37 +59,39 @@ __global__ void __launch_bounds__(256) k_gram_partial(int64_t n, const double* _
   }
 }
 
+// a warp per output entry: lanes stride over the block partials (fixed
+// order), then a warp reduction; the symmetric variant averages the entry
+// with its transpose
 __global__ void k_gram_final(int nb, int ka, int kb, const double* __restrict__ part, double* __restrict__ out,
                              int sym) {
   const int npair = ka * kb;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* g = (double*)smem_raw;
-  for (int p = threadIdx.x; p < npair; p += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[(int64_t)b * npair + p];
-    g[p] = s;
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= npair) return;
+  const int ia = p / kb, ib = p % kb;
+  const int pt = ib * kb + ia;
+  double s = 0.0, st = 0.0;
+  for (int b = lane; b < nb; b += 32) {
+    s += part[(int64_t)b * npair + p];
+    if (sym) st += part[(int64_t)b * npair + pt];
   }
-  __syncthreads();
-  for (int p = threadIdx.x; p < npair; p += blockDim.x) {
-    if (sym) {
-      const int ia = p / kb, ib = p % kb;
-      out[p] = 0.5 * (g[ia * kb + ib] + g[ib * kb + ia]);
-    } else {
-      out[p] = g[p];
-    }
-  }
+  s = warp_sum(s);
+  if (sym) st = warp_sum(st);
+  if (lane == 0) out[p] = sym ? 0.5 * (s + st) : s;
 }
 
 void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B, int64_t ldb,
                     int kb, double* out, bool sym) {
   if (ka < 1 || kb < 1 || ka > 64 || kb > 64) fail(USBS_ERR_SHAPE, "gram: 1 <= k <= 64");
   if (sym && ka != kb) fail(USBS_ERR_SHAPE, "gram: symmetric output needs ka == kb");
-  int nb = (int)std::min<int64_t>(2 * ctx->num_sms, std::max<int64_t>(1, (n + 255) / 256));
+  // one block per SM for n >= 148 * 64 rows, else a 64-row chunk per block:
+  // the partial pass is latency-bound per tile, so short chunks win
+  int nb = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + 63) / 64));
   double* part = (double*)ctx->ws.get(WS_GRAM_PARTIAL, (size_t)nb * ka * kb * sizeof(double));
   size_t sm = (size_t)GRAM_TR * (ka + kb) * sizeof(double);
   k_gram_partial<<<nb, 256, sm, ctx->stream>>>(n, A, lda, ka, B, ldb, kb, part);
   check_launch(ctx);
-  k_gram_final<<<1, 256, (size_t)ka * kb * sizeof(double), ctx->stream>>>(nb, ka, kb, part, out, sym ? 1 : 0);
+  k_gram_final<<<(ka * kb + 7) / 8, 256, 0, ctx->stream>>>(nb, ka, kb, part, out, sym ? 1 : 0);
   check_launch(ctx);
 }
 
