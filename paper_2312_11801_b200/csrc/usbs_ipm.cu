@@ -70,6 +70,7 @@ struct IpmSmem {
   double *S, *T, *H, *dS, *dT, *W1, *W2, *X1, *X2;  // k x k
   double *s, *t, *vI, *h, *g, *f1, *rhs, *ds, *dt, *rd, *tmp, *cb0, *cb1;  // d
   unsigned char *pi, *pj;
+  unsigned short* ctab;  // lower-triangle table of the warp Cholesky
   double* red;   // 32
   double* sc;    // scalars 64
   int* flg;      // 16
@@ -90,55 +91,52 @@ __device__ double blk_max_abs(const double* x, int n, double* red) {
   return r;
 }
 
-// warp 0: in-place Cholesky (lower, row-major k x k in W). returns ok to all
-// threads of the block (via flg[slot]).  Fails on pivot <= 0 or NaN (potrf).
-__device__ void warp_chol(double* W, int k, int* flg, int slot) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int ok = 1;
-    for (int j = 0; j < k; ++j) {
-      double piv = W[j * k + j];
-      if (!(piv > 0.0)) { ok = 0; break; }
-      const double r = rsqrt(piv);
-      const double ljj = piv * r;
-      __syncwarp();
-      if (lane == 0) W[j * k + j] = ljj;
-      if (lane > j && lane < k) W[lane * k + j] *= r;
-      __syncwarp();
-      if (lane > j && lane < k) {
-        double lij = W[lane * k + j];
-        for (int c = j + 1; c <= lane; ++c) W[lane * k + c] -= lij * W[c * k + j];
-      }
-      __syncwarp();
+// One warp factors W (lower, row-major k x k, k <= 32) in place: per column
+// the pivot's rsqrt, the column scaled by the lanes below it, then the
+// trailing update W[r][c] -= L[r][j] L[c][j] over all (r, c), j < c <= r,
+// spread across the lanes from a column-major table of the lower triangle
+// (ctab: entries (r << 5 | c) for 1 <= c <= r < k, column c from
+// (c - 1) k - c (c - 1) / 2), so the updates of one column are independent
+// and pipeline instead of forming one lane's serial chain.  Same arithmetic
+// per entry as the row-by-row form.  Fails on a pivot <= 0 or NaN (potrf);
+// returns ok.
+__device__ __forceinline__ int warp_chol_core(double* W, int k, const unsigned short* ctab) {
+  const int lane = threadIdx.x & 31;
+  const int ntab = k * (k - 1) / 2;
+  int ok = 1;
+  for (int j = 0; j < k; ++j) {
+    const double piv = W[j * k + j];
+    if (!(piv > 0.0)) { ok = 0; break; }
+    const double r = rsqrt(piv);
+    const int row = j + 1 + lane;
+    if (row < k) W[row * k + j] *= r;
+    if (lane == 0) W[j * k + j] = piv * r;
+    __syncwarp();
+    for (int e = j * k - (j + 1) * j / 2 + lane; e < ntab; e += 32) {
+      const int rc = ctab[e], rr = rc >> 5, cc = rc & 31;
+      W[rr * k + cc] -= W[rr * k + j] * W[cc * k + j];
     }
-    if (lane == 0) flg[slot] = ok;
+    __syncwarp();
+  }
+  return ok;
+}
+
+// warp 0 factors W; the result goes to all threads through flg[slot]
+__device__ void warp_chol(double* W, int k, int* flg, int slot, const unsigned short* ctab) {
+  if (threadIdx.x < 32) {
+    const int ok = warp_chol_core(W, k, ctab);
+    if ((threadIdx.x & 31) == 0) flg[slot] = ok;
   }
   __syncthreads();
 }
 
 // two independent k x k Cholesky tests at once: warp 0 factors Wa, warp 1 Wb
 // (the line search's S + d dS and T + d dT); flg[sa], flg[sb] get the results
-__device__ void warp_chol2(double* Wa, double* Wb, int k, int* flg, int sa, int sb) {
+__device__ void warp_chol2(double* Wa, double* Wb, int k, int* flg, int sa, int sb, const unsigned short* ctab) {
   const int w = threadIdx.x >> 5;
   if (w < 2) {
-    double* W = w == 0 ? Wa : Wb;
-    const int lane = threadIdx.x & 31;
-    int ok = 1;
-    for (int j = 0; j < k; ++j) {
-      const double piv = W[j * k + j];
-      if (!(piv > 0.0)) { ok = 0; break; }
-      const double r = rsqrt(piv);
-      __syncwarp();
-      if (lane == 0) W[j * k + j] = piv * r;
-      if (lane > j && lane < k) W[lane * k + j] *= r;
-      __syncwarp();
-      if (lane > j && lane < k) {
-        const double lij = W[lane * k + j];
-        for (int c = j + 1; c <= lane; ++c) W[lane * k + c] -= lij * W[c * k + j];
-      }
-      __syncwarp();
-    }
-    if (lane == 0) flg[w == 0 ? sa : sb] = ok;
+    const int ok = warp_chol_core(w == 0 ? Wa : Wb, k, ctab);
+    if ((threadIdx.x & 31) == 0) flg[w == 0 ? sa : sb] = ok;
   }
   __syncthreads();
 }
@@ -392,7 +390,14 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   unsigned char* ub = (unsigned char*)(sm.M + (m_in_smem ? d * (d + 1) / 2 : 0));
   sm.pi = ub; sm.pj = ub + 600;
   sm.flg = (int*)(ub + 1200);
+  sm.ctab = (unsigned short*)(ub + 1264);
 
+  // lower-triangle table of the warp Cholesky: column c (1 <= c < k) holds
+  // rows c .. k-1 from entry (c - 1) k - c (c - 1) / 2
+  for (int c = 1 + tid; c < k; c += nth) {
+    const int base = (c - 1) * k - c * (c - 1) / 2;
+    for (int r = c; r < k; ++r) sm.ctab[base + r - c] = (unsigned short)((r << 5) | c);
+  }
   // svec index tables (column-major lower triangle, symlin.py:57-69)
   if (tid == 0) {
     int p = 0;
@@ -421,9 +426,9 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     int ok = (wo > 0.0 && sig > 0.0) && (!has_eta || (we > 0.0 && wz > 0.0));
     __syncthreads();
     if (ok) {
-      warp_chol(sm.W1, k, sm.flg, 0);
+      warp_chol(sm.W1, k, sm.flg, 0, sm.ctab);
       int ok1 = sm.flg[0];
-      warp_chol(sm.W2, k, sm.flg, 1);
+      warp_chol(sm.W2, k, sm.flg, 1, sm.ctab);
       int ok2 = sm.flg[1];
       ok = ok1 && ok2;
     }
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     // H = S^-1 via Cholesky: S = L L^T, Linv by forward substitution, H = Linv^T Linv
     for (int x = tid; x < kk; x += nth) sm.W1[x] = sm.S[x];
     __syncthreads();
-    warp_chol(sm.W1, k, sm.flg, 2);
+    warp_chol(sm.W1, k, sm.flg, 2, sm.ctab);
     if (!sm.flg[2]) fail = 1;
     if (!fail) {
       // X1 = L^-1 (lower): column c solved by thread c
@@ -716,7 +721,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
               sm.W2[x] = sm.T[x] + delta * sm.dT[x];
             }
             __syncthreads();
-            warp_chol2(sm.W1, sm.W2, k, sm.flg, 3, 4);  // both PSD tests at once
+            warp_chol2(sm.W1, sm.W2, k, sm.flg, 3, 4, sm.ctab);  // both PSD tests at once
             int ok = sm.flg[3] && sm.flg[4];
             if (ok) {
               if (omega + delta * domega <= 0 || sigma + delta * dsig <= 0) ok = 0;
@@ -795,7 +800,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
 size_t ipm_smem_bytes(int k) {
   const int d = k * (k + 1) / 2, kk = k * k;
   size_t doubles = 9 * kk + 13 * d + 32 + 64 + (d <= SMEM_D ? d * (d + 1) / 2 : 0);
-  return doubles * sizeof(double) + 1200 + 16 * sizeof(int) + 64;
+  return doubles * sizeof(double) + 1264 + 2 * (k * (k - 1) / 2 + 1) + 64;
 }
 
 void launch_ipm(usbs_ctx* ctx, const IpmArgs& a) {
