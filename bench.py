@@ -403,6 +403,36 @@ def c4_operator_apply(rt):
     out["lanczos_top"] = {"ms": ms, "matvecs": r.matvecs, "restarts": r.restarts, "algorithmic_bytes": b,
                           "achieved_gbs": b / (ms / 1e3) / 1e9, "frac_of_measured_peak": b / (ms / 1e3) / 1e9 / peak,
                           "kernel": "k_lanczos (grid)"}
+    # K4: the d x d compressed Gram (SYRK over m generated rows) on the FP64
+    # tensor cores, against the measured FP64 DMMA peak (profiles/fp64_peak.json)
+    from paper_2312_11801_b200.engine import Engine
+    eng = Engine(dp)
+    k = cfg.k_c + cfg.k_p
+    d = k * (k + 1) // 2
+    vq, _ = np.linalg.qr(np.random.default_rng(1234).standard_normal((p.n, k)))
+    V = rt.upload(vq)
+    G = rt.empty(d, d)
+    for _ in range(2):
+        eng.compressed(V, scale_gram=1.0, gram_out=G)
+    ts = []
+    for _ in range(5):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(rt.stream)
+        eng.compressed(V, scale_gram=1.0, gram_out=G)
+        e1.record(rt.stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    flop = p.m * d * (d + 1)
+    try:
+        fp64 = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())["fp64_dmma_tflops"]
+    except Exception:
+        fp64 = None
+    out["k4_compressed_gram"] = {"ms": ms, "m": p.m, "d": d, "flop": flop, "achieved_tflops": flop / (ms / 1e3) / 1e12,
+                                 "peak_tflops": fp64, "peak_source": "measured FP64 DMMA (profiles/fp64_peak.json)",
+                                 "frac": (flop / (ms / 1e3) / 1e12 / fp64) if fp64 else None,
+                                 "kernel": "k_compressed_mma (mma.sync m8n8k4 f64)"}
     return out
 
 

@@ -237,6 +237,155 @@ __global__ void __launch_bounds__(256) k_compressed(int64_t m, int diag_only, co
   }
 }
 
+// The same partial sums with the d x d Gram on the FP64 tensor cores: per
+// 32-row tile of generated rows (smem, as above), G += T^T T as m8n8k4 MMAs
+// over 8 x 8 output tiles of the lower triangle, TPW tiles per warp
+// (16 warps), accumulators in registers for the whole row range; the
+// tiles' (I, K) come from a smem table.
+template <int TPW>
+__global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_only, const int* __restrict__ cptr,
+                                                        const int* __restrict__ cent, const int* __restrict__ erow,
+                                                        const int* __restrict__ ecol, const double* __restrict__ eval,
+                                                        const double* __restrict__ V, int64_t ldv, int k, int d,
+                                                        const double* __restrict__ avec,
+                                                        const double* __restrict__ wvec, double* __restrict__ gpart,
+                                                        double* __restrict__ apart, double* __restrict__ wpart) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // row stride = 8 (mod 16) doubles: the fragment loads (rows 4ks + q,
+  // columns 8X + g) then hit every bank exactly twice
+  const int dp = d + 1 + ((8 - (d + 1)) & 15);
+  double* tile = (double*)smem_raw;  // CTR * dp
+  double* aw = tile + CTR * dp;       // CTR
+  double* ww = aw + CTR;              // CTR
+  unsigned char* pi = (unsigned char*)(ww + CTR);
+  unsigned char* pj = pi + 600;
+  unsigned short* ttab = (unsigned short*)(pj + 600);  // (I << 8) | K of the 8 x 8 lower tiles
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
+  const int g = lane >> 2, q = lane & 3;
+  const int n8 = (d + 7) >> 3, nt8 = n8 * (n8 + 1) / 2;
+  if (tid == 0) {
+    int p = 0;
+    for (int j = 0; j < k; ++j)
+      for (int i = j; i < k; ++i) { pi[p] = (unsigned char)i; pj[p] = (unsigned char)j; ++p; }
+  }
+  for (int t = tid; t < nt8; t += nth) {
+    int I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > t) --I;
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    ttab[t] = (unsigned short)((I << 8) | (t - I * (I + 1) / 2));
+  }
+  const int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = blockIdx.x * chunk, c1 = min(m, c0 + chunk);
+  double acc0[TPW], acc1[TPW];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) acc0[u] = acc1[u] = 0.0;
+  double accA[2] = {0, 0}, accW[2] = {0, 0};
+  __syncthreads();
+  for (int64_t base = c0; base < c1; base += CTR) {
+    const int rows = (int)min((int64_t)CTR, c1 - base);
+    __syncthreads();
+    // rows of the tile: a warp per constraint row (k <= 32), the V rows of
+    // its entries loaded once per entry into the lanes and the d products
+    // formed by shuffles, lane p handling entries p, p + 32, ...
+    for (int r = warp; r < CTR; r += nth >> 5) {
+      double accp[7];
+#pragma unroll
+      for (int jj = 0; jj < 7; ++jj) accp[jj] = 0.0;
+      if (r < rows) {
+        const int64_t i = base + r;
+        const int t0 = diag_only ? 0 : cptr[i], t1 = diag_only ? 1 : cptr[i + 1];
+        for (int t = t0; t < t1; ++t) {
+          int rr, cc2;
+          double val;
+          if (diag_only) {
+            rr = cc2 = (int)i;
+            val = 1.0;
+          } else {
+            const int e = cent[t];
+            rr = erow[e];
+            cc2 = ecol[e];
+            val = eval[e];
+          }
+          const double vr = lane < k ? V[(int64_t)rr * ldv + lane] : 0.0;
+          const double vc = lane < k ? V[(int64_t)cc2 * ldv + lane] : 0.0;
+          const double half = rr == cc2 ? 0.5 : 1.0;
+#pragma unroll
+          for (int jj = 0; jj < 7; ++jj) {
+            const int pp = lane + 32 * jj;
+            const int aa = pp < d ? pi[pp] : 0, bb = pp < d ? pj[pp] : 0;
+            const double ra = __shfl_sync(0xffffffffu, vr, aa), cb = __shfl_sync(0xffffffffu, vc, bb);
+            const double ca = __shfl_sync(0xffffffffu, vc, aa), rb = __shfl_sync(0xffffffffu, vr, bb);
+            const double wpp = aa == bb ? 1.0 : 1.4142135623730951;
+            double gg = ra * cb + ca * rb;
+            gg *= half;
+            accp[jj] += gg * val * wpp;
+          }
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 7; ++jj) {
+        const int pp = lane + 32 * jj;
+        if (pp < d) tile[r * dp + pp] = accp[jj];
+      }
+    }
+    for (int r = tid; r < CTR; r += nth) {
+      aw[r] = (avec && r < rows) ? avec[base + r] : 0.0;
+      ww[r] = (wvec && r < rows) ? wvec[base + r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      const int t = warp + 16 * u;
+      if (t < nt8) {
+        const unsigned e = ttab[t];
+        const int ca = 8 * (int)(e >> 8) + g, cb = 8 * (int)(e & 255u) + g;
+        const bool va = ca < d, vb = cb < d;
+#pragma unroll
+        for (int ks = 0; ks < CTR / 4; ++ks) {
+          const double* row = tile + (4 * ks + q) * dp;
+          const double av = va ? row[ca] : 0.0, bv = vb ? row[cb] : 0.0;
+          dmma_m8n8k4(acc0[u], acc1[u], av, bv, acc0[u], acc1[u]);
+        }
+      }
+    }
+    if (avec || wvec) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int p = tid + u * 512;
+        if (p < d) {
+          double sa = accA[u], sw = accW[u];
+          for (int r = 0; r < rows; ++r) {
+            const double c = tile[r * dp + p];
+            sa = fma(aw[r], c, sa);
+            sw = fma(ww[r], c, sw);
+          }
+          accA[u] = sa;
+          accW[u] = sw;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int t = warp + 16 * u;
+    if (t < nt8) {
+      const unsigned e = ttab[t];
+      const int P = 8 * (int)(e >> 8) + g, Q0 = 8 * (int)(e & 255u) + 2 * q;
+      double* out = gpart + (int64_t)blockIdx.x * d * d;
+      if (P < d && Q0 < d && Q0 <= P) out[(int64_t)P * d + Q0] = acc0[u];
+      if (P < d && Q0 + 1 < d && Q0 + 1 <= P) out[(int64_t)P * d + Q0 + 1] = acc1[u];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int p = tid + u * 512;
+    if (p < d) {
+      if (apart) apart[(int64_t)blockIdx.x * d + p] = accA[u];
+      if (wpart) wpart[(int64_t)blockIdx.x * d + p] = accW[u];
+    }
+  }
+}
+
 // sum block partials in fixed order; gram output mirrored to full symmetric
 __global__ void k_compressed_final(int nb, int d, const double* __restrict__ gpart, const double* __restrict__ apart,
                                    const double* __restrict__ wpart, double sg, double sa, double sw,
@@ -771,7 +920,27 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
                                                   p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, dg, gpart, \
                                                   apart, wpart);                                          \
   }
-  if (tpt <= 1) USBS_COMP(1)
+  const int n8 = (d + 7) / 8, nt8 = n8 * (n8 + 1) / 2;
+  const char* emma = getenv("USBS_COMPRESSED_MMA");
+  if (gram_out && nt8 <= 16 * 24 && !(emma && emma[0] == '0')) {
+    // tensor-core Gram (d <= 216)
+    const size_t smm = (size_t)(CTR * (d + 1 + ((8 - (d + 1)) & 15)) + 2 * CTR) * sizeof(double) + 1200 + 2 * nt8 + 16;
+#define USBS_COMP_MMA(T)                                                                                   \
+  {                                                                                                        \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      USBS_CUDA(cudaFuncSetAttribute(k_compressed_mma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    k_compressed_mma<T><<<nb, 512, smm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row, \
+                                                       p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, gpart, \
+                                                       apart, wpart);                                      \
+  }
+    if (nt8 <= 16 * 3) USBS_COMP_MMA(3)
+    else if (nt8 <= 16 * 8) USBS_COMP_MMA(8)
+    else USBS_COMP_MMA(24)
+#undef USBS_COMP_MMA
+  } else if (tpt <= 1) USBS_COMP(1)
   else if (tpt <= 2) USBS_COMP(2)
   else if (tpt <= 4) USBS_COMP(4)
   else if (tpt <= 6) USBS_COMP(6)

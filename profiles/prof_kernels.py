@@ -4,6 +4,7 @@
     python profiles/prof_kernels.py ipm       # k_ipm (d = 66) on a C2-like subproblem
     python profiles/prof_kernels.py spmm      # K1 on C4 (n = 1e6), k = 1 and 11
     python profiles/prof_kernels.py lanczos4  # k_lanczos on the C4 slack operator (HBM-resident Q)
+    python profiles/prof_kernels.py compressed  # K4 compressed d x d Gram on C3, C4, C5 (FP64 roofline)
 """
 from __future__ import annotations
 
@@ -134,6 +135,34 @@ def main(which):
             nn = 4 * r.newton_iters
             for nm, v in zip(names, out[:9]):
                 print(f"  {nm:14s} {v / 1e3 / nn:8.2f} us/newton  {100 * v / max(tot, 1):5.1f}%")
+    elif which == "compressed":
+        import json
+        from paper_2312_11801_b200.engine import Engine
+        peak = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())["fp64_dmma_tflops"]
+        for name in ("C3", "C4", "C5"):
+            cb = inst.baseline_config(name)
+            p = cb.problem
+            dp = DeviceProblem(p)
+            eng = Engine(dp)
+            k = cb.k_c + cb.k_p
+            d = k * (k + 1) // 2
+            v, _ = np.linalg.qr(np.random.default_rng(1234).standard_normal((p.n, k)))
+            V = dp.rt.upload(v)
+            G = dp.rt.empty(d, d)
+            for _ in range(2):
+                eng.compressed(V, scale_gram=1.0, gram_out=G)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 5
+            e0.record(dp.rt.stream)
+            for _ in range(reps):
+                eng.compressed(V, scale_gram=1.0, gram_out=G)
+            e1.record(dp.rt.stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            flop = p.m * d * (d + 1)  # lower triangle incl. diagonal, multiply-add = 2 flop
+            print(json.dumps({"config": name, "m": p.m, "d": d, "ms": ms, "gflop": flop / 1e9,
+                              "tflops": flop / (ms * 1e-3) / 1e12, "frac_of_fp64_dmma_peak": flop / (ms * 1e-3) / 1e12 / peak}))
     elif which == "spmm":
         p = inst.baseline_config("C4").problem
         dp = DeviceProblem(p)
