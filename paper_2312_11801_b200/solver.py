@@ -422,7 +422,8 @@ class DeviceSolver:
         # single D2H fetches them (sc 0:64, res_q 64:72, res_e 72:80, a k-vector
         # slot 80:144, lamc 144:208)
         self._scratch = self.rt.zeros(208)
-        self._scratch_h = self.rt.torch.empty(208, dtype=self.rt.torch.float64, pin_memory=True)
+        on_gpu = self._scratch.is_cuda
+        self._scratch_h = self.rt.torch.empty(208, dtype=self.rt.torch.float64, pin_memory=on_gpu)
         self.sc = self._scratch[:64]
         self.opts = _ipm_opts(cfg)
         lz = getattr(cfg, "lanczos", None) or LanczosSettings()
@@ -478,8 +479,11 @@ class DeviceSolver:
         """The first `upto` entries of the scalar buffer in one synchronising
         D2H (pinned)."""
         h = self._scratch_h[:upto]
-        h.copy_(self._scratch[:upto], non_blocking=True)
-        self.rt.stream.synchronize()
+        if self._scratch.is_cuda:
+            h.copy_(self._scratch[:upto], non_blocking=True)
+            self.rt.stream.synchronize()
+        else:  # the CPU stand-in of the multi-process tests
+            h.copy_(self._scratch[:upto])
         return h.numpy().copy()
 
     def penalized_lanczos(self, y_dev, which=1, assembled=False):
