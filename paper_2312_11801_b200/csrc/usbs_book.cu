@@ -390,30 +390,35 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
 __global__ void k_compressed_final(int nb, int d, const double* __restrict__ gpart, const double* __restrict__ apart,
                                    const double* __restrict__ wpart, double sg, double sa, double sw,
                                    double* __restrict__ G, double* __restrict__ A, double* __restrict__ W) {
-  const int64_t tot = (int64_t)d * d;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot + 2 * d;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    if (x < tot) {
-      if (!G) continue;
-      const int P = (int)(x / d), Qc = (int)(x % d);
-      if (Qc > P) continue;
-      double s = 0.0;
-      for (int b = 0; b < nb; ++b) s += gpart[(int64_t)b * tot + x];
+  // a warp per output entry (lower triangle of G, then A, then W): the lanes
+  // stride over the block partials with their loads in flight together
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ntri = (int64_t)d * (d + 1) / 2, tot = (int64_t)d * d;
+  if (wid < ntri) {
+    if (!G) return;
+    int P = (int)((sqrt(8.0 * (double)wid + 1.0) - 1.0) * 0.5);
+    while ((int64_t)P * (P + 1) / 2 > wid) --P;
+    while ((int64_t)(P + 1) * (P + 2) / 2 <= wid) ++P;
+    const int Qc = (int)(wid - (int64_t)P * (P + 1) / 2);
+    const int64_t x = (int64_t)P * d + Qc;
+    double s = 0.0;
+    for (int bb = lane; bb < nb; bb += 32) s += gpart[(int64_t)bb * tot + x];
+    s = warp_sum(s);
+    if (lane == 0) {
       G[(int64_t)P * d + Qc] = sg * s;
       G[(int64_t)Qc * d + P] = sg * s;
-    } else if (x < tot + d) {
-      if (!A) continue;
-      const int p = (int)(x - tot);
-      double s = 0.0;
-      for (int b = 0; b < nb; ++b) s += apart[(int64_t)b * d + p];
-      A[p] = sa * s;
-    } else {
-      if (!W) continue;
-      const int p = (int)(x - tot - d);
-      double s = 0.0;
-      for (int b = 0; b < nb; ++b) s += wpart[(int64_t)b * d + p];
-      W[p] = sw * s;
     }
+  } else if (wid < ntri + 2 * d) {
+    const bool isA = wid < ntri + d;
+    const int p = (int)(wid - ntri - (isA ? 0 : d));
+    const double* part = isA ? apart : wpart;
+    double* out = isA ? A : W;
+    if (!out) return;
+    double s = 0.0;
+    for (int bb = lane; bb < nb; bb += 32) s += part[(int64_t)bb * d + p];
+    s = warp_sum(s);
+    if (lane == 0) out[p] = (isA ? sa : sw) * s;
   }
 }
 
@@ -948,7 +953,7 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
   else fail(USBS_ERR_SHAPE, "cons_compressed: d too large");
 #undef USBS_COMP
   check_launch(ctx);
-  k_compressed_final<<<nblocks(ctx, (int64_t)d * d + 2 * d), 256, 0, ctx->stream>>>(
+  k_compressed_final<<<(int)(((int64_t)d * (d + 1) / 2 + 2 * d + 7) / 8), 256, 0, ctx->stream>>>(
       nb, d, gpart, apart, wpart, scale_gram, scale_a, scale_w, gram_out, a_vec ? a_out : nullptr,
       w_vec ? w_out : nullptr);
   check_launch(ctx);
