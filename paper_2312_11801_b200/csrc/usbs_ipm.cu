@@ -381,13 +381,14 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   sm.S = base; sm.T = sm.S + kk; sm.H = sm.T + kk; sm.dS = sm.H + kk; sm.dT = sm.dS + kk;
   sm.W1 = sm.dT + kk; sm.W2 = sm.W1 + kk; sm.X1 = sm.W2 + kk; sm.X2 = sm.X1 + kk;
   sm.s = sm.X2 + kk; sm.t = sm.s + d; sm.vI = sm.t + d; sm.h = sm.vI + d; sm.g = sm.h + d;
-  sm.f1 = sm.g + d; sm.rhs = sm.f1 + d; sm.ds = sm.rhs + d; sm.dt = sm.ds + d; sm.rd = sm.dt + d;
+  sm.f1 = sm.g + d; sm.rhs = sm.f1 + d + 1;  // f1: d + 1 entries (rdiag of the augmented factor)
+  sm.ds = sm.rhs + d; sm.dt = sm.ds + d; sm.rd = sm.dt + d;
   sm.tmp = sm.rd + d; sm.cb0 = sm.tmp + d; sm.cb1 = sm.cb0 + d;
   sm.red = sm.cb1 + d; sm.sc = sm.red + 32;
   sm.M = sm.sc + 64;
   const bool m_in_smem = d <= SMEM_D;
   double* Mp = m_in_smem ? sm.M : a.gM;
-  unsigned char* ub = (unsigned char*)(sm.M + (m_in_smem ? d * (d + 1) / 2 : 0));
+  unsigned char* ub = (unsigned char*)(sm.M + (m_in_smem ? (d + 1) * (d + 2) / 2 : 0));
   sm.pi = ub; sm.pj = ub + 600;
   sm.flg = (int*)(ub + 1200);
   sm.ctab = (unsigned short*)(ub + 1264);
@@ -585,53 +586,25 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
         }
       }
       __syncthreads();
+      // the right-hand side as row d of the packed matrix, with a diagonal
+      // no pivot can reach: factorising [M rhs; rhs^T big] leaves
+      // y = L^-1 rhs in row d of the factor, so the forward solve is folded
+      // into the Cholesky's panel substitutions and tile updates
+      for (int q = tid; q <= d; q += nth) Mp[pidx(d, q)] = q < d ? sm.rhs[q] : 1e300;
+      __syncthreads();
       IPM_MARK(3);
       // Cholesky of M (potrf semantics: fails on a pivot <= 0 or NaN) in
       // 8-column panels with the trailing update on the FP64 tensor cores;
       // rdiag keeps 1 / L_jj for the solves (f1 is dead once rhs is formed)
       double* rdiag = sm.f1;
-      if (!chol_tiled(Mp, d, rdiag, &sm.flg[5])) fail = 1;
+      if (!chol_tiled(Mp, d + 1, rdiag, &sm.flg[5])) fail = 1;
       IPM_MARK(4);
       if (!fail) {
-        // blocked triangular solves: the 32-row diagonal triangles by warp 0
-        // with shuffles, the off-diagonal updates by the whole block
         const int lane = tid & 31;
-        for (int J = 0; J < d; J += 32) {  // forward: L y = rhs
-          const int JB = min(32, d - J);
-          if (tid < 32) {
-            // the triangle's row of this lane and 1/L_jj preloaded into
-            // registers: the dependent chain is one shuffle + one FMA per step
-            double x = lane < JB ? sm.rhs[J + lane] : 0.0;
-            const double rdl = lane < JB ? rdiag[J + lane] : 0.0;
-            double Lr[32];
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) Lr[jj] = (jj < lane && lane < JB) ? Mp[pidx(J + lane, J + jj)] : 0.0;
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              if (jj < JB) {
-                const double yj = __shfl_sync(0xffffffffu, x * rdl, jj);
-                if (lane == jj) x = yj;
-                else x = fma(-Lr[jj], yj, x);
-              }
-            }
-            if (lane < JB) sm.rhs[J + lane] = x;
-          }
-          __syncthreads();
-          for (int i = J + JB + tid; i < d; i += nth) {
-            const int base = i * (i + 1) / 2 + J;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int jj = 0;
-            for (; jj + 3 < JB; jj += 4) {
-              s0 = fma(Mp[base + jj], sm.rhs[J + jj], s0);
-              s1 = fma(Mp[base + jj + 1], sm.rhs[J + jj + 1], s1);
-              s2 = fma(Mp[base + jj + 2], sm.rhs[J + jj + 2], s2);
-              s3 = fma(Mp[base + jj + 3], sm.rhs[J + jj + 3], s3);
-            }
-            for (; jj < JB; ++jj) s0 = fma(Mp[base + jj], sm.rhs[J + jj], s0);
-            sm.rhs[i] -= (s0 + s1) + (s2 + s3);
-          }
-          __syncthreads();
-        }
+        for (int q = tid; q < d; q += nth) sm.rhs[q] = Mp[pidx(d, q)];
+        __syncthreads();
+        // blocked backward solve: the 32-row diagonal triangles by warp 0
+        // with shuffles, the off-diagonal updates by the whole block
         for (int Jend = d; Jend > 0; Jend -= 32) {  // backward: L^T x = y
           const int J = max(0, Jend - 32), JB = Jend - J;
           if (tid < 32) {
@@ -799,7 +772,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
 
 size_t ipm_smem_bytes(int k) {
   const int d = k * (k + 1) / 2, kk = k * k;
-  size_t doubles = 9 * kk + 13 * d + 32 + 64 + (d <= SMEM_D ? d * (d + 1) / 2 : 0);
+  size_t doubles = 9 * kk + 13 * d + 1 + 32 + 64 + (d <= SMEM_D ? (d + 1) * (d + 2) / 2 : 0);
   return doubles * sizeof(double) + 1264 + 2 * (k * (k - 1) / 2 + 1) + 64;
 }
 
@@ -835,7 +808,7 @@ extern "C" usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const d
   a.warm = warm_state;
   a.state = state_out;
   a.result = result;
-  a.gM = a.d > SMEM_D ? (double*)ctx->ws.get(WS_IPM, (size_t)a.d * (a.d + 1) / 2 * sizeof(double)) : nullptr;
+  a.gM = a.d > SMEM_D ? (double*)ctx->ws.get(WS_IPM, (size_t)(a.d + 1) * (a.d + 2) / 2 * sizeof(double)) : nullptr;
   a.prof = nullptr;
   if (getenv("USBS_IPM_PROF")) {
     static bool zeroed = false;
