@@ -688,21 +688,43 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           blk_smat(sm.dt, k, d, sm, sm.dT);
           __syncthreads();
           bool found = false;
+          // the backtracking sequence delta, 0.8 delta, ... tested two steps
+          // per round (warps 0-1 the first, 2-3 the second, X1/X2 are free
+          // here): the first passing step of the pair is the one the
+          // sequential search would stop at
+          auto step_ok = [&](double dl, int f0, int f1) {
+            int ok = sm.flg[f0] && sm.flg[f1];
+            if (ok) {
+              if (omega + dl * domega <= 0 || sigma + dl * dsig <= 0) ok = 0;
+              if (has_eta && (eta + dl * deta <= 0 || zeta + dl * dzeta <= 0)) ok = 0;
+            }
+            return ok;
+          };
           while (delta >= a.o.min_step) {
+            const double d2 = delta * a.o.backtrack;
+            const bool two = d2 >= a.o.min_step;
             for (int x = tid; x < kk; x += nth) {
               sm.W1[x] = sm.S[x] + delta * sm.dS[x];
               sm.W2[x] = sm.T[x] + delta * sm.dT[x];
+              sm.X1[x] = sm.S[x] + d2 * sm.dS[x];
+              sm.X2[x] = sm.T[x] + d2 * sm.dT[x];
             }
             __syncthreads();
-            warp_chol2(sm.W1, sm.W2, k, sm.flg, 3, 4, sm.ctab);  // both PSD tests at once
-            int ok = sm.flg[3] && sm.flg[4];
-            if (ok) {
-              if (omega + delta * domega <= 0 || sigma + delta * dsig <= 0) ok = 0;
-              if (has_eta && (eta + delta * deta <= 0 || zeta + delta * dzeta <= 0)) ok = 0;
+            {
+              const int w = tid >> 5;
+              if (w < 4 && (w < 2 || two)) {
+                double* Wm = w == 0 ? sm.W1 : (w == 1 ? sm.W2 : (w == 2 ? sm.X1 : sm.X2));
+                const int ok = warp_chol_core(Wm, k, sm.ctab);
+                if ((tid & 31) == 0) sm.flg[6 + w] = ok;
+              }
             }
             __syncthreads();
-            if (ok) { found = true; break; }
-            delta *= a.o.backtrack;
+            const int ok1 = step_ok(delta, 6, 7);
+            const int ok2 = two ? step_ok(d2, 8, 9) : 0;
+            __syncthreads();
+            if (ok1) { found = true; break; }
+            if (ok2) { delta = d2; found = true; break; }
+            delta = d2 * a.o.backtrack;
           }
           if (!found) {
             fail = 1;
