@@ -160,13 +160,26 @@ __device__ void blk_smat(const double* v, int k, int d, const IpmSmem& sm, doubl
 
 // y = Q11 x (+ beta*y0) over d, warp per row (Q11 in global, coalesced rows)
 __device__ void blk_gemv_q11(const double* Q, const double* x, int d, double* y) {
+  // rows in groups of four per warp, every load of the group issued before
+  // the FMAs (Q11 sits in L2: its latency, not bandwidth, bounds this)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int p = w; p < d; p += nw) {
-    double s = 0.0;
-    if (Q)
-      for (int q = lane; q < d; q += 32) s = fma(Q[(int64_t)p * d + q], x[q], s);
-    s = warp_sum(s);
-    if (lane == 0) y[p] = s;
+  for (int p0 = 4 * w; p0 < d; p0 += 4 * nw) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (Q) {
+      for (int q = lane; q < d; q += 32) {
+        double qv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) qv[u] = p0 + u < d ? __ldg(Q + (int64_t)(p0 + u) * d + q) : 0.0;
+        const double xq = x[q];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = fma(qv[u], xq, s[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = warp_sum(s[u]);
+      if (lane == 0 && p0 + u < d) y[p0 + u] = t;
+    }
   }
 }
 
@@ -566,21 +579,28 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
         const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
         const double* Hm = sm.H;
         const double* Gm = sm.T;
+        // the rank-one/-two terms scale by one reciprocal, not a division
+        // per entry; the row's Q11 entries (global, L2) are loaded one
+        // iteration ahead so their latency overlaps the E computation
+        const double ik1 = 1.0 / kappa1, icd = 1.0 / cden;
         for (int p = wid; p < d; p += nwp) {
           const int i = sm.pi[p], j = sm.pj[p];
           const double wp = (i == j) ? 1.0 : SQ2;
           const double gp = sm.g[p], vp = sm.vI[p];
-          const int64_t row = (int64_t)p * d;
+          const double* qrow = a.Q11 ? a.Q11 + (int64_t)p * d : nullptr;
           const int base = p * (p + 1) / 2;
+          double qn = (qrow && lane <= p) ? __ldg(qrow + lane) : 0.0;
           for (int q = lane; q <= p; q += 32) {
+            const double qv = qn;
+            qn = (qrow && q + 32 <= p) ? __ldg(qrow + q + 32) : 0.0;
             const int kq = sm.pi[q], l = sm.pj[q];
             const double wq = (kq == l) ? 1.0 : SQ2;
             double e = Hm[i * k + kq] * Gm[l * k + j] + Hm[i * k + l] * Gm[kq * k + j] +
                        Gm[i * k + kq] * Hm[l * k + j] + Gm[i * k + l] * Hm[kq * k + j];
             e *= (wp * wq) * 0.25;
-            double v = (a.Q11 ? a.Q11[row + q] : 0.0) + e;
-            if (!has_eta) v += vp * sm.vI[q] / kappa1;
-            else v -= (gp * (kappa1 * sm.g[q] + sm.vI[q]) + vp * (sm.g[q] - kappa2 * sm.vI[q])) / cden;
+            double v = qv + e;
+            if (!has_eta) v += vp * sm.vI[q] * ik1;
+            else v -= (gp * (kappa1 * sm.g[q] + sm.vI[q]) + vp * (sm.g[q] - kappa2 * sm.vI[q])) * icd;
             Mp[base + q] = v;
           }
         }
