@@ -579,10 +579,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
         const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
         const double* Hm = sm.H;
         const double* Gm = sm.T;
-        // the rank-one/-two terms scale by one reciprocal, not a division
-        // per entry; the row's Q11 entries (global, L2) are loaded one
-        // iteration ahead so their latency overlaps the E computation
-        const double ik1 = 1.0 / kappa1, icd = 1.0 / cden;
+        // the row's Q11 entries (global, L2) are loaded one iteration ahead
+        // so their latency overlaps the E computation
         for (int p = wid; p < d; p += nwp) {
           const int i = sm.pi[p], j = sm.pj[p];
           const double wp = (i == j) ? 1.0 : SQ2;
@@ -599,8 +597,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
                        Gm[i * k + kq] * Hm[l * k + j] + Gm[i * k + l] * Hm[kq * k + j];
             e *= (wp * wq) * 0.25;
             double v = qv + e;
-            if (!has_eta) v += vp * sm.vI[q] * ik1;
-            else v -= (gp * (kappa1 * sm.g[q] + sm.vI[q]) + vp * (sm.g[q] - kappa2 * sm.vI[q])) * icd;
+            if (!has_eta) v += vp * sm.vI[q] / kappa1;
+            else v -= (gp * (kappa1 * sm.g[q] + sm.vI[q]) + vp * (sm.g[q] - kappa2 * sm.vI[q])) / cden;
             Mp[base + q] = v;
           }
         }
