@@ -285,39 +285,6 @@ __device__ __forceinline__ void chol_tile_update(double* __restrict__ Mp, int d,
   if (v1) Mp[oa + cc + 1] = d1;
 }
 
-// the same for the tile pair (I, K) and (I, K + 1) (when K + 1 <= I): the
-// L_IJ fragments and row offsets are shared and both tiles' operands are
-// loaded before either MMA
-__device__ __forceinline__ void chol_tile_update2(double* __restrict__ Mp, int d, int j0, int jb, int I, int K) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  const int ra = I * 8 + g;
-  const bool va = ra < d;
-  const int oa = va ? pidx(ra, 0) : 0;
-  const double a0 = (va && q < jb) ? -Mp[oa + j0 + q] : 0.0;
-  const double a1 = (va && q + 4 < jb) ? -Mp[oa + j0 + 4 + q] : 0.0;
-  const bool two = K + 1 <= I;
-  const int rb0 = K * 8 + g, rb1 = rb0 + 8;
-  const int ob0 = rb0 < d ? pidx(rb0, 0) : 0, ob1 = (two && rb1 < d) ? pidx(rb1, 0) : 0;
-  const double b00 = (rb0 < d && q < jb) ? Mp[ob0 + j0 + q] : 0.0;
-  const double b01 = (rb0 < d && q + 4 < jb) ? Mp[ob0 + j0 + 4 + q] : 0.0;
-  const double b10 = (two && rb1 < d && q < jb) ? Mp[ob1 + j0 + q] : 0.0;
-  const double b11 = (two && rb1 < d && q + 4 < jb) ? Mp[ob1 + j0 + 4 + q] : 0.0;
-  const int cc0 = K * 8 + 2 * q, cc1 = cc0 + 8;
-  const bool v00 = va && cc0 <= ra, v01 = va && cc0 + 1 <= ra;
-  const bool v10 = two && va && cc1 <= ra, v11 = two && va && cc1 + 1 <= ra;
-  const double c00 = v00 ? Mp[oa + cc0] : 0.0, c01 = v01 ? Mp[oa + cc0 + 1] : 0.0;
-  const double c10 = v10 ? Mp[oa + cc1] : 0.0, c11 = v11 ? Mp[oa + cc1 + 1] : 0.0;
-  double d00, d01, d10, d11;
-  dmma8x8x4(d00, d01, a0, b00, c00, c01);
-  dmma8x8x4(d10, d11, a0, b10, c10, c11);
-  dmma8x8x4(d00, d01, a1, b01, d00, d01);
-  dmma8x8x4(d10, d11, a1, b11, d10, d11);
-  if (v00) Mp[oa + cc0] = d00;
-  if (v01) Mp[oa + cc0 + 1] = d01;
-  if (v10) Mp[oa + cc1] = d10;
-  if (v11) Mp[oa + cc1 + 1] = d11;
-}
-
 // Blocked right-looking Cholesky of the packed lower matrix M (d x d) by
 // 8-column panels with look-ahead: per panel J, (a) the rows below block J
 // by forward substitution, a thread per row; (b) the trailing update
@@ -365,17 +332,31 @@ __device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ r
         __syncwarp();
         chol_diag8(Mp, d, J + 1, rdiag, flag);
       }
-    } else if (R > 0) {
-      // the rest in jobs of two adjacent tiles of one tile row: row I has
-      // I / 2 + 1 jobs (tile columns 2 k2, 2 k2 + 1); job 0 of row 0 is the
-      // diagonal tile warp 0 handles, so the round robin starts at job 1
-      const int nw1 = nwp - 1;
-      int I = 0, k2 = warp;
-      while (I < R && k2 >= I / 2 + 1) { k2 -= I / 2 + 1; ++I; }
-      while (I < R) {
-        chol_tile_update2(Mp, d, j0, jb, J + 1 + I, J + 1 + 2 * k2);
-        k2 += nw1;
-        while (I < R && k2 >= I / 2 + 1) { k2 -= I / 2 + 1; ++I; }
+    } else if (R > 1) {
+      // the other warps take whole tile rows I >= J + 2 (longest first),
+      // the row's L_IJ fragments and offsets loaded once for all its tiles
+      const int lane = tid & 31, g = lane >> 2, q = lane & 3, nw1 = nwp - 1;
+      for (int I = T - warp; I >= J + 2; I -= nw1) {
+        const int ra = I * 8 + g;
+        const bool va = ra < d;
+        const int oa = va ? pidx(ra, 0) : 0;
+        const double a0 = (va && q < jb) ? -Mp[oa + j0 + q] : 0.0;
+        const double a1 = (va && q + 4 < jb) ? -Mp[oa + j0 + 4 + q] : 0.0;
+        for (int K = J + 1; K <= I; ++K) {
+          const int rb = K * 8 + g;
+          const bool vb = rb < d;
+          const int ob = vb ? pidx(rb, 0) : 0;
+          const double b0 = (vb && q < jb) ? Mp[ob + j0 + q] : 0.0;
+          const double b1 = (vb && q + 4 < jb) ? Mp[ob + j0 + 4 + q] : 0.0;
+          const int cc = K * 8 + 2 * q;
+          const bool v0 = va && cc <= ra, v1 = va && cc + 1 <= ra;
+          const double c0 = v0 ? Mp[oa + cc] : 0.0, c1 = v1 ? Mp[oa + cc + 1] : 0.0;
+          double d0, d1;
+          dmma8x8x4(d0, d1, a0, b0, c0, c1);
+          dmma8x8x4(d0, d1, a1, b1, d0, d1);
+          if (v0) Mp[oa + cc] = d0;
+          if (v1) Mp[oa + cc + 1] = d1;
+        }
       }
     }
     __syncthreads();

@@ -37,6 +37,7 @@ __device__ __forceinline__ void tile_apply(double* __restrict__ M, const TileFra
   dmma(d0, d1, f.a1, f.b1, d0, d1);
   if (f.st) *reinterpret_cast<double2*>(M + f.cpos) = make_double2(d0, d1);
 }
+__device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
 __global__ void __launch_bounds__(512, 1) k(int mode, long long* out, double* sink) {
   extern __shared__ __align__(16) double M[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3, sg = t_sw(g);
@@ -51,7 +52,56 @@ __global__ void __launch_bounds__(512, 1) k(int mode, long long* out, double* si
   double acc = 0.0;
   long long t0 = clock64();
   for (int rep = 0; rep < 10; ++rep) {
-    if (mode >= 4) {
+    if (mode == 7 || mode == 8) {
+      // packed lower storage; panel J = 0 (jb = 8), tile rows I = 1..26
+      // mode 7: pair round robin (the kernel's two-tile jobs are similar)
+      // mode 8: a warp per tile row, the row's A fragments loaded once
+      const int d = D, j0 = 0, jb = 8;
+      if (mode == 8) {
+        if (warp >= 1) {
+          for (int Ir = warp - 1; Ir < 26; Ir += 15) {
+            const int I = 26 - Ir;  // longest rows first
+            const int ra = I * 8 + g;
+            const bool va = ra < d;
+            const int oa = va ? pidx(ra, 0) : 0;
+            const double a0 = va ? -M[oa + j0 + q] : 0.0, a1 = va ? -M[oa + j0 + 4 + q] : 0.0;
+            for (int K = 1; K <= I; ++K) {
+              const int rb = K * 8 + g;
+              const int ob = rb < d ? pidx(rb, 0) : 0;
+              const double b0 = rb < d ? M[ob + j0 + q] : 0.0, b1 = rb < d ? M[ob + j0 + 4 + q] : 0.0;
+              const int cc = K * 8 + 2 * q;
+              const bool v0 = va && cc <= ra, v1 = va && cc + 1 <= ra;
+              double c0 = v0 ? M[oa + cc] : 0.0, c1 = v1 ? M[oa + cc + 1] : 0.0;
+              double d0, d1;
+              dmma(d0, d1, a0, b0, c0, c1);
+              dmma(d0, d1, a1, b1, d0, d1);
+              if (v0) M[oa + cc] = d0;
+              if (v1) M[oa + cc + 1] = d1;
+            }
+          }
+        }
+      } else if (warp >= 1) {
+        int I = 0, K = warp - 1;
+        while (K > I) { K -= I + 1; ++I; }
+        for (int pq = warp - 1; pq < npairs; pq += 15) {
+          const int Ia = I + 1, Ka = K + 1;
+          const int ra = Ia * 8 + g, rb = Ka * 8 + g;
+          const int oa = ra < d ? pidx(ra, 0) : 0, ob = rb < d ? pidx(rb, 0) : 0;
+          const double a0 = (ra < d && q < jb) ? -M[oa + j0 + q] : 0.0, a1 = (ra < d && q + 4 < jb) ? -M[oa + j0 + 4 + q] : 0.0;
+          const double b0 = (rb < d && q < jb) ? M[ob + j0 + q] : 0.0, b1 = (rb < d && q + 4 < jb) ? M[ob + j0 + 4 + q] : 0.0;
+          const int cc = Ka * 8 + 2 * q;
+          const bool v0 = ra < d && cc <= ra, v1 = ra < d && cc + 1 <= ra;
+          double c0 = v0 ? M[oa + cc] : 0.0, c1 = v1 ? M[oa + cc + 1] : 0.0;
+          double d0, d1;
+          dmma(d0, d1, a0, b0, c0, c1);
+          dmma(d0, d1, a1, b1, d0, d1);
+          if (v0) M[oa + cc] = d0;
+          if (v1) M[oa + cc + 1] = d1;
+          K += 15;
+          while (K > I) { K -= I + 1; ++I; }
+        }
+      }
+    } else if (mode >= 4) {
       if (warp & 3) {
         const int nup = 12, w = warp - 1 - (warp >> 2);
         for (int pq = w; pq < npairs; pq += nup) {
@@ -98,8 +148,8 @@ __global__ void __launch_bounds__(512, 1) k(int mode, long long* out, double* si
 int main() {
   long long* o; double* s; cudaMalloc(&o, 64); cudaMalloc(&s, 64);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const char* nm[] = {"full", "loads+store", "dmma only", "decode only", "kernel path", "ptab only", "kernel no dmma"};
-  for (int mode = 0; mode < 7; ++mode) {
+  const char* nm[] = {"full", "loads+store", "dmma only", "decode only", "kernel path", "ptab only", "kernel no dmma", "packed pairs", "packed rows"};
+  for (int mode = 0; mode < 9; ++mode) {
     k<<<1, 512, 24000 * 8>>>(mode, o, s);
     cudaError_t e = cudaDeviceSynchronize();
     long long h; cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
