@@ -1017,7 +1017,14 @@ __global__ void __launch_bounds__(512, 1) k_lanczos_cl(LzArgs a, int R, int hmax
     LZ_MARK(4);
     const int ell_next = max(1, min(a.k_c + 3, m - 2));
     const int nwant = min(m, max(ell_next, a.k_c));
-    rr_arrow(m, ell, nwant, a.H, M1, ts, thetaS, Ys, m, (a.prof && b == 0) ? a.prof + 8 : nullptr);
+    // the eigenvalues split over the cluster's CTAs, each shared by DSMEM
+    auto share_lam = [&](double* lam, int r, int nwn) {
+      if (r < nwn && tid == 0)
+        for (int dd = 0; dd < CS; ++dd) cluster.map_shared_rank(lam, dd)[r] = lam[r];
+      cluster.sync();
+    };
+    rr_arrow(m, ell, nwant, a.H, M1, ts, thetaS, Ys, m, (a.prof && b == 0) ? a.prof + 8 : nullptr, b, CS,
+             share_lam);
     LZ_MARK(5);
     const double beta_last = a.H[m * M1 + (m - 1)];
     if (tid == 0) {

@@ -153,8 +153,19 @@ __device__ __forceinline__ unsigned long long tri_clock() {
     }                                                   \
   } while (0)
 
+struct RrNoShare {
+  __device__ void operator()(double*, int, int) const {}
+};
+
+// csize > 1 (one CTA of a cluster of csize, rank crank, all calling): the
+// eigenvalues are split across the CTAs -- CTA j runs the multisection of
+// eigenvalue j with all its warps (32 x warps shifts a sweep instead of 32)
+// and share(lam, j, nw) publishes lam[j] to every CTA; the rest of the
+// Rayleigh-Ritz step is redundant per CTA as before.
+template <class Share = RrNoShare>
 __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh, TriSmem s, double* vals, double* Y,
-                                int ldy, unsigned long long* tprof = nullptr) {
+                                int ldy, unsigned long long* tprof = nullptr, int crank = 0, int csize = 1,
+                                Share share = Share()) {
   unsigned long long tlast = (tprof && threadIdx.x == 0) ? tri_clock() : 0ull;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwp = nth >> 5;
   double* U0 = s.A;  // [i * nw + j]: reciprocal pivots (arrow: 1/(theta_k - lam))
@@ -200,7 +211,60 @@ __device__ inline void rr_arrow(int N, int ell, int nw, const double* H, int ldh
   const double pivmin = 1e-300 + 2.2e-16 * 2.2e-16 * tnorm * tnorm;
   TRI_MARK(0);
   // ------------------------------------------------ 1. multisection
-  for (int j = warp; j < nw; j += nwp) {
+  const bool split = csize >= nw && csize > 1;
+  if (split) {
+    const int j = crank;
+    if (j < nw) {
+      // four warps: a sweep's Sturm counts are latency-bound up to ~4 warps
+      // and FP64-throughput-bound beyond, so 128 shifts per sweep is the
+      // cheapest way down (measured: 16 warps, 512 shifts, cost more per
+      // sweep than they save in sweeps)
+      const int NWU = nwp < 4 ? nwp : 4;
+      const int asc = N - 1 - j, P = NWU * 32;
+      const double tol = 2.2e-16 * tnorm;
+      double lo = glo, hi = ghi;
+      int* wf = s.iw;  // per-warp first shift (the cluster table is built later)
+      // the sweep's shifts: geometric above theta_j (first sweep after a
+      // restart, as in the warp version) or uniform in (lo, hi)
+      auto sweep = [&](bool geo, double l0) {
+        if (warp < NWU) {
+          const double sig = geo ? (tid < P - 1 ? fmin(l0 + tnorm * exp10(15.0 * tid / (P - 2) - 15.0), ghi) : ghi)
+                                 : lo + (hi - lo) * (double)(tid + 1) / (double)(P + 1);
+          const int cnt = sturm_arrow(N, ell, s.dd, s.p, sig, pivmin);
+          const unsigned mask = __ballot_sync(0xffffffffu, cnt >= asc + 1);
+          if (lane == 0) wf[warp] = mask ? __ffs(mask) - 1 : 32;
+        }
+        __syncthreads();
+        int g = P;
+        for (int w = 0; w < NWU; ++w)
+          if (wf[w] < 32) { g = 32 * w + wf[w]; break; }
+        __syncthreads();
+        if (geo) {
+          const double sg = g < P - 1 ? fmin(l0 + tnorm * exp10(15.0 * g / (P - 2) - 15.0), ghi) : ghi;
+          const double sp = g > 0 ? fmin(l0 + tnorm * exp10(15.0 * (g - 1) / (P - 2) - 15.0), ghi) : l0;
+          hi = sg;
+          lo = sp;
+        } else {
+          const double nhi = g < P ? lo + (hi - lo) * (double)(g + 1) / (double)(P + 1) : hi;
+          const double nlo = g > 0 ? lo + (hi - lo) * (double)g / (double)(P + 1) : lo;
+          lo = nlo;
+          hi = nhi;
+        }
+      };
+      if (j < ell) {
+        const double th = s.dd[j];
+        sweep(true, fmax(glo, th - 8.8e-16 * fabs(th) - pivmin));
+      }
+      for (int it = 0; it < 24; ++it) {
+        if (hi - lo <= fmax(4.4e-16 * fmax(fabs(lo), fabs(hi)), tol) + 1e-300) break;
+        sweep(false, 0.0);
+      }
+      if (tid == 0) s.lam[j] = 0.5 * (lo + hi);
+    }
+    __syncthreads();
+    share(s.lam, crank, nw);
+  }
+  for (int j = split ? nw : warp; j < nw; j += nwp) {
     const int asc = N - 1 - j;  // ascending index of the j-th largest
     double lo = glo, hi = ghi;
     if (j < ell) {
