@@ -70,6 +70,41 @@ __device__ __forceinline__ void chol_diag8_v1(double* Mp, int d, int J, double* 
   }
   if (lane == 0) *flag = ok;
 }
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r;
+}
+__device__ __forceinline__ void chol_diag8_v2(double* Mp, int d, int J, double* rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = J * 8, jb = min(8, d - j0);
+  const int r = lane & 7;
+  double a[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) a[t] = (r < jb && t <= r) ? Mp[pidx(j0 + r, j0 + t)] : 0.0;
+  int ok = 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < jb) {
+      const double pv = __shfl_sync(0xffffffffu, a[c], c);
+      if (!(pv > 0.0)) ok = 0;
+      const double rs = ok ? rsqrt_nr(pv) : 0.0;
+      if (lane == 0) rdiag[j0 + c] = rs;
+      a[c] = (r == c) ? pv * rs : a[c] * rs;
+#pragma unroll
+      for (int t = c + 1; t < 8; ++t) {
+        const double ltc = __shfl_sync(0xffffffffu, a[c], t);
+        if (t <= r) a[t] -= a[c] * ltc;
+      }
+    }
+  }
+  if (lane < 8 && r < jb) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) if (t <= r) Mp[pidx(j0 + r, j0 + t)] = a[t];
+  }
+  if (lane == 0) *flag = ok;
+}
 __global__ void k(int v, double* g, long long* out) {
   __shared__ double Mp[64 * 65 / 2];
   __shared__ double rd[64];
@@ -79,7 +114,7 @@ __global__ void k(int v, double* g, long long* out) {
   __syncthreads();
   long long t0 = clock64();
   for (int rep = 0; rep < 50; ++rep) {
-    if (v == 0) chol_diag8(Mp, d, rep & 7, rd, &flag); else chol_diag8_v1(Mp, d, rep & 7, rd, &flag);
+    if (v == 0) chol_diag8(Mp, d, rep & 7, rd, &flag); else if (v == 1) chol_diag8_v1(Mp, d, rep & 7, rd, &flag); else chol_diag8_v2(Mp, d, rep & 7, rd, &flag);
     __syncwarp();
   }
   long long t1 = clock64();
@@ -91,15 +126,15 @@ int main() {
   static double h[8192];
   for (int i = 0; i < d; ++i) for (int j = 0; j <= i; ++j) h[i * (i + 1) / 2 + j] = (i == j) ? 100.0 + i : 1.0 / (1 + i + j);
   double* g; long long* o; cudaMalloc(&g, 8192 * 8); cudaMalloc(&o, 64);
-  double rd0[64], rd1[64];
-  for (int v = 0; v < 2; ++v) {
+  double rd0[64], rd1[64], rd2[64];
+  for (int v = 0; v < 3; ++v) {
     cudaMemcpy(g, h, 8192 * 8, cudaMemcpyHostToDevice);
     k<<<1, 32>>>(v, g, o);
     cudaDeviceSynchronize();
-    cudaMemcpy(v ? rd1 : rd0, g + 4096, 64 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(v == 2 ? rd2 : (v ? rd1 : rd0), g + 4096, 64 * 8, cudaMemcpyDeviceToHost);
   }
-  long long c[2]; cudaMemcpy(c, o, 16, cudaMemcpyDeviceToHost);
-  double mx = 0; for (int i = 0; i < 64; ++i) mx = fmax(mx, fabs(rd0[i] - rd1[i]));
-  printf("diag8 v0 %lld cycles, v1 %lld cycles, max |rdiag diff| %.3e\n", c[0], c[1], mx);
+  long long c[3]; cudaMemcpy(c, o, 24, cudaMemcpyDeviceToHost);
+  double mx = 0, mx2 = 0; for (int i = 0; i < 64; ++i) { mx = fmax(mx, fabs(rd0[i] - rd1[i])); mx2 = fmax(mx2, fabs(rd0[i] - rd2[i]) / fabs(rd0[i])); }
+  printf("diag8 v0 %lld cycles, v1 %lld cycles, v2 %lld cycles, v1 diff %.3e, v2 rel diff %.3e\n", c[0], c[1], c[2], mx, mx2);
   return 0;
 }
