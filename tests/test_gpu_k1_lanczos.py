@@ -323,3 +323,25 @@ def test_lanczos_hub_rows(cluster, monkeypatch):
     assert abs(r.eigenvalues[0] - ro.eigenvalues[0]) <= 1e-10 * abs(ro.eigenvalues[0])
     assert r.restarts == ro.restarts and r.matvecs == ro.matvecs
     np.testing.assert_allclose(r.eigenvalues, ro.eigenvalues, rtol=1e-7, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_lanczos_halo_matches_dsmem_gather(name, monkeypatch):
+    """The cluster kernel's two SpMV paths -- the per-step halo fetch and the
+    DSMEM gather inside the row loop (USBS_LZ_HALO=0, the fallback when the
+    halo does not fit) -- multiply the same operands in the same order: the
+    whole call is bit-identical."""
+    eigen, runtime = dev()
+    p = case_problem(name)
+    y = np.random.default_rng(12).standard_normal(p.m) * 1e-3
+    dp_h = runtime.DeviceProblem(p)
+    monkeypatch.setenv("USBS_LZ_HALO", "0")
+    dp_g = runtime.DeviceProblem(p)
+    assert dp_g.lanczos_plan(32)[0] > 0
+    monkeypatch.delenv("USBS_LZ_HALO")
+    assert dp_h.lanczos_plan(32)[0] > 0
+    rh = eigen.lanczos_top(eigen.dual_slack_operator(dp_h, y), 10, seed=5)
+    rg = eigen.lanczos_top(eigen.dual_slack_operator(dp_g, y), 10, seed=5)
+    assert rh.restarts == rg.restarts and rh.matvecs == rg.matvecs
+    np.testing.assert_array_equal(rh.eigenvalues, rg.eigenvalues)
+    np.testing.assert_array_equal(rh.eigenvectors, rg.eigenvectors)

@@ -107,8 +107,12 @@ def test_constraint_kernels_vs_reference(tag):
     np.testing.assert_allclose(W.cpu().numpy(), -comp.T @ y, rtol=1e-11, atol=1e-13)
 
 
+@pytest.mark.parametrize("mma", ["1", "0"])
 @pytest.mark.parametrize("name", ["C1", "C5s", "qap20"])
-def test_compressed_gram_at_scale(name):
+def test_compressed_gram_at_scale(name, mma, monkeypatch):
+    """Both Gram paths (FP64 tensor cores, and the DFMA register tiles kept
+    for d > 216) against the oracle's dense compressed rows."""
+    monkeypatch.setenv("USBS_COMPRESSED_MMA", mma)
     engine, runtime, solver, _ = mods()
     if name == "C1":
         p, k = inst.baseline_config("C1").problem, 11
