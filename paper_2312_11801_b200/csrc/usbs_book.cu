@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {
-      const int t = warp + 16 * u;
+      const int t = blockIdx.y * 16 + warp + 16 * (int)gridDim.y * u;
       if (t < nt8) {
         const unsigned e = ttab[t];
         const int ca = 8 * (int)(e >> 8) + g, cb = 8 * (int)(e & 255u) + g;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
         }
       }
     }
-    if (avec || wvec) {
+    if ((avec || wvec) && blockIdx.y == 0) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int p = tid + u * 512;
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
   }
 #pragma unroll
   for (int u = 0; u < TPW; ++u) {
-    const int t = warp + 16 * u;
+    const int t = blockIdx.y * 16 + warp + 16 * (int)gridDim.y * u;
     if (t < nt8) {
       const unsigned e = ttab[t];
       const int P = 8 * (int)(e >> 8) + g, Q0 = 8 * (int)(e & 255u) + 2 * q;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int p = tid + u * 512;
-    if (p < d) {
+    if (p < d && blockIdx.y == 0) {
       if (apart) apart[(int64_t)blockIdx.x * d + p] = accA[u];
       if (wpart) wpart[(int64_t)blockIdx.x * d + p] = accW[u];
     }
@@ -930,20 +930,20 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
   if (gram_out && nt8 <= 16 * 24 && !(emma && emma[0] == '0')) {
     // tensor-core Gram (d <= 216)
     const size_t smm = (size_t)(CTR * (d + 1 + ((8 - (d + 1)) & 15)) + 2 * CTR) * sizeof(double) + 1200 + 2 * nt8 + 16;
-#define USBS_COMP_MMA(T)                                                                                   \
+#define USBS_COMP_MMA(T, HY)                                                                               \
   {                                                                                                        \
     static bool attr = false;                                                                              \
     if (!attr) {                                                                                           \
       USBS_CUDA(cudaFuncSetAttribute(k_compressed_mma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
       attr = true;                                                                                         \
     }                                                                                                      \
-    k_compressed_mma<T><<<nb, 512, smm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row, \
+    k_compressed_mma<T><<<dim3(nb, HY), 512, smm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row, \
                                                        p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, gpart, \
                                                        apart, wpart);                                      \
   }
-    if (nt8 <= 16 * 3) USBS_COMP_MMA(3)
-    else if (nt8 <= 16 * 8) USBS_COMP_MMA(8)
-    else USBS_COMP_MMA(24)
+    if (nt8 <= 16 * 3) USBS_COMP_MMA(3, 1)
+    else if (nt8 <= 16 * 8) USBS_COMP_MMA(8, 1)
+    else USBS_COMP_MMA(12, 2)  // the tiles split over two CTAs per row range: 24 accumulators a lane, no spill
 #undef USBS_COMP_MMA
   } else if (tpt <= 1) USBS_COMP(1)
   else if (tpt <= 2) USBS_COMP(2)
