@@ -1,7 +1,11 @@
 // Microbenchmark (diagnostic): the IPM Cholesky's 8 x 8 diagonal-block
 // factorisation by one warp (packed lower storage), cycles per call:
-//   v0 the kernel's chol_diag8 (shuffle chain, double rsqrt)
+//   v0 two entries per lane (the round's first version; shuffle chain)
 //   v1 rows in lanes 0..7 (row r in lane r, all 8 entries in registers)
+//   v2 v1 with an FP32-seeded rsqrt
+//   v3 the whole block in every lane, factored redundantly (no shuffles)
+// B200, d = 64 block: v0 2321, v1 1638 (the kernel's), v2 2173, v3 2678
+// cycles; v1 = v3 bit for bit (single-lane issue makes v3 slower)
 #include <cstdio>
 __device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
 __device__ __forceinline__ void chol_diag8(double* Mp, int d, int J, double* rdiag, int* flag) {
@@ -105,6 +109,45 @@ __device__ __forceinline__ void chol_diag8_v2(double* Mp, int d, int J, double* 
   }
   if (lane == 0) *flag = ok;
 }
+
+// v3: every lane holds the whole 8 x 8 lower block and factors it
+// redundantly (no shuffles; same per-entry operation sequence as v1);
+// lane r (< 8) stores row r
+__device__ __forceinline__ void chol_diag8_v3(double* Mp, int d, int J, double* rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = J * 8, jb = min(8, d - j0);
+  double a[36];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int t = 0; t <= r; ++t) a[r * (r + 1) / 2 + t] = (r < jb) ? Mp[pidx(j0 + r, j0 + t)] : 0.0;
+  int ok = 1;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < jb) {
+      const double pv = a[c * (c + 1) / 2 + c];
+      if (!(pv > 0.0)) ok = 0;
+      const double rs = ok ? rsqrt(pv) : 0.0;
+      if (lane == 0) rdiag[j0 + c] = rs;
+      a[c * (c + 1) / 2 + c] = pv * rs;
+#pragma unroll
+      for (int r = c + 1; r < 8; ++r) a[r * (r + 1) / 2 + c] *= rs;
+#pragma unroll
+      for (int r = c + 1; r < 8; ++r)
+#pragma unroll
+        for (int t = c + 1; t <= r; ++t) a[r * (r + 1) / 2 + t] -= a[r * (r + 1) / 2 + c] * a[t * (t + 1) / 2 + c];
+    }
+  }
+  const int r = lane & 7;
+  if (lane < 8 && r < jb) {
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr)
+      if (rr == r)
+#pragma unroll
+        for (int t = 0; t <= rr; ++t) Mp[pidx(j0 + rr, j0 + t)] = a[rr * (rr + 1) / 2 + t];
+  }
+  if (lane == 0) *flag = ok;
+}
 __global__ void k(int v, double* g, long long* out) {
   __shared__ double Mp[64 * 65 / 2];
   __shared__ double rd[64];
@@ -114,7 +157,7 @@ __global__ void k(int v, double* g, long long* out) {
   __syncthreads();
   long long t0 = clock64();
   for (int rep = 0; rep < 50; ++rep) {
-    if (v == 0) chol_diag8(Mp, d, rep & 7, rd, &flag); else if (v == 1) chol_diag8_v1(Mp, d, rep & 7, rd, &flag); else chol_diag8_v2(Mp, d, rep & 7, rd, &flag);
+    if (v == 0) chol_diag8(Mp, d, rep & 7, rd, &flag); else if (v == 1) chol_diag8_v1(Mp, d, rep & 7, rd, &flag); else if (v == 2) chol_diag8_v2(Mp, d, rep & 7, rd, &flag); else chol_diag8_v3(Mp, d, rep & 7, rd, &flag);
     __syncwarp();
   }
   long long t1 = clock64();
@@ -126,15 +169,15 @@ int main() {
   static double h[8192];
   for (int i = 0; i < d; ++i) for (int j = 0; j <= i; ++j) h[i * (i + 1) / 2 + j] = (i == j) ? 100.0 + i : 1.0 / (1 + i + j);
   double* g; long long* o; cudaMalloc(&g, 8192 * 8); cudaMalloc(&o, 64);
-  double rd0[64], rd1[64], rd2[64];
-  for (int v = 0; v < 3; ++v) {
+  double rd0[64], rd1[64], rd2[64], rd3[64];
+  for (int v = 0; v < 4; ++v) {
     cudaMemcpy(g, h, 8192 * 8, cudaMemcpyHostToDevice);
     k<<<1, 32>>>(v, g, o);
     cudaDeviceSynchronize();
-    cudaMemcpy(v == 2 ? rd2 : (v ? rd1 : rd0), g + 4096, 64 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(v == 3 ? rd3 : v == 2 ? rd2 : (v ? rd1 : rd0), g + 4096, 64 * 8, cudaMemcpyDeviceToHost);
   }
-  long long c[3]; cudaMemcpy(c, o, 24, cudaMemcpyDeviceToHost);
-  double mx = 0, mx2 = 0; for (int i = 0; i < 64; ++i) { mx = fmax(mx, fabs(rd0[i] - rd1[i])); mx2 = fmax(mx2, fabs(rd0[i] - rd2[i]) / fabs(rd0[i])); }
-  printf("diag8 v0 %lld cycles, v1 %lld cycles, v2 %lld cycles, v1 diff %.3e, v2 rel diff %.3e\n", c[0], c[1], c[2], mx, mx2);
+  long long c[4]; cudaMemcpy(c, o, 32, cudaMemcpyDeviceToHost);
+  double mx = 0, mx2 = 0, mx3 = 0; for (int i = 0; i < 64; ++i) { mx3 = fmax(mx3, fabs(rd3[i] - rd1[i])); mx = fmax(mx, fabs(rd0[i] - rd1[i])); mx2 = fmax(mx2, fabs(rd0[i] - rd2[i]) / fabs(rd0[i])); }
+  printf("diag8 v0 %lld cycles, v1 %lld cycles, v2 %lld cycles, v3 %lld cycles, v1 diff %.3e, v2 rel diff %.3e, v3-v1 diff %.3e\n", c[0], c[1], c[2], c[3], mx, mx2, mx3);
   return 0;
 }
