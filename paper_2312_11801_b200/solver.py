@@ -443,7 +443,6 @@ class DeviceSolver:
         self.nu_b = rt.empty(m)
         self.ax = rt.empty(m)
         self.ycand = rt.empty(m)
-        self.img_b = rt.empty(m)
         d = k * (k + 1) // 2
         self.d = d
         self.Q11 = rt.empty(d, d)
@@ -645,9 +644,10 @@ class DeviceSolver:
         CF = self.tmp_nk2[:, :kc]
         eng.apply(0, F, CF)
         eng.wcoldot(F, CF, lamc, self.sc[S_CFIP:S_CFIP + 1])
-        img_new = self.img_b
+        # every model owns its image (the reference's BundleModel owns its
+        # arrays): a fresh tensor, never the previous model's or the caller's
+        img_new = rt.empty(self.m)
         eng.image(F, lamc, img_new, s_is_diag=True, beta=eta, base=model.stats.constr_image_dev)
-        self.img_b = model.stats.constr_image_dev  # ping-pong
         if model.store is not None:
             model.store.update(eta, F, lamc)
         if kp == 0:
@@ -754,15 +754,19 @@ class DeviceSolver:
                 state.null_steps += 1
             step = "descent" if accept else "null"
             model, pending = self.model_update(model, eta_act, eig.eigenvectors_dev, tag=t + 1)
-            primal = AggregateStats(tr_x, c_x, self.ax)
+            # records handed to a callback own their m-vectors (the solver's
+            # scratch and the y ping-pong buffers are reused by later iterations)
+            own = (lambda v: v.clone()) if callback is not None else (lambda v: v)
+            primal = AggregateStats(tr_x, c_x, own(self.ax))
             residuals = self.residuals(y, f_y, lam_y, primal, pending=pending, model=model)
             state.y_dev, state.f_y, state.lam_y, state.model = y, f_y, lam_y, model
             state.last_primal, state.residuals, state.iterations = primal, residuals, t + 1
             state.best_rel_infeas = min(state.best_rel_infeas, residuals.rel_infeas)
             state.best_rel_subopt = min(state.best_rel_subopt, residuals.rel_subopt)
             if callback is not None:
-                callback(IterationInfo(t, time.monotonic() - t_start, step, f_y, f_cand, model_val, y, self.ycand,
-                                       nu_keep, residuals, primal, eta_act, lam_c, state, model, passes,
+                callback(IterationInfo(t, time.monotonic() - t_start, step, f_y, f_cand, model_val, own(y),
+                                       own(self.ycand), own(nu_keep), residuals, primal, eta_act, lam_c, state,
+                                       model, passes,
                                        eig.matvecs, eig.restarts))
             t += 1
             if residuals.converged(cfg.eps, cfg.linf_check):
