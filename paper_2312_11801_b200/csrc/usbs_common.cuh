@@ -130,6 +130,16 @@ struct usbs_problem {
   int* lz_split_row = nullptr;    //   row, first piece, piece count
   int* lz_split_first = nullptr;
   int* lz_split_cnt = nullptr;
+  // TMA-pipelined grid Lanczos plan (usbs_lanczos_grid.cu), built on first use
+  std::vector<int32_t> h_rowptr;  // host copy of rowptr (the plan's input)
+  int lzg_ready = 0, lzg_G = 0, lzg_npieces = 0, lzg_nsplit = 0;
+  int* lzg_blk_row = nullptr;
+  int* lzg_blk_item = nullptr;
+  int4* lzg_items = nullptr;
+  int* lzg_split_row = nullptr;
+  int* lzg_split_first = nullptr;
+  int* lzg_split_cnt = nullptr;
+  int* lzg_blk_split = nullptr;
   std::vector<void*> owned;
 };
 

@@ -36,64 +36,11 @@
 #include "usbs_jacobi.cuh"
 #include "usbs_tridiag.cuh"
 #include "usbs_kernels.cuh"
+#include "usbs_lanczos.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace usbs {
-
-enum LzFlag { F_EXIT = 0, F_J = 1, F_CYCLE = 2, F_ELL = 3, F_RESTARTS = 4, F_CONV = 5, F_NHIST = 6,
-              F_MATVECS = 7, F_NONFINITE = 8, F_PENDING = 9 };
-enum LzExit { EXIT_DONE = 0, EXIT_BREAKDOWN = 1, EXIT_NONFINITE = 2 };
-
-struct LzArgs {
-  int n, m, k_c, max_restarts;
-  int64_t ldq;  // row stride of W0/W1 (>= n)
-  double tol;
-  const int* rowptr;
-  const int* col;
-  const double* val;
-  const int* blk_row;  // block b owns rows [blk_row[b], blk_row[b+1]) (Q passes)
-  const int* blk_seg;  // ... and SpMV segments [blk_seg[b], blk_seg[b+1]) (nnz-balanced)
-  const int* seg_r0;   // segment: rows [seg_r0, seg_r1), <= LZT_NNZ nonzeros,
-  const int* seg_r1;   //   or (seg_r1 < 0) piece -seg_r1-1 of a longer row
-  const int* piece_z0;  // nonzero range of each piece
-  const int* piece_z1;
-  double* piece_sum;    // partial sum of each piece
-  const int* blk_split;  // row block b's split rows [blk_split[b], blk_split[b+1])
-  const int* split_row;
-  const int* split_first;
-  const int* split_cnt;
-  double* Q;
-  double* W0;
-  double* W1;
-  double* H;
-  double* P1;  // [64][G] column partials, P1[t * G + b]
-  double* P2;  // [64][G]
-  double* P3;  // [G]
-  int* flags;
-  double* theta;  // [m]   output (after the last Rayleigh-Ritz)
-  double* Y;      // [m*m] output
-  double* res;    // [m]
-  double* hist;   // [max_restarts + 1]
-  // resume state
-  int cycle0, ell0, j0, restarts0, nhist0, matvecs0, wbuf0;
-  double beta_prev;  // beta of the step before j0 (only used if first step gathers from W)
-  int first_from_q;  // 1: q_{j0} is materialised in Q (start/restart/reseed)
-  double* vecs_out;  // n x k_c row-major (written when done)
-  int64_t ldvecs;
-  unsigned long long* prof;  // optional phase timer accumulators (ns), block 0
-};
-
-// Q element (row i, column t) in the row-blocked layout
-__host__ __device__ __forceinline__ int64_t qidx(int64_t i, int t, int M1) {
-  return ((i >> 5) * M1 + t) * 32 + (i & 31);
-}
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // phase timers (block 0, thread 0): 0 phase A work, 1 grid barriers,
 // 2 phase B work, 3 phase C work, 4 end-of-cycle, 5 Rayleigh-Ritz, 6 restart
@@ -1511,6 +1458,13 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   double* tmp = (double*)ctx->ws.get(WS_LZ_TMP, (size_t)(ldq + 128) * sizeof(double));
   USBS_CUDA(cudaMemsetAsync(H, 0, (size_t)(m + 1) * (m + 1) * sizeof(double), st));
   USBS_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), st));
+  // padding rows of the last 32-row tile stay zero (the TMA variant streams
+  // whole tiles), as do the padding rows of W
+  if (n % 32) {
+    USBS_CUDA(cudaMemsetAsync(Q + (n / 32) * (m + 1) * 32, 0, (size_t)(m + 1) * 32 * sizeof(double), st));
+    USBS_CUDA(cudaMemsetAsync(W + n, 0, (size_t)(ldq - n) * sizeof(double), st));
+    USBS_CUDA(cudaMemsetAsync(W + ldq + n, 0, (size_t)(ldq - n) * sizeof(double), st));
+  }
   {
     int bl0 = (int)std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms);
     k_qcol_set<<<bl0, 256, 0, st>>>(n, v0, 1.0, Q, 0, m + 1);
@@ -1523,7 +1477,14 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   a.rowptr = p->rowptr; a.col = p->col; a.val = val;
   a.blk_row = p->blk_row; a.blk_seg = p->blk_seg; a.seg_r0 = p->seg_r0; a.seg_r1 = p->seg_r1;
   a.piece_z0 = p->lz_piece_z0; a.piece_z1 = p->lz_piece_z1;
-  a.piece_sum = (double*)ctx->ws.get(WS_LZ_SPLIT, (size_t)std::max(1, p->lz_npieces) * sizeof(double));
+  // small operators: one thread-block cluster with Q resident in smem; large
+  // ones: the TMA-pipelined grid kernel (m <= 32) or the v1 grid kernel
+  const LzClusterPlan clp = lz_cached_plan(ctx, p, m);
+  const char* ev1 = getenv("USBS_LZ_V1");
+  const bool use_tma = clp.cs == 0 && m <= 32 && !(ev1 && ev1[0] == '1');
+  if (use_tma) lz_tma_plan(ctx, p);
+  a.piece_sum = (double*)ctx->ws.get(
+      WS_LZ_SPLIT, (size_t)std::max(1, std::max(p->lz_npieces, use_tma ? p->lzg_npieces : 0)) * sizeof(double));
   a.blk_split = p->lz_blk_split; a.split_row = p->lz_split_row; a.split_first = p->lz_split_first;
   a.split_cnt = p->lz_split_cnt;
   a.Q = Q; a.W0 = W; a.W1 = W + ldq; a.H = H;
@@ -1547,12 +1508,17 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   size_t smem = (size_t)(nw * 32 * NH + 64 * 3 + 8 + 64 + m * m + 4 * m * m + 64 * 2 + 32) * sizeof(double) +
                 68 * sizeof(int) + JAC_PTAB_BYTES + (6 * 64) * sizeof(double) + 128 * sizeof(int) + 64 +
                 LZT_NNZ * sizeof(double) + (2 * LZT_ROWS + 2) * sizeof(int);
-  // small operators: one thread-block cluster with Q resident in smem
-  const LzClusterPlan clp = lz_cached_plan(ctx, p, m);
+  if (use_tma) {
+    // P partials are [32][G'] with the TMA plan's block count
+    const int Gt = p->lzg_G;
+    double* Pt = (double*)ctx->ws.get(WS_LZ_P, (size_t)(std::max(G, Gt) * 64 * 2 + std::max(G, Gt)) * sizeof(double));
+    a.P1 = Pt; a.P2 = Pt + Gt * 64; a.P3 = Pt + 2 * Gt * 64;
+  }
   int64_t ctr = 0;
   int* hf = ctx->pinned_i;
   for (;;) {
     if (clp.cs > 0) lz_cl_launch(ctx, a, clp);
+    else if (use_tma) lz_tma_launch(ctx, p, a);
     else if (NH == 1) lz_dispatch<1>(ctx, a, G, p->spmv_group, smem);
     else lz_dispatch<2>(ctx, a, G, p->spmv_group, smem);
     // flags and (speculatively) the results in one round trip

@@ -570,6 +570,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
 
   // --- upload
   p->rowptr = dev_upload(p, rp32.data(), rp32.size());
+  p->h_rowptr = rp32;
   p->col = dev_upload(p, col.data(), col.size());
   p->cval = dev_upload(p, cval.data(), cval.size());
   p->zval = dev_alloc<double>(p, p->nnz);
