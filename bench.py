@@ -434,7 +434,7 @@ def operator_apply(rt, dp, cfg_b, flush):
     info = dp.info()
     y = np.random.default_rng(1234).standard_normal(p.m) * 1e-3
     if dp.has_ineq:
-        y[dp.ineq_idx] = -np.abs(y[dp.ineq_idx])
+        y[dp.ineq_idx] = np.abs(y[dp.ineq_idx])
     dp.assemble(rt.upload(y))
     out = {"n": p.n, "nnz_z": info.nnz_z}
     peak, _ = peaks()

@@ -200,7 +200,9 @@ usbs_status usbs_wcoldot(usbs_ctx* ctx, int64_t n, const double* f_dev, int64_t 
 usbs_status usbs_dense_update(usbs_ctx* ctx, int64_t n, double* x_dev, double eta,
                               const double* f_dev, int64_t ldf, int kc, const double* l_dev);
 /* m-vector operations (op codes in csrc/usbs_book.cu VecOp); red_out (dev, 2)
- * receives [sum, max] reductions where the op defines them. */
+ * receives [sum, max] reductions where the op defines them.  Ops 10/11 are the
+ * two reductions of psi_value (subqp.py:546-549): <b + nu - a_x, y> and
+ * ||b + nu - a_x||^2 with x = a_x, z = nu. */
 usbs_status usbs_vec(usbs_ctx* ctx, int op, int64_t m, const double* x, const double* y,
                      const double* z, const double* b, const double* ineq, double s0, double s1,
                      double* out, double* red_out);

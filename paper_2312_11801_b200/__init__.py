@@ -39,6 +39,7 @@ _LAZY = {
     "DeviceProblem": ("runtime", "DeviceProblem"),
     "ipm_quad": ("subproblem", "ipm_quad"),
     "ipm_eval": ("subproblem", "ipm_eval"),
+    "psi_value": ("subproblem", "psi_value"),
     "maxcut_round": ("rounding", "maxcut_round"),
     "DeviceConstraints": ("constraints", "DeviceConstraints"),
     "orthonormalize": ("linalg", "orthonormalize"),

@@ -75,7 +75,8 @@ PROTOS = {
 }
 
 # VecOp codes (csrc/usbs_book.cu)
-VOP_W, VOP_PROJN, VOP_AXPBY, VOP_NUNEXT, VOP_CAND, VOP_RESID, VOP_DOT, VOP_MINI, VOP_RELU, VOP_DOTAFF = range(10)
+VOP_W, VOP_PROJN, VOP_AXPBY, VOP_NUNEXT, VOP_CAND, VOP_RESID, VOP_DOT, VOP_MINI, VOP_RELU, VOP_DOTAFF, VOP_PSIWY, \
+    VOP_PSIWW = range(12)
 
 # symbols declared in include/usbs_b200.h that must be exported (checked by tests)
 _lib = None

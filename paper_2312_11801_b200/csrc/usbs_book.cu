@@ -512,6 +512,8 @@ enum VecOp {
   VOP_MINI = 7,      // red1 = min over ineq of x  (stored as max of -x)
   VOP_RELU = 8,      // out = max(x, 0)
   VOP_DOTAFF = 9,    // red_out[0] = s0 * sum x*y + s1   (only one slot written)
+  VOP_PSIWY = 10,    // red0 += (b + z - x) * y   (psi_value, subqp.py:546-549: w = b + nu - a_x)
+  VOP_PSIWW = 11,    // red0 += (b + z - x)^2
 };
 
 // x, y, z are operand vectors; red: per-block partials [nb][2]
@@ -551,6 +553,12 @@ __global__ void k_vec(int op, int64_t m, const double* __restrict__ x, const dou
       }
       case VOP_DOT:
       case VOP_DOTAFF: r0 = fma(x[i], y[i], r0); break;
+      case VOP_PSIWY: r0 = fma(b[i] + z[i] - x[i], y[i], r0); break;  // <b + nu - a_x, y>
+      case VOP_PSIWW: {                                             // ||b + nu - a_x||^2
+        const double w = b[i] + z[i] - x[i];
+        r0 = fma(w, w, r0);
+        break;
+      }
       case VOP_RELU: out[i] = fmax(x[i], 0.0); break;
       case VOP_MINI:
         if (iq) r1 = fmax(r1, -x[i]);
@@ -916,11 +924,7 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
   const int dg = gram_out ? 1 : 0;
 #define USBS_COMP(T)                                                                                      \
   {                                                                                                       \
-    static bool attr = false;                                                                             \
-    if (!attr) {                                                                                          \
-      USBS_CUDA(cudaFuncSetAttribute(k_compressed<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
-      attr = true;                                                                                        \
-    }                                                                                                     \
+    smem_optin(ctx, (const void*)k_compressed<T>, 200 * 1024);                                            \
     k_compressed<T><<<nb, 256, sm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row,  \
                                                   p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, dg, gpart, \
                                                   apart, wpart);                                          \
@@ -932,11 +936,7 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
     const size_t smm = (size_t)(CTR * (d + 1 + ((8 - (d + 1)) & 15)) + 2 * CTR) * sizeof(double) + 1200 + 2 * nt8 + 16;
 #define USBS_COMP_MMA(T, HY)                                                                               \
   {                                                                                                        \
-    static bool attr = false;                                                                              \
-    if (!attr) {                                                                                           \
-      USBS_CUDA(cudaFuncSetAttribute(k_compressed_mma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
-      attr = true;                                                                                         \
-    }                                                                                                      \
+    smem_optin(ctx, (const void*)k_compressed_mma<T>, 200 * 1024);                                         \
     k_compressed_mma<T><<<dim3(nb, HY), 512, smm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row, \
                                                        p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, gpart, \
                                                        apart, wpart);                                      \

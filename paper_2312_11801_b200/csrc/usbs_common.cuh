@@ -6,6 +6,9 @@
 #include <string>
 #include <vector>
 #include <unordered_map>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/usbs_b200.h"
 
@@ -169,6 +172,19 @@ T* dev_alloc(usbs_problem* p, size_t count) {
 }
 
 inline void note_launch(usbs_ctx* c, int n = 1) { c->launches += n; }
+
+// Large dynamic shared memory opt-in for kernel `fn` on the context's device.
+// cudaFuncSetAttribute acts on the current device only, so the opt-in is
+// recorded per (kernel, device); thread-safe.
+inline void smem_optin(const usbs_ctx* c, const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> g(mu);
+  const auto key = std::make_pair(fn, c->device * 1048576 + bytes);
+  if (done.count(key)) return;
+  USBS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(key);
+}
 
 inline void check_launch(usbs_ctx* c) {
   note_launch(c);

@@ -798,11 +798,7 @@ size_t ipm_smem_bytes(int k) {
 }
 
 void launch_ipm(usbs_ctx* ctx, const IpmArgs& a) {
-  static bool attr = false;
-  if (!attr) {
-    USBS_CUDA(cudaFuncSetAttribute(k_ipm, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  smem_optin(ctx, (const void*)k_ipm, 227 * 1024);
   size_t sm = ipm_smem_bytes(a.k);
   IpmArgs b = a;
   k_ipm<<<1, IPM_THREADS, sm, ctx->stream>>>(b);

@@ -1198,11 +1198,7 @@ static size_t eigh_smem(int n) {
 
 void launch_small_eigh(usbs_ctx* ctx, int k, const double* a, double* vals, double* vecs) {
   size_t sm = eigh_smem(k);
-  static bool attr = false;
-  if (!attr) {
-    USBS_CUDA(cudaFuncSetAttribute(k_small_eigh, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_optin(ctx, (const void*)k_small_eigh, 200 * 1024);
   k_small_eigh<<<1, 256, sm, ctx->stream>>>(k, a, vals, vecs);
   check_launch(ctx);
 }
@@ -1210,11 +1206,7 @@ void launch_small_eigh(usbs_ctx* ctx, int k, const double* a, double* vals, doub
 template <int LG, int NH>
 static void lz_launch(usbs_ctx* ctx, LzArgs& a, int G, size_t smem) {
   auto fn = k_lanczos<LG, NH>;
-  static bool attr = false;
-  if (!attr) {
-    USBS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_optin(ctx, (const void*)fn, 200 * 1024);
   const int threads = NH == 1 ? 512 : 256;
   int per_sm = 0;
   USBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
@@ -1417,16 +1409,12 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   const int m = std::max(std::max(inner_iters, k_c + 1), 2);
   if (k_c >= n || inner_iters >= n || m >= n) {
     // dense fallback
-    if (n > 40) fail(USBS_ERR_CONFIG, "dense Lanczos fallback supports n <= 40");
+    if (n > 64) fail(USBS_ERR_CONFIG, "dense Lanczos fallback supports n <= 64");
     int* nf = (int*)ctx->ws.get(WS_LZ_FLAGS, 64 * sizeof(int));
     USBS_CUDA(cudaMemsetAsync(nf, 0, sizeof(int), st));
     double* dv = (double*)ctx->ws.get(WS_LZ_OUT, 64 * sizeof(double));
     const int k = (int)std::min<int64_t>(k_c, n);
-    static bool attr = false;
-    if (!attr) {
-      USBS_CUDA(cudaFuncSetAttribute(k_dense_eigh, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    smem_optin(ctx, (const void*)k_dense_eigh, 200 * 1024);
     k_dense_eigh<<<1, 256, eigh_smem((int)n), st>>>((int)n, p->rowptr, p->col, val, k, dv, vecs_dev, ldvecs, nf);
     check_launch(ctx);
     USBS_CUDA(cudaMemcpyAsync(ctx->pinned, dv, k * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -809,7 +809,7 @@ template <int NCW, int SEG, bool ALIAS>
 static void lz_tma_launch_t(usbs_ctx* ctx, usbs_problem* p, LzArgs& a) {
   auto fn = k_lanczos_tma<NCW, SEG, ALIAS>;
   const size_t smem = lz_tma_smem(NCW, SEG, ALIAS);
-  USBS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin(ctx, (const void*)fn, (int)smem);
   int per_sm = 0;
   USBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LG_THREADS, smem));
   const int G = p->lzg_G;

@@ -303,7 +303,8 @@ class PrimalOutput:
 
 
 # scalar slots of the device scratch vector
-S_Q22, S_LINETA, S_EQ22, S_ELINETA, S_DNU, S_CQS, S_BYC, S_RES, S_BY, S_MINI, S_CFIP = 0, 1, 2, 3, 4, 6, 8, 10, 12, 14, 16
+S_Q22, S_LINETA, S_EQ22, S_ELINETA, S_DNU, S_CQS, S_BYC, S_RES, S_BY, S_MINI, S_CFIP, S_PSI = (0, 1, 2, 3, 4, 6, 8, 10, 12,
+                                                                           14, 16, 20)
 
 
 def orthonormalize_dev(eng: Engine, A, drop_tol: float = 1e-12):
@@ -433,6 +434,13 @@ class DeviceSolver:
         self.k_p = min(cfg.k_p, self.n_global - self.k_c)
         k = self.k_c + self.k_p
         self.k = k
+        # device limits, checked up front (not at the first subproblem):
+        # the k x k master problem (k_ipm) and the Lanczos basis (m <= 64)
+        if k > 32:
+            raise ValueError(f"k_c + k_p = {k} exceeds the device IPM limit of 32")
+        m_lz = max(int(lz.inner_iters), self.k_c + 1, 2)
+        if m_lz > 64 and m_lz < self.n_global:
+            raise ValueError(f"Lanczos basis size {m_lz} exceeds the device limit of 64")
         rt = self.rt
         n, m = self.n, self.m
         self.tmp_nk = rt.empty(n, max(k, 1))
@@ -577,9 +585,12 @@ class DeviceSolver:
                            scale_c=float(self.prob.scale_c))
 
     # ------------------------------------------------------------ subproblem
-    def alternating_max(self, model: BundleModel, y, nu0, max_passes=50, tol=1e-8):
+    def alternating_max(self, model: BundleModel, y, nu0, max_passes=50, tol=1e-8, psi_trace=None):
         """subqp.alternating_max (subqp.py:552-614) + assemble_quad_coeffs
-        (471-527): compressed Gram, C^T w, IPM and A(V S V^T) on device."""
+        (471-527): compressed Gram, C^T w, IPM and A(V S V^T) on device.
+        psi_trace (a list) receives psi_value (subqp.py:546-549) before and
+        after every nu update -- the reference's monotonicity check
+        (test_subqp.py:376-409); it costs host syncs, so only tests pass it."""
         eng, rt, sc = self.eng, self.rt, self.sc
         a, rho = self.alpha, float(self.cfg.rho)
         V = model.basis_dev
@@ -616,8 +627,16 @@ class DeviceSolver:
             eng.image(V, S, self.ax, s_scale=a, beta_dev=self.res_q[3:4] if has_eta else None,
                       beta=(a / tr) if has_eta else 0.0, base=img if has_eta else None)
             nxt = self.nu_b if nu is self.nu_a else self.nu_a
+            if psi_trace is not None:
+                from .subproblem import psi_value
+                eng.dot_into(self.cq.view(-1), self.st_q[:k * k], sc[S_PSI:S_PSI + 1], scale=a)
+                eta_act = a * float(self.res_q[3].item()) / tr if has_eta else 0.0
+                c_x = eta_act * model.stats.cost_ip + float(sc[S_PSI].item())
+                psi_trace.append(psi_value(self.dp, y, rho, c_x, self.ax, nu, engine=eng))
             eng.vec(N.VOP_NUNEXT, self.m, x=self.ax, y=y, z=nu, b=self.b, ineq=self.ineq, s0=rho, out=nxt,
                     red=sc[S_DNU:S_DNU + 2])
+            if psi_trace is not None:
+                psi_trace.append(psi_value(self.dp, y, rho, c_x, self.ax, nxt, engine=eng))
             nu = nxt
             if not self.has_ineq:
                 break

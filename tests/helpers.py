@@ -76,3 +76,15 @@ TRAJ_CFG = {
     "mixed40": dict(k_c=4, k_p=1, sketch_rank=4, max_iters=30),
     "qap4": dict(rho=0.005, k_c=4, k_p=0, sketch_rank=4, max_iters=20),
 }
+
+
+_BASELINE_CACHE: dict = {}
+
+
+def baseline_cached(name, small=False):
+    """instances.baseline_config, built once per test session (C4 and C5 take
+    seconds to tens of seconds on the host)."""
+    key = (name, small)
+    if key not in _BASELINE_CACHE:
+        _BASELINE_CACHE[key] = inst.baseline_config(name, small=small)
+    return _BASELINE_CACHE[key]
