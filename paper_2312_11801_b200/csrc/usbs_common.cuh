@@ -7,7 +7,7 @@
 #include <vector>
 #include <unordered_map>
 #include <mutex>
-#include <set>
+#include <map>
 #include <utility>
 
 #include "../../include/usbs_b200.h"
@@ -175,15 +175,17 @@ inline void note_launch(usbs_ctx* c, int n = 1) { c->launches += n; }
 
 // Large dynamic shared memory opt-in for kernel `fn` on the context's device.
 // cudaFuncSetAttribute acts on the current device only, so the opt-in is
-// recorded per (kernel, device); thread-safe.
+// recorded per (kernel, device) as the largest size requested so far (the
+// attribute is an upper bound: raising it never breaks smaller launches);
+// thread-safe.
 inline void smem_optin(const usbs_ctx* c, const void* fn, int bytes) {
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, int> done;
   std::lock_guard<std::mutex> g(mu);
-  const auto key = std::make_pair(fn, c->device * 1048576 + bytes);
-  if (done.count(key)) return;
+  int& cur = done[std::make_pair(fn, c->device)];
+  if (bytes <= cur) return;
   USBS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done.insert(key);
+  cur = bytes;
 }
 
 inline void check_launch(usbs_ctx* c) {

@@ -9,6 +9,7 @@
 
 #include "usbs_common.cuh"
 #include "usbs_kernels.cuh"
+#include "usbs_tma.cuh"
 
 namespace usbs {
 
@@ -80,10 +81,125 @@ __global__ void k_gram_final(int nb, int ka, int kb, const double* __restrict__ 
   if (lane == 0) out[p] = sym ? 0.5 * (s + st) : s;
 }
 
+// TMA-fed Gram for 16-byte-aligned row-major operands: a block streams its
+// row chunk in tiles of R rows through GB_S shared-memory stages (one
+// cp.async.bulk per operand per tile -- rows of a row-major block are one
+// contiguous range whatever the column count used -- completing on the
+// stage's mbarrier); 256 threads own 4 x 4 output blocks of A^T B for a
+// subset of rows each (register blocking: 16 FMAs per 8 shared loads); the
+// row groups are summed in fixed order at the end, then the blocks
+// (k_gram_final).  Memory-bound: (ka + kb) 8 bytes per row.
+constexpr int GB_S = 3;
+constexpr int GB_THREADS = 256;
+
+__global__ void __launch_bounds__(GB_THREADS, 2) k_gram_bulk(int64_t n, const double* __restrict__ A, int64_t lda,
+                                                          int ka, const double* __restrict__ B, int64_t ldb, int kb,
+                                                          int R, int64_t rows_per_block, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
+  const int stA = R * (int)lda, stB = R * (int)ldb;
+  const int stride = (stA + stB + 1) & ~1;
+  double* st = (double*)smem_raw;
+  uint64_t* bar = (uint64_t*)(st + GB_S * stride);
+  const int tid = threadIdx.x;
+  const int nt = r1 > r0 ? (int)((r1 - r0 + R - 1) / R) : 0;
+  if (tid == 0) {
+    for (int s = 0; s < GB_S; ++s) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int t) {
+    const int s = t % GB_S;
+    const int64_t row = r0 + (int64_t)t * R;
+    const int rows = (int)min((int64_t)R, r1 - row);
+    const uint32_t na = (uint32_t)rows * (uint32_t)lda, nb = (uint32_t)rows * (uint32_t)ldb;
+    const uint32_t ba = (na * 8u) & ~15u, bb = (nb * 8u) & ~15u;
+    double* sa = st + s * stride;
+    double* sb = sa + stA;
+    fence_proxy_smem();  // this thread's earlier plain stores into the stage
+    mbar_expect_tx(bar + s, ba + bb);
+    if (ba) bulk_g2s(sa, A + row * lda, ba, bar + s);
+    if (bb) bulk_g2s(sb, B + row * ldb, bb, bar + s);
+    // an odd element count leaves the last element to a plain load
+    if (na & 1u) sa[na - 1] = A[row * lda + na - 1];
+    if (nb & 1u) sb[nb - 1] = B[row * ldb + nb - 1];
+  };
+  if (tid == 0)
+    for (int t = 0; t < GB_S && t < nt; ++t) issue(t);
+  const int cbA = (ka + 3) >> 2, cbB = (kb + 3) >> 2, nob = cbA * cbB;
+  const int nrg = GB_THREADS / nob;
+  const int ob = tid % nob, rg = tid / nob;
+  const bool act = rg < nrg;
+  const int ia = (ob / cbB) * 4, ib = (ob % cbB) * 4;
+  double acc[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    const int s = t % GB_S;
+    mbar_wait(bar + s, (uint32_t)(t / GB_S) & 1u);
+    __syncthreads();  // the odd-element plain loads of this stage (thread 0)
+    const double* sa = st + s * stride;
+    const double* sb = sa + stA;
+    const int rows = (int)min((int64_t)R, r1 - (r0 + (int64_t)t * R));
+    if (act) {
+      for (int r = rg; r < rows; r += nrg) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          av[u] = ia + u < ka ? sa[r * lda + ia + u] : 0.0;
+          bv[u] = ib + u < kb ? sb[r * ldb + ib + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u * 4 + v] = fma(av[u], bv[v], acc[u * 4 + v]);
+      }
+    }
+    __syncthreads();  // stage s free
+    if (tid == 0 && t + GB_S < nt) issue(t + GB_S);
+  }
+  // fixed-order sum over the row groups (stage memory reused)
+  double* red = st;
+  const int np = ka * kb;
+  if (act)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (ia + u < ka && ib + v < kb) red[rg * np + (ia + u) * kb + ib + v] = acc[u * 4 + v];
+  __syncthreads();
+  for (int p = tid; p < np; p += GB_THREADS) {
+    double sm = 0.0;
+    for (int g = 0; g < nrg; ++g) sm += red[g * np + p];
+    part[(int64_t)blockIdx.x * np + p] = sm;
+  }
+}
+
 void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B, int64_t ldb,
                     int kb, double* out, bool sym) {
   if (ka < 1 || kb < 1 || ka > 64 || kb > 64) fail(USBS_ERR_SHAPE, "gram: 1 <= k <= 64");
   if (sym && ka != kb) fail(USBS_ERR_SHAPE, "gram: symmetric output needs ka == kb");
+  const char* eg = getenv("USBS_GRAM_V1");
+  if (n >= 1024 && lda <= 128 && ldb <= 128 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0 &&
+      !(eg && eg[0] == '1')) {
+    int R = (int)std::min<int64_t>(128, std::max<int64_t>(16, 4096 / (lda + ldb)));
+    R &= ~15;
+    int nb = (int)std::min<int64_t>(2 * ctx->num_sms, (n + R - 1) / R);
+    int64_t rpb = ((n + nb - 1) / nb + R - 1) / R * R;
+    nb = (int)((n + rpb - 1) / rpb);
+    const int stride = (int)((R * (lda + ldb) + 1) & ~1);
+    const size_t sm = (size_t)GB_S * stride * sizeof(double) + GB_S * sizeof(uint64_t);
+    const int nob = ((ka + 3) / 4) * ((kb + 3) / 4);
+    if ((size_t)(GB_THREADS / nob) * ka * kb <= (size_t)GB_S * stride) {
+      smem_optin(ctx, (const void*)k_gram_bulk, (int)sm);
+      double* part = (double*)ctx->ws.get(WS_GRAM_PARTIAL, (size_t)nb * ka * kb * sizeof(double));
+      k_gram_bulk<<<nb, GB_THREADS, sm, ctx->stream>>>(n, A, lda, ka, B, ldb, kb, R, rpb, part);
+      check_launch(ctx);
+      k_gram_final<<<(ka * kb + 7) / 8, 256, 0, ctx->stream>>>(nb, ka, kb, part, out, sym ? 1 : 0);
+      check_launch(ctx);
+      return;
+    }
+  }
   // one block per SM for n >= 148 * 64 rows, else a 64-row chunk per block:
   // the partial pass is latency-bound per tile, so short chunks win
   int nb = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + 63) / 64));
