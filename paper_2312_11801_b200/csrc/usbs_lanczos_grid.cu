@@ -56,7 +56,6 @@ namespace usbs {
 constexpr int LG_THREADS = 512;
 constexpr int LG_WARPS = LG_THREADS / 32;
 constexpr int LG_CONS = LG_WARPS - 1;  // SpMV warps (warp 15 keeps the block's bookkeeping)
-constexpr int LG_SPW = 2;              // slots per consuming warp
 constexpr int LG_SLOT = 32 * 32;       // doubles per slot: 32 rows x <= 32 columns
 constexpr int LG_SEGROWS = 64;         // rows per SpMV item (2 per lane)
 constexpr int LG_SHORT = 32;           // rows up to this long: summed by one lane
@@ -98,7 +97,7 @@ struct LgPass {
     }                                                   \
   } while (0)
 
-template <int NCW, int LG_SEG, bool ALIAS>
+template <int NCW, int LG_SEG, bool ALIAS, int LG_SPW>
 __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
   constexpr int RING = NCW * LG_SPW;
   constexpr int STG = LG_CONS * LG_SEG > LG_RRS ? LG_CONS * LG_SEG : LG_RRS;  // staging doubles
@@ -674,8 +673,8 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
   }
 }
 
-static size_t lz_tma_smem(int ncw, int seg, bool alias) {
-  const int ring = ncw * LG_SPW, stg = std::max(LG_CONS * seg, LG_RRS);
+static size_t lz_tma_smem(int ncw, int seg, bool alias, int spw) {
+  const int ring = ncw * spw, stg = std::max(LG_CONS * seg, LG_RRS);
   const int scr = alias ? LG_YS : stg + LG_YS;
   return (size_t)(ring * LG_SLOT + scr + 32 + 32 + LG_WARPS * 32 + 8) * sizeof(double) + ring * sizeof(uint64_t);
 }
@@ -683,9 +682,11 @@ static size_t lz_tma_smem(int ncw, int seg, bool alias) {
 struct LgVariant {
   int ncw, seg;
   bool alias;
+  int spw;
 };
 static LgVariant lz_tma_variant() {
-  static const LgVariant v[] = {{8, 512, true}, {9, 512, true}, {10, 512, true}, {8, 512, false}, {6, 512, true}};
+  static const LgVariant v[] = {{16, 512, true, 1}, {15, 512, true, 1}, {12, 512, true, 1}, {8, 512, true, 2},
+                                {10, 512, true, 1}};
   int i = 0;
   if (const char* e = getenv("USBS_LZG_VARIANT")) i = std::max(0, std::min(4, atoi(e)));
   return v[i];
@@ -709,7 +710,7 @@ void lz_tma_plan(usbs_ctx* ctx, usbs_problem* p) {
   int G = (int)std::min<int64_t>(std::max(1, ctx->num_sms - 4), ntile);
   if (const char* e = getenv("USBS_LZG_BLOCKS")) G = std::max(1, std::min<int>(ctx->num_sms, atoi(e)));
   G = (int)std::min<int64_t>(G, ntile);
-  double row_cost = 2.0, item_cost = 256.0, long_cost = 64.0;
+  double row_cost = 1.0, item_cost = 16.0, long_cost = 64.0;  // fitted to per-block timers (profiles/lz_spmv_fit.py)
   if (const char* e = getenv("USBS_LZG_ROWCOST")) row_cost = atof(e);
   if (const char* e = getenv("USBS_LZG_ITEMCOST")) item_cost = atof(e);
   if (const char* e = getenv("USBS_LZG_LONGCOST")) long_cost = atof(e);
@@ -774,10 +775,10 @@ void lz_tma_plan(usbs_ctx* ctx, usbs_problem* p) {
   p->lzg_ready = LG_SEG;
 }
 
-template <int NCW, int SEG, bool ALIAS>
+template <int NCW, int SEG, bool ALIAS, int SPW>
 static void lz_tma_launch_t(usbs_ctx* ctx, usbs_problem* p, LzArgs& a) {
-  auto fn = k_lanczos_tma<NCW, SEG, ALIAS>;
-  const size_t smem = lz_tma_smem(NCW, SEG, ALIAS);
+  auto fn = k_lanczos_tma<NCW, SEG, ALIAS, SPW>;
+  const size_t smem = lz_tma_smem(NCW, SEG, ALIAS, SPW);
   smem_optin(ctx, (const void*)fn, (int)smem);
   int per_sm = 0;
   USBS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LG_THREADS, smem));
@@ -798,11 +799,11 @@ void lz_tma_launch(usbs_ctx* ctx, usbs_problem* p, LzArgs& a) {
   a.gsplit_cnt = p->lzg_split_cnt;
   a.blk_gsplit = p->lzg_blk_split;
   const LgVariant v = lz_tma_variant();
-  if (v.ncw == 9) lz_tma_launch_t<9, 512, true>(ctx, p, a);
-  else if (v.ncw == 8 && v.alias) lz_tma_launch_t<8, 512, true>(ctx, p, a);
-  else if (v.ncw == 8) lz_tma_launch_t<8, 512, false>(ctx, p, a);
-  else if (v.ncw == 10) lz_tma_launch_t<10, 512, true>(ctx, p, a);
-  else lz_tma_launch_t<6, 512, true>(ctx, p, a);
+  if (v.ncw == 8) lz_tma_launch_t<8, 512, true, 2>(ctx, p, a);
+  else if (v.ncw == 15) lz_tma_launch_t<15, 512, true, 1>(ctx, p, a);
+  else if (v.ncw == 12) lz_tma_launch_t<12, 512, true, 1>(ctx, p, a);
+  else if (v.ncw == 16) lz_tma_launch_t<16, 512, true, 1>(ctx, p, a);
+  else lz_tma_launch_t<10, 512, true, 1>(ctx, p, a);
 }
 
 }  // namespace usbs
