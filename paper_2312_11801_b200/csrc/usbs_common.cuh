@@ -65,6 +65,8 @@ struct usbs_ctx {
   usbs::Workspace ws;
   double* pinned = nullptr;  // 4096 doubles of pinned host scratch
   int* pinned_i = nullptr;   // 256 ints
+  unsigned char* stage[2] = {nullptr, nullptr};  // pinned upload staging (lazy)
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 struct usbs_problem {
@@ -152,12 +154,16 @@ namespace usbs {
 constexpr int LZT_NNZ = 4096;
 constexpr int LZT_ROWS = 2048;
 
+// Host -> device copy through two pinned staging chunks (host memcpy of one
+// chunk overlaps the DMA of the other); small arrays go directly.
+void staged_h2d(usbs_ctx* ctx, void* dst, const void* src, size_t bytes);
+
 template <typename T>
 T* dev_upload(usbs_problem* p, const T* host, size_t count) {
   T* d = nullptr;
   size_t bytes = count * sizeof(T);
   USBS_CUDA(cudaMalloc(&d, bytes < 16 ? 16 : bytes));
-  if (count) USBS_CUDA(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+  if (count) staged_h2d(p->ctx, d, host, bytes);
   p->owned.push_back(d);
   return d;
 }

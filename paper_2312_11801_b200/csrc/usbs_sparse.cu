@@ -8,13 +8,42 @@
 //   problem.py:284-286  cost_quad = sym(V^T C V)
 //   subqp.py:459        V^T A*(y) V - V^T C V  (= -sym(V^T Z V))
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <thread>
 
 #include "usbs_common.cuh"
 #include "usbs_kernels.cuh"
+
+namespace usbs {
+void staged_h2d(usbs_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  constexpr size_t CH = 8u << 20;
+  if (bytes <= (1u << 20)) {
+    USBS_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (!ctx->stage[k]) {
+      USBS_CUDA(cudaMallocHost(&ctx->stage[k], CH));
+      USBS_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[k], cudaEventDisableTiming));
+    }
+  size_t off = 0;
+  int k = 0;
+  while (off < bytes) {
+    const size_t len = std::min(CH, bytes - off);
+    USBS_CUDA(cudaEventSynchronize(ctx->stage_ev[k]));  // the chunk's previous copy has drained
+    std::memcpy(ctx->stage[k], (const unsigned char*)src + off, len);
+    USBS_CUDA(cudaMemcpyAsync((unsigned char*)dst + off, ctx->stage[k], len, cudaMemcpyHostToDevice, ctx->stream));
+    USBS_CUDA(cudaEventRecord(ctx->stage_ev[k], ctx->stream));
+    off += len;
+    k ^= 1;
+  }
+  USBS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace usbs
 
 namespace usbs {
 
@@ -287,6 +316,10 @@ usbs_status usbs_ctx_destroy(usbs_ctx* c) {
   if (!c) return USBS_OK;
   cudaStreamSynchronize(c->stream);
   c->ws.release();
+  for (int k = 0; k < 2; ++k) {
+    if (c->stage[k]) cudaFreeHost(c->stage[k]);
+    if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);
+  }
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->pinned_i) cudaFreeHost(c->pinned_i);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -319,6 +352,7 @@ usbs_status usbs_memcpy_d2h(usbs_ctx* c, void* dst, const void* src, int64_t byt
   }
   USBS_API_END
 }
+
 
 static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, const int64_t* c_indptr,
                            const int32_t* c_indices, const double* c_data, int64_t ne, const int64_t* e_idx,
@@ -353,6 +387,15 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   if (n < 1 || n_cols < 1 || m < 0 || ne < 0) fail(USBS_ERR_SHAPE, "invalid problem dimensions");
   if (n >= (1LL << 31) - 1 || n_cols >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "n exceeds int32 indexing");
   USBS_CUDA(cudaSetDevice(ctx->device));
+  // USBS_PLAN_PROF=1: host planning phase times on stderr
+  const bool tprof = getenv("USBS_PLAN_PROF") != nullptr;
+  auto tlast = std::chrono::steady_clock::now();
+  auto PT = [&](const char* what) {
+    if (!tprof) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[plan] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tlast).count());
+    tlast = now;
+  };
   auto* p = new usbs_problem();
   p->ctx = ctx;
   p->n = n;
@@ -377,66 +420,105 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   for (int64_t i = 0; i < n; ++i) xcnt[i + 1] += xcnt[i];
   std::vector<int32_t> xcol(xcnt[n]);
   std::vector<int64_t> xent(xcnt[n]);
+  std::vector<int64_t> xpos_r(ne), xpos_c(ne, -1);  // x-positions of each entry (slot -> entries below)
   {
     std::vector<int64_t> pos(xcnt.begin(), xcnt.end() - 1);
     for (int64_t e = 0; e < ne; ++e) {
       int64_t r = e_rows[e], c = e_cols[e];
+      xpos_r[e] = pos[r];
       xcol[pos[r]] = (int32_t)c;
       xent[pos[r]++] = e;
       if (!directed && r != c) {
+        xpos_c[e] = pos[c];
         xcol[pos[c]] = (int32_t)r;
         xent[pos[c]++] = e;
       }
     }
   }
-  // --- merge per row: C columns (sorted copy) with the extra columns
+  PT("constraint entries -> rows");
+  // --- merge per row: C columns (sorted, duplicates summed) with the extra
+  // columns.  Two passes over row ranges on host threads: merged lengths,
+  // then the merged pattern written in place (same result as a serial merge).
   std::vector<int64_t> rowptr(n + 1, 0);
+  std::vector<int64_t> slot_of_x(xcnt[n]);
+  const int nthr = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
+                                                              n / 4096 + 1));
   std::vector<int32_t> col;
   std::vector<double> cval;
-  std::vector<int64_t> slot_of_x(xcnt[n]);
-  col.reserve(p->nnz_c + xcnt[n]);
-  cval.reserve(p->nnz_c + xcnt[n]);
-  std::vector<std::pair<int32_t, double>> crow;
-  std::vector<std::pair<int32_t, int64_t>> xrow;
-  for (int64_t i = 0; i < n; ++i) {
-    crow.clear();
-    for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) {
-      if (c_indices[z] < 0 || c_indices[z] >= n_cols) fail(USBS_ERR_SHAPE, "cost column index out of range");
-      crow.emplace_back(c_indices[z], c_data[z]);
-    }
-    if (!std::is_sorted(crow.begin(), crow.end(),
-                        [](auto& a, auto& b) { return a.first < b.first; }))
-      std::stable_sort(crow.begin(), crow.end(), [](auto& a, auto& b) { return a.first < b.first; });
-    xrow.clear();
-    for (int64_t t = xcnt[i]; t < xcnt[i + 1]; ++t) xrow.emplace_back(xcol[t], t);
-    std::stable_sort(xrow.begin(), xrow.end(), [](auto& a, auto& b) { return a.first < b.first; });
-    size_t a = 0, b = 0;
-    while (a < crow.size() || b < xrow.size()) {
-      int32_t cc = INT32_MAX;
-      if (a < crow.size()) cc = crow[a].first;
-      if (b < xrow.size()) cc = std::min(cc, xrow[b].first);
-      double v = 0.0;
-      while (a < crow.size() && crow[a].first == cc) v += crow[a++].second;  // duplicate C entries summed
-      int64_t s = (int64_t)col.size();
-      while (b < xrow.size() && xrow[b].first == cc) slot_of_x[xrow[b++].second] = s;
-      col.push_back(cc);
-      cval.push_back(v);
-    }
-    rowptr[i + 1] = (int64_t)col.size();
+  {
+    std::vector<std::string> errs(nthr);
+    auto merge_rows = [&](int th, int64_t i0, int64_t i1, bool write) {
+      std::vector<std::pair<int32_t, double>> crow;
+      std::vector<std::pair<int32_t, int64_t>> xrow;
+      for (int64_t i = i0; i < i1; ++i) {
+        crow.clear();
+        for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) {
+          if (c_indices[z] < 0 || c_indices[z] >= n_cols) {
+            errs[th] = "cost column index out of range";
+            return;
+          }
+          crow.emplace_back(c_indices[z], c_data[z]);
+        }
+        if (!std::is_sorted(crow.begin(), crow.end(), [](auto& a, auto& b) { return a.first < b.first; }))
+          std::stable_sort(crow.begin(), crow.end(), [](auto& a, auto& b) { return a.first < b.first; });
+        xrow.clear();
+        for (int64_t t = xcnt[i]; t < xcnt[i + 1]; ++t) xrow.emplace_back(xcol[t], t);
+        if (xrow.size() > 1)
+          std::stable_sort(xrow.begin(), xrow.end(), [](auto& a, auto& b) { return a.first < b.first; });
+        size_t a = 0, b = 0;
+        int64_t o = write ? rowptr[i] : 0;
+        while (a < crow.size() || b < xrow.size()) {
+          int32_t cc = INT32_MAX;
+          if (a < crow.size()) cc = crow[a].first;
+          if (b < xrow.size()) cc = std::min(cc, xrow[b].first);
+          double v = 0.0;
+          while (a < crow.size() && crow[a].first == cc) v += crow[a++].second;  // duplicate C entries summed
+          while (b < xrow.size() && xrow[b].first == cc) {
+            if (write) slot_of_x[xrow[b].second] = o;
+            ++b;
+          }
+          if (write) {
+            col[o] = cc;
+            cval[o] = v;
+          }
+          ++o;
+        }
+        if (!write) rowptr[i + 1] = o;  // row length (prefix-summed below)
+      }
+    };
+    auto run = [&](bool write) {
+      std::vector<std::thread> ts;
+      for (int th = 0; th < nthr; ++th) {
+        const int64_t i0 = n * th / nthr, i1 = n * (th + 1) / nthr;
+        ts.emplace_back(merge_rows, th, i0, i1, write);
+      }
+      for (auto& t : ts) t.join();
+      for (auto& e : errs)
+        if (!e.empty()) fail(USBS_ERR_SHAPE, e);
+    };
+    run(false);
+    for (int64_t i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
+    col.resize(rowptr[n]);
+    cval.resize(rowptr[n]);
+    run(true);
   }
+  PT("merge C with the entries");
   p->nnz = (int64_t)col.size();
   if (p->nnz >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "nnz exceeds int32 indexing");
-  // --- slot -> entries (ascending entry id within a slot)
+  // --- slot -> entries (ascending entry id within a slot): counting pass
+  // over the entries in order
   std::vector<int32_t> aptr(p->nnz + 1, 0);
   for (int64_t t = 0; t < (int64_t)slot_of_x.size(); ++t) aptr[slot_of_x[t] + 1]++;
   for (int64_t s = 0; s < p->nnz; ++s) aptr[s + 1] += aptr[s];
   std::vector<int32_t> aent(aptr[p->nnz]);
   {
-    std::vector<std::pair<int64_t, int64_t>> tmp(slot_of_x.size());
-    for (int64_t t = 0; t < (int64_t)slot_of_x.size(); ++t) tmp[t] = {slot_of_x[t], xent[t]};
-    std::sort(tmp.begin(), tmp.end());
-    for (size_t t = 0; t < tmp.size(); ++t) aent[t] = (int32_t)tmp[t].second;
+    std::vector<int32_t> cur(aptr.begin(), aptr.end() - 1);
+    for (int64_t e = 0; e < ne; ++e) {
+      aent[cur[slot_of_x[xpos_r[e]]]++] = (int32_t)e;
+      if (xpos_c[e] >= 0) aent[cur[slot_of_x[xpos_c[e]]]++] = (int32_t)e;
+    }
   }
+  PT("slot -> entries");
   std::vector<int32_t> rp32(n + 1);
   for (int64_t i = 0; i <= n; ++i) rp32[i] = (int32_t)rowptr[i];
 
@@ -464,6 +546,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->n_split_items = nsplit;
   p->n_split_rows = (int)srow.size();
 
+  PT("SpMM work items");
   // --- Lanczos grid partition: rows for the Q passes, SpMV segments apart
   // leave 4 SMs free for kernels that overlap the Lanczos kernel (the
   // model-evaluation IPM on the auxiliary stream)
@@ -556,6 +639,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     }
     for (int bb = sb + 1; bb <= G; ++bb) blk_seg[bb] = (int32_t)ns;
   }
+  PT("v1 Lanczos partition");
   std::vector<int32_t> diag_slot;
   if (p->diag_only) {
     if (m != n || ne != n) fail(USBS_ERR_SHAPE, "diag_only requires m == n == entries");
@@ -568,6 +652,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     for (int64_t i = 0; i < n; ++i) diag_slot[i] = (int32_t)slot_of_x[xcnt[i]];
   }
 
+  PT("diag slots");
   // --- upload
   p->rowptr = dev_upload(p, rp32.data(), rp32.size());
   p->h_rowptr = rp32;
@@ -644,6 +729,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->blk_seg = dev_upload(p, blk_seg.data(), blk_seg.size());
   p->seg_r0 = dev_upload(p, seg_r0.data(), seg_r0.size());
   p->seg_r1 = dev_upload(p, seg_r1.data(), seg_r1.size());
+  PT("uploads + tiles + lists");
   *out = p;
 }
 

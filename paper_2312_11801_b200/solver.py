@@ -114,11 +114,22 @@ class Residuals:
         return ok
 
 
+_PSI_POOL = None
+
+
+def _psi_async(n, r, seed, r0, r1):
+    global _PSI_POOL
+    if _PSI_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _PSI_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="usbs-psi")
+    return _PSI_POOL.submit(lambda: np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))[r0:r1])
+
+
 class DeviceSketchStore:
     """SketchStore + sketch.py on the device: P (n x r), Psi (n x r)."""
 
     def __init__(self, eng: Engine, n: int, r: int, seed: int, psi_host: Optional[np.ndarray] = None,
-                 rows: Optional[tuple] = None, shard=None, comm=None):
+                 rows: Optional[tuple] = None, shard=None, comm=None, psi_job=None):
         """n is the global dimension; rows = (r0, r1) selects this rank's
         block of Psi and P when the problem is row-sharded."""
         if not 1 <= r <= n:
@@ -127,11 +138,27 @@ class DeviceSketchStore:
         self.shard, self.comm = shard, comm
         r0, r1 = rows if rows is not None else (0, n)
         rt = eng.rt
-        if psi_host is None:  # make_test_matrix (sketch.py:25-27): legacy MT19937, host once
-            psi_host = np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))[r0:r1]
-        self.psi = rt.upload(psi_host)
+        self._psi = None
+        self._psi_job = None
+        if psi_job is not None:
+            self._psi_job = psi_job
+        elif psi_host is None:
+            # make_test_matrix (sketch.py:25-27): legacy MT19937 normals on the
+            # host (bit-exact with the reference), generated on a worker thread
+            # (numpy releases the GIL while filling) so it overlaps the cold
+            # start; joined at the first use
+            self._psi_job = _psi_async(n, r, seed, r0, r1)
+        else:
+            self._psi = rt.upload(psi_host)
         self.P = rt.zeros(r1 - r0, r)
         self.G = rt.empty(64, max(r, 1))
+
+    @property
+    def psi(self):
+        if self._psi is None:
+            self._psi = self.eng.rt.upload(self._psi_job.result())
+            self._psi_job = None
+        return self._psi
 
     def update(self, eta: float, F, lams) -> None:
         """sketch_update with Q = I (sketch.py:58-74): P <- eta P + (F L)(F^T Psi)."""
@@ -404,6 +431,13 @@ class DeviceSolver:
     def __init__(self, prob, cfg, dprob: Optional[DeviceProblem] = None, comm=None, engine=None):
         self.prob = prob
         self.cfg = cfg
+        # the sketch test matrix (host, legacy MT19937) is generated while the
+        # problem is uploaded and planned and the cold-start Lanczos runs
+        self._psi_job = None
+        if getattr(cfg, "sketch_rank", 0) > 0 and (dprob is None or getattr(dprob, "shard", None) is None):
+            n0 = int(prob.n)
+            self._psi_job = _psi_async(n0, min(int(cfg.sketch_rank), n0),
+                                       int(np.random.SeedSequence(int(cfg.seed)).generate_state(2)[0]), 0, n0)
         self.dp = dprob or DeviceProblem(prob)
         self.comm = comm
         self.eng = engine or Engine(self.dp, comm)
@@ -552,8 +586,9 @@ class DeviceSolver:
         basis = self.completion(eig.eigenvectors_dev, self.k, tag=0)
         stats = AggregateStats(0.0, 0.0, rt.zeros(self.m))
         if self.cfg.sketch_rank > 0:
+            job, self._psi_job = self._psi_job, None
             store = DeviceSketchStore(self.eng, self.n_global, min(self.cfg.sketch_rank, self.n_global), sketch_seed,
-                                      rows=(self.r0, self.r1), shard=self.shard, comm=self.comm)
+                                      rows=(self.r0, self.r1), shard=self.shard, comm=self.comm, psi_job=job)
         else:
             store = DeviceExplicitStore(self.eng, self.n)
         model = BundleModel(basis, stats, self.k_c, self.k_p, store)
