@@ -102,6 +102,14 @@ usbs_status usbs_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y_
 usbs_status usbs_op_apply(usbs_ctx* ctx, usbs_problem* p, int which, const double* v_dev,
                           int64_t ldv, int k, double* y_dev, int64_t ldy, double* gram_dev);
 
+/* Kronecker-structured cost (build_qap, problem.py:462-477): C = coef *
+ * (0 (+) D (x) W) with composite index a = i*l + k (problem.py:364-371),
+ * D, W host l x l row-major, n = l^2 + 1.  op_apply then runs C V as the
+ * contraction coef * D X W^T on the FP64 tensor cores (mma.sync m8n8k4) and
+ * Z V as that minus a sparse pass over A*(y) (USBS_KRON=0 disables it). */
+usbs_status usbs_problem_set_kron(usbs_ctx* ctx, usbs_problem* p, int l, const double* d_host,
+                                  const double* w_host, double coef);
+
 /* ---- K2/K3: thick-restart Lanczos --------------------------------------- */
 /* Host callback producing the PCG64 stream of eigsolve._seeded_unit for a
  * counter (eigsolve.py:49-52) into a device n-vector (unnormalised normals).

@@ -99,8 +99,14 @@ def ref_problem(cfg_name: str):
         g = inst.chung_lu(20_000, seed=3)
         gi = sbp.GraphInstance.from_edges(g.n, list(zip(g.eu.tolist(), g.ev.tolist(), g.ew.tolist())))
         return sbp.build_maxcut(gi)
-    if cfg_name == "C5s":
-        n, eu, ev, ew = inst.knn_correlation(n=3000, clusters=100, seed=4)
+    if cfg_name == "C4":
+        # full size: from_edges over the de-duplicated Chung-Lu edge list
+        g = inst.chung_lu(1_000_000, seed=3)
+        gi = sbp.GraphInstance.from_edges(g.n, list(zip(g.eu.tolist(), g.ev.tolist(), g.ew.tolist())))
+        return sbp.build_maxcut(gi)
+    if cfg_name in ("C5s", "C5"):
+        n, eu, ev, ew = (inst.knn_correlation(n=3000, clusters=100, seed=4) if cfg_name == "C5s"
+                         else inst.knn_correlation(seed=4))
         import scipy.sparse as sp
         cost = sp.coo_matrix((np.concatenate([ew, ew]), (np.concatenate([eu, ev]), np.concatenate([ev, eu]))),
                              shape=(n, n)).tocsr()
@@ -122,6 +128,20 @@ def mine_problem(cfg_name: str):
     if cfg_name == "C5s":
         return inst.baseline_config("C5", small=True).problem
     return inst.baseline_config(cfg_name).problem
+
+
+def builders_full():
+    """Full-size C4 (n = 10^6) and C5 (n = 63,000, m = 1.37 M) through the
+    reference builders (from_edges / build_from_families), hashed like
+    builders(); written to builders_full.json."""
+    rec = {}
+    for name in ("C4", "C5"):
+        rp = ref_problem(name)
+        rec[name] = problem_digest(rp)
+        md = problem_digest(mine_problem(name))
+        print(f"builders {name}: framework builder bit-exact vs reference = {md == rec[name]}", flush=True)
+        del rp
+    (OUT / "builders_full.json").write_text(json.dumps(rec, indent=1, sort_keys=True))
 
 
 def builders():
@@ -400,7 +420,7 @@ def state_cases():
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
     which = sys.argv[1:] or ["builders", "quad", "lanczos", "ipm", "cons", "sketch", "traj", "lockstep", "rounding", "state"]
-    fn = {"builders": builders, "quad": quad_oracle, "lanczos": lanczos_cases, "ipm": ipm_cases,
+    fn = {"builders": builders, "builders_full": builders_full, "quad": quad_oracle, "lanczos": lanczos_cases, "ipm": ipm_cases,
           "cons": cons_cases, "sketch": sketch_cases, "traj": trajectories, "lockstep": lockstep,
           "rounding": rounding_cases, "state": state_cases}
     for w in which:

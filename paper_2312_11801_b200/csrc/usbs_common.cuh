@@ -135,6 +135,12 @@ struct usbs_problem {
   int* lz_split_row = nullptr;    //   row, first piece, piece count
   int* lz_split_first = nullptr;
   int* lz_split_cnt = nullptr;
+  // Kronecker-structured cost (QAP, usbs_kron.cu): C = coef (0 (+) D (x) W)
+  int kron_l = 0;
+  double* kron_D = nullptr;
+  double* kron_W = nullptr;
+  double kron_coef = 0.0;
+  double* aval = nullptr;  // A*(y) on the merged pattern (set by slack assembly)
   // TMA-pipelined grid Lanczos plan (usbs_lanczos_grid.cu), built on first use
   std::vector<int32_t> h_rowptr;  // host copy of rowptr (the plan's input)
   int lzg_ready = 0, lzg_G = 0, lzg_npieces = 0, lzg_nsplit = 0;

@@ -33,6 +33,9 @@ void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int
 void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,
                       double* Y, int64_t ldy);
 void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, double* tval);
+bool kron_enabled(const usbs_problem* p);
+void launch_kron_apply(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k, double* Y, int64_t ldy,
+                       double beta);
 // out (ka x kb, row-major, dev) = A^T B for row-major n x ka A and n x kb B;
 // sym: out = 0.5 (G + G^T) (requires ka == kb)
 void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B,

@@ -762,7 +762,17 @@ usbs_status usbs_op_apply(usbs_ctx* ctx, usbs_problem* p, int which, const doubl
                           double* Y, int64_t ldy, double* gram) {
   USBS_API_BEGIN
   if (k < 1 || ldv < k || ldy < k) fail(USBS_ERR_SHAPE, "op_apply: bad k / leading dimension");
-  launch_spmm(ctx, p, which, V, ldv, k, Y, ldy);
+  if (kron_enabled(p)) {
+    // QAP cost on the FP64 tensor cores; Z V = C V - A*(y) V
+    if (which) {
+      launch_spmm_vals(ctx, p, p->aval, V, ldv, k, Y, ldy);
+      launch_kron_apply(ctx, p, V, ldv, k, Y, ldy, -1.0);
+    } else {
+      launch_kron_apply(ctx, p, V, ldv, k, Y, ldy, 0.0);
+    }
+  } else {
+    launch_spmm(ctx, p, which, V, ldv, k, Y, ldy);
+  }
   if (gram) launch_gram_tn(ctx, p->n, V, ldv, k, Y, ldy, k, gram, true);
   USBS_API_END
 }
@@ -783,6 +793,7 @@ void launch_slack_assemble(usbs_ctx* ctx, usbs_problem* p, const double* y) {
                                                               p->e_val, y, p->zval);
     check_launch(ctx);
   }
+  if (p->kron_l) launch_adjoint_values(ctx, p, y, p->aval);  // the sparse part of Z V on the Kronecker path
 }
 
 void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int64_t ldv, int k,

@@ -202,6 +202,7 @@ class Problem:
     sense: int = 1
     labels: Optional[list] = None
     op_norm_estimate: Optional[float] = None
+    kron_factors: Optional[tuple] = None  # (D, W): cost = -(0 (+) D (x) W) / scale_c (QAP)
 
     def __post_init__(self):
         self.b = np.asarray(self.b, dtype=float)
@@ -322,7 +323,8 @@ def qap_problem(q: Qap, alpha: float = 2.0) -> Problem:
         ops = ops.scaled(np.full(m, 1.0 / op_norm))
         b = b / op_norm
     return Problem(n=big, m=m, cost=cost, constraints=ops, b=b, ineq_mask=ineq, alpha=alpha,
-                   scale_c=scale_c, scale_x=scale_x, sense=-1, op_norm_estimate=op_norm)
+                   scale_c=scale_c, scale_x=scale_x, sense=-1, op_norm_estimate=op_norm,
+                   kron_factors=(np.asarray(q.distances, dtype=float), np.asarray(q.weights, dtype=float)))
 
 
 def family_problem(n, cost_raw, triples, b_raw, ineq_mask, alpha=2.0, scale_x=1.0) -> Problem:
