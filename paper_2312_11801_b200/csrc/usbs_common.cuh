@@ -135,6 +135,10 @@ struct usbs_problem {
   int* lz_split_row = nullptr;    //   row, first piece, piece count
   int* lz_split_first = nullptr;
   int* lz_split_cnt = nullptr;
+  // tiled SpMM plan (usbs_spmm.cu), built per tile size on first use
+  int spt_T = 0, spt_ntiles = 0, spt_nch = 0, spt_nhuge = 0;
+  int *spt_r0 = nullptr, *spt_r1 = nullptr, *spt_z0 = nullptr, *spt_z1 = nullptr;
+  int *spt_hrow = nullptr, *spt_hfirst = nullptr, *spt_hcnt = nullptr;
   // Kronecker-structured cost (QAP, usbs_kron.cu): C = coef (0 (+) D (x) W)
   int kron_l = 0;
   double* kron_D = nullptr;

@@ -34,6 +34,9 @@ void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const d
                       double* Y, int64_t ldy);
 void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, double* tval);
 bool kron_enabled(const usbs_problem* p);
+bool spmm_tiles_ok(const usbs_problem* p, int k);
+void launch_spmm_tiles(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,
+                       double* Y, int64_t ldy);
 void launch_kron_apply(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k, double* Y, int64_t ldy,
                        double beta);
 // out (ka x kb, row-major, dev) = A^T B for row-major n x ka A and n x kb B;

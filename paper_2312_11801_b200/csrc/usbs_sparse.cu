@@ -824,6 +824,10 @@ void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, doub
 
 void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,
                       double* Y, int64_t ldy) {
+  if (spmm_tiles_ok(p, k)) {  // block CSR-stream SpMM (usbs_spmm.cu; A/B via USBS_SPMM_V1=0)
+    launch_spmm_tiles(ctx, p, val, V, ldv, k, Y, ldy);
+    return;
+  }
   double* partial = nullptr;
   if (p->n_split_items) partial = (double*)ctx->ws.get(WS_SPMM_PARTIAL, (size_t)p->n_split_items * k * sizeof(double));
   const int th = 256;

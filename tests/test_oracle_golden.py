@@ -151,3 +151,13 @@ def test_lockstep_snapshot_c1():
     assert r.model_val == float(z["n_model_val"])
     np.testing.assert_array_equal(r.y_cand, z["n_y_cand"])
     np.testing.assert_array_equal(r.primal.constr_image, z["n_image"])
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_builders_full_size_bit_exact(name):
+    """Full-size C4 (n = 10^6 through GraphInstance.from_edges, problem.py:67-87)
+    and C5 (n = 63,000, m = 1.37 M through build_from_families,
+    problem.py:509-539): every array hash-equal to the reference builders'
+    (builders_full.json, recorded by oracle/make_golden.py builders_full)."""
+    ref = json.loads((GOLDEN / "builders_full.json").read_text())[name]
+    assert digest(inst.baseline_config(name).problem) == ref
