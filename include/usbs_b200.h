@@ -111,6 +111,17 @@ usbs_status usbs_problem_set_kron(usbs_ctx* ctx, usbs_problem* p, int l, const d
                                   const double* w_host, double coef);
 
 /* ---- K2/K3: thick-restart Lanczos --------------------------------------- */
+/* Row-sharded Lanczos (dist.lanczos_sharded; eigsolve.py:125-176 per rank):
+ * the epilogue of step j on the device -- H[:j+1, j] = c1 + c2, beta =
+ * sqrt(nrm2) into H[j+1, j], q_{j+1} = w / beta on the local rows (zero on
+ * breakdown), flags[0] = first breakdown step (beta <= 1e-13 max(1, max|c|),
+ * eigsolve.py:136-147), flags[1] |= non-finite -- and the thick-restart reset
+ * H = diag(theta[:ell]).  c1, c2, nrm2 are the allreduced (replicated) CGS2
+ * coefficients and norm; no host reads inside a cycle. */
+usbs_status usbs_lz_step_finish(usbs_ctx* ctx, int j, int m1, const double* c1_dev, const double* c2_dev,
+                                const double* nrm2_dev, double* h_dev, int* flags_dev, const double* w_dev,
+                                int64_t nl, int64_t ldw, double* q_dev, int64_t ldq);
+usbs_status usbs_lz_restart_h(usbs_ctx* ctx, int m1, int ell, const double* theta_dev, double* h_dev);
 /* Host callback producing the PCG64 stream of eigsolve._seeded_unit for a
  * counter (eigsolve.py:49-52) into a device n-vector (unnormalised normals).
  * Returns 0 on success. */

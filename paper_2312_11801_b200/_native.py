@@ -44,6 +44,8 @@ PROTOS = {
     "usbs_problem_info": (_i32, [_p, C.POINTER(_i64), C.POINTER(_i64), _pi, _pi]),
     "usbs_slack_assemble": (_i32, [_p, _p, _p]),
     "usbs_problem_set_kron": (_i32, [_p, _p, _i32, _p, _p, C.c_double]),
+    "usbs_lz_step_finish": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _p, _p, _i64, _i64, _p, _i64]),
+    "usbs_lz_restart_h": (_i32, [_p, _i32, _i32, _p, _p]),
     "usbs_op_apply": (_i32, [_p, _p, _i32, _p, _i64, _i32, _p, _i64, _p]),
     "usbs_lanczos_top": (_i32, [_p, _p, _i32, _i32, _i32, _i32, C.c_double, _p, RNG_FILL, _p,
                                  _pd, _p, _i64, _pd, _pi, _pi, _pd, _pi, _pi]),

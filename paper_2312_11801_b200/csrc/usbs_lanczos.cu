@@ -1128,6 +1128,56 @@ __global__ void k_scale_into(int64_t n, const double* __restrict__ v, double s, 
     out[i] = v[i] * s;
 }
 
+// ---- row-sharded Lanczos (dist.py): one step's epilogue on the device, so a
+// cycle issues no host reads.  c1, c2: the allreduced CGS2 coefficients
+// (j+1 each), nrm2 = ||w''||^2 allreduced.  Writes H[:j+1, j] = c1 + c2
+// (symmetric), beta = ||w''|| into H[j+1, j] (0 on breakdown), the local
+// rows of q_{j+1} = w'' / beta (0 on breakdown) and flags[0] = first breakdown
+// step (eigsolve.py:136-147: beta <= 1e-13 max(1, max|c|)), flags[1] |= a
+// non-finite matvec (eigsolve.py:128-129).
+__global__ void k_lz_step_finish(int j, int m1, const double* __restrict__ c1, const double* __restrict__ c2,
+                                 const double* __restrict__ nrm2, double* __restrict__ H, int* __restrict__ flags,
+                                 const double* __restrict__ w, int64_t nl, int64_t ldw, double* __restrict__ q,
+                                 int64_t ldq) {
+  __shared__ double s_inv;
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    bool bad = false;
+    for (int t = 0; t <= j; ++t) {
+      const double c = c1[t] + c2[t];
+      if (!isfinite(c)) bad = true;
+      mx = fmax(mx, fabs(c));
+    }
+    const double beta = sqrt(fmax(nrm2[0], 0.0));
+    if (!isfinite(beta)) bad = true;
+    const bool brk = !(beta > 1e-13 * fmax(1.0, mx));
+    s_inv = brk ? 0.0 : 1.0 / beta;
+    if (blockIdx.x == 0) {
+      for (int t = 0; t <= j; ++t) {
+        const double c = c1[t] + c2[t];
+        H[(int64_t)t * m1 + j] = c;
+        H[(int64_t)j * m1 + t] = c;
+      }
+      H[(int64_t)(j + 1) * m1 + j] = brk ? 0.0 : beta;
+      H[(int64_t)j * m1 + j + 1] = brk ? 0.0 : beta;
+      if (brk && flags[0] < 0) flags[0] = j;
+      if (bad) flags[1] = 1;
+    }
+  }
+  __syncthreads();
+  const double inv = s_inv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x)
+    q[i * ldq] = w[i * ldw] * inv;
+}
+
+// thick restart of the replicated H: H = diag(theta[:ell]) (eigsolve.py:175-176)
+__global__ void k_lz_restart_h(int m1, int ell, const double* __restrict__ theta, double* __restrict__ H) {
+  for (int x = threadIdx.x; x < m1 * m1; x += blockDim.x) {
+    const int r = x / m1, c = x % m1;
+    H[x] = (r == c && r < ell) ? theta[r] : 0.0;
+  }
+}
+
 // dense fallback (eigsolve.py:66-80): Z = M I densely, symmetrise, eigh
 __global__ void k_dense_eigh(int n, const int* __restrict__ rowptr, const int* __restrict__ col,
                              const double* __restrict__ val, int k, double* vals_out, double* vecs_out,
@@ -1383,6 +1433,24 @@ extern "C" usbs_status usbs_lanczos_plan(usbs_ctx* ctx, usbs_problem* p, int m, 
   const LzClusterPlan pl = (p->n_cols == p->n) ? lz_cached_plan(ctx, p, m) : LzClusterPlan{};
   *cluster_size = pl.cs;
   *rows_per_cta = pl.R;
+  USBS_API_END
+}
+
+extern "C" usbs_status usbs_lz_step_finish(usbs_ctx* ctx, int j, int m1, const double* c1, const double* c2,
+                                           const double* nrm2, double* H, int* flags, const double* w, int64_t nl,
+                                           int64_t ldw, double* q, int64_t ldq) {
+  USBS_API_BEGIN
+  if (j < 0 || j + 1 >= m1) fail(USBS_ERR_SHAPE, "lz_step_finish: 0 <= j < m");
+  const int bl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, 4 * ctx->num_sms));
+  k_lz_step_finish<<<bl, 256, 0, ctx->stream>>>(j, m1, c1, c2, nrm2, H, flags, w, nl, ldw, q, ldq);
+  check_launch(ctx);
+  USBS_API_END
+}
+
+extern "C" usbs_status usbs_lz_restart_h(usbs_ctx* ctx, int m1, int ell, const double* theta, double* H) {
+  USBS_API_BEGIN
+  k_lz_restart_h<<<1, 256, 0, ctx->stream>>>(m1, ell, theta, H);
+  check_launch(ctx);
   USBS_API_END
 }
 

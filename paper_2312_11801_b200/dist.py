@@ -351,14 +351,30 @@ class ShardedDeviceProblem:
 
 
 def lanczos_sharded(eng, dp, which: int, k_c: int, inner_iters: int = 32, max_restarts: int = 10,
-                    tol: Optional[float] = None, seed: int = 0, out=None):
-    """lanczos_top (eigsolve.py:83-181) on a row-sharded operator, host-driven
-    step by step on the engine's primitives (SpMV with allgather, allreduced
-    Grams, local row GEMMs).  Same m, ell, tolerance, breakdown and restart
-    rules as the single-GPU kernel; H and the Ritz data are replicated."""
+                    tol: Optional[float] = None, seed: int = 0, out=None, sync_guard=None):
+    """lanczos_top (eigsolve.py:83-181) on a row-sharded operator, device
+    resident: within a restart cycle every step is enqueued without a host
+    read -- SpMV on the local rows after an allgather of q_j, CGS2 with
+    allreduced coefficients (engine Grams), the allreduced norm and the step
+    epilogue on the device (usbs_lz_step_finish: H column, beta, q_{j+1},
+    breakdown / non-finite flags).  The host reads once per cycle (flags,
+    Ritz values, the last row of the Ritz vectors, beta_m) to take the
+    reference's decisions; a breakdown (flagged at the first step where
+    beta <= 1e-13 max(1, max|c|)) is replayed exactly: the fresh direction
+    of eigsolve.py:136-147 (PCG64 counters as the reference) replaces
+    q_{j+1} and the rest of the cycle is recomputed.  Same m, ell,
+    tolerance and restart rules as the single-GPU kernel; H and the Ritz
+    data are replicated (allreduced inputs, identical on every rank).
+
+    sync_guard: optional context-manager factory entered around each cycle's
+    steps (tests pass torch.cuda sync-debug mode "error" to prove the cycle
+    issues no synchronising call)."""
+    import contextlib
+
     from .eigen import EigResult
 
     rt = eng.rt
+    torch = rt.torch
     shard = dp.shard
     n = shard.n
     nl = dp.n
@@ -369,84 +385,101 @@ def lanczos_sharded(eng, dp, which: int, k_c: int, inner_iters: int = 32, max_re
         raise NotImplementedError("dense fallback (n <= inner_iters) is not sharded")
     tol = 1e-9 if tol is None else tol
     seed32 = int(seed) & 0xFFFFFFFF
+    m1 = m + 1
+    guard = sync_guard or contextlib.nullcontext
 
     def seeded(counter):
         g = np.random.default_rng([seed32, counter])
         v = g.standard_normal(n)
         return v / np.linalg.norm(v)
 
-    Q = rt.zeros(nl, m + 1)
-    h = np.zeros((m + 1, m + 1))
+    Q = rt.zeros(nl, m1)
+    H = rt.zeros(m1, m1)
+    flags = torch.full((2,), -1, dtype=torch.int32, device=rt.device)
+    flags[1] = 0
     Q[:, 0:1].copy_(rt.upload(seeded(0)[shard.r0: shard.r1].reshape(-1, 1)))
     xfull = rt.empty(n, 1)
     w = rt.empty(nl, 1)
-    cvec = rt.empty(m + 1, 1)
+    c1b, c2b = rt.empty(m1, 1), rt.empty(m1, 1)
     red = rt.zeros(2)
+    hm = rt.empty(m, m)
+    vals, vecs = rt.empty(m), rt.empty(m, m)
     ell, ctr, hist, conv, restarts, mv = 0, 0, [], False, 0, 0
-    theta, ymat, res = np.zeros(m), np.eye(m), np.full(m, np.inf)
+    theta, res = np.zeros(m), np.full(m, np.inf)
+    ell_next = max(1, min(k_c + 3, m - 2))
+    nwant = min(m, max(ell_next, k_c))
 
-    def proj_out(v, used):
-        """v -= Q[:, :used] (Q[:, :used]^T v), allreduced coefficients."""
-        cv = cvec[:used]
+    def steps(j0):
+        with guard():
+            for j in range(j0, m):
+                dp.apply(which, Q[:, j: j + 1], out=w, xfull=xfull)
+                c1 = c1b[: j + 1]
+                eng.gram(Q[:, : j + 1], w, c1)
+                eng.rowgemm(Q[:, : j + 1], c1, w, alpha=-1.0, beta=1.0, Y0=w)
+                c2 = c2b[: j + 1]
+                eng.gram(Q[:, : j + 1], w, c2)
+                eng.rowgemm(Q[:, : j + 1], c2, w, alpha=-1.0, beta=1.0, Y0=w)
+                eng.dot_into(w.view(-1), w.view(-1), red[0:1])
+                eng.lz_step_finish(j, m1, c1, c2, red[0:1], H, flags, w, Q[:, j + 1: j + 2])
+
+    def proj_norm(v, used):
+        """v -= Q[:, :used] (Q[:, :used]^T v) (allreduced); returns ||v||."""
+        cv = c1b[:used]
         eng.gram(Q[:, :used], v, cv)
         eng.rowgemm(Q[:, :used], cv, v, alpha=-1.0, beta=1.0, Y0=v)
-        return cv
-
-    def norm(v):
         eng.dot_into(v.view(-1), v.view(-1), red[0:1])
         return math.sqrt(max(float(red[0].item()), 0.0))
 
     for cyc in range(max_restarts + 1):
-        for j in range(ell, m):
-            dp.apply(which, Q[:, j: j + 1], out=w, xfull=xfull)
-            mv += 1
-            eng.dot_into(w.view(-1), w.view(-1), red[0:1])
-            if not math.isfinite(float(red[0].item())):
+        j0 = ell
+        while True:
+            steps(j0)
+            fl = flags.cpu().numpy()  # one host read per cycle (and per replayed breakdown)
+            if fl[1]:
                 raise NumericError("matvec returned non-finite values")
-            c1 = proj_out(w, j + 1).cpu().numpy().ravel().copy()
-            c2 = proj_out(w, j + 1).cpu().numpy().ravel().copy()
-            c = c1 + c2
-            h[: j + 1, j] = c
-            h[j, : j + 1] = c
-            beta = norm(w)
-            scale = max(1.0, float(np.max(np.abs(c))) if c.size else 0.0)
-            if beta <= 1e-13 * scale:
-                ctr += 16
-                got = False
-                for att in range(8):
-                    v = rt.upload(seeded(ctr + att + 1)[shard.r0: shard.r1].reshape(-1, 1))
-                    proj_out(v, j + 1)
-                    nv = norm(v)
-                    if nv > 1e-8:
-                        eng.rowgemm(v, rt.upload(np.ones((1, 1))), Q[:, j + 1: j + 2], alpha=1.0 / nv)
-                        got = True
-                        break
-                if not got:
-                    Q[:, j + 1: j + 2].zero_()
-                h[j + 1, j] = h[j, j + 1] = 0.0
-            else:
-                eng.rowgemm(w, rt.upload(np.ones((1, 1))), Q[:, j + 1: j + 2], alpha=1.0 / beta)
-                h[j + 1, j] = h[j, j + 1] = beta
-        hm = rt.upload(h[:m, :m])
-        vals, vecs = rt.empty(m), rt.empty(m, m)
+            jb = int(fl[0])
+            if jb < 0:
+                mv += m - j0
+                break
+            # breakdown at step jb: fresh direction for q_{jb+1}
+            # (eigsolve.py:136-147, _fresh_direction 55-63), then replay
+            mv += jb + 1 - j0
+            ctr += 16
+            got = False
+            for att in range(8):
+                v = rt.upload(seeded(ctr + att + 1)[shard.r0: shard.r1].reshape(-1, 1))
+                nv = proj_norm(v, jb + 1)
+                if nv > 1e-8:
+                    Q[:, jb + 1: jb + 2].copy_(v * (1.0 / nv))
+                    got = True
+                    break
+            if not got:
+                Q[:, jb + 1: jb + 2].zero_()
+            flags[0] = -1
+            if jb + 1 >= m:
+                break
+            j0 = jb + 1
+        hm.copy_(H[:m, :m])
         eng.small_eigh(hm, vals, vecs)
-        theta, ymat = vals.cpu().numpy(), vecs.cpu().numpy()
-        res = np.abs(h[m, m - 1] * ymat[m - 1, :])
+        pack = torch.cat([vals[:nwant], vecs[m - 1, :nwant], H[m, m - 1: m]]).cpu().numpy()
+        theta = pack[:nwant]
+        last = pack[nwant: 2 * nwant]
+        beta_last = float(pack[-1])
+        res = np.abs(beta_last * last)
         hist.append(float(theta[0]))
         if np.all(res[:k_c] <= tol * (1.0 + abs(float(theta[0])))):
             conv = True
             break
         if cyc == max_restarts:
             break
-        ell = max(1, min(k_c + 3, m - 2))
+        ell = ell_next
         kept = rt.empty(nl, ell)
-        eng.rowgemm(Q[:, :m], rt.upload(ymat[:, :ell]), kept)
+        eng.rowgemm(Q[:, :m], vecs[:, :ell], kept)
         Q[:, ell: ell + 1].copy_(Q[:, m: m + 1])
         Q[:, :ell].copy_(kept)
-        h[:, :] = 0.0
-        h[:ell, :ell] = np.diag(theta[:ell])
+        eng.lz_restart_h(m1, ell, vals, H)
         restarts += 1
     k = min(k_c, n)
     vecs_out = out if out is not None else rt.empty(nl, k)
-    eng.rowgemm(Q[:, :m], rt.upload(ymat[:, :k_c]), vecs_out)
-    return EigResult(theta[:k_c].copy(), vecs_out, res[:k_c].copy(), conv, restarts, hist, mv)
+    eng.rowgemm(Q[:, :m], vecs[:, :k_c], vecs_out)
+    return EigResult(np.asarray(theta[:k_c]).copy(), vecs_out, res[:k_c].copy(), conv, restarts, hist, mv)

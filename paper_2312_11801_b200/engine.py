@@ -75,6 +75,16 @@ class Engine:
         if self.comm is not None:
             self.comm.allreduce_sum(out[0:1])
 
+    # ---------------------------------------------------------------- sharded Lanczos
+    def lz_step_finish(self, j, m1, c1, c2, nrm2, H, flags, w, q):
+        """Step epilogue of the row-sharded Lanczos (usbs_lz_step_finish):
+        H column j, beta, q_{j+1} = w / beta on the local rows, flags."""
+        check(self.lib.usbs_lz_step_finish(self.h, int(j), int(m1), _p(c1), _p(c2), _p(nrm2), _p(H), _p(flags),
+                                           _p(w), w.shape[0], w.stride(0), _p(q), q.stride(0)), "lz_step_finish")
+
+    def lz_restart_h(self, m1, ell, theta, H):
+        check(self.lib.usbs_lz_restart_h(self.h, int(m1), int(ell), _p(theta), _p(H)), "lz_restart_h")
+
     def small_eigh(self, a, vals, vecs):
         check(self.lib.usbs_small_eigh(self.h, a.shape[0], _p(a), _p(vals), _p(vecs)), "small_eigh")
 

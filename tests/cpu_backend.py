@@ -186,6 +186,26 @@ class CpuEngine:
         out[0] = float(np.sum(F.numpy() * G.numpy() * w.numpy()[None, : F.shape[1]]))
         self._ar(out[0:1])
 
+    def lz_step_finish(self, j, m1, c1, c2, nrm2, H, flags, w, q):
+        c = (c1.reshape(-1) + c2.reshape(-1)).numpy()
+        beta = math.sqrt(max(float(nrm2.reshape(-1)[0]), 0.0))
+        bad = (not np.all(np.isfinite(c))) or not math.isfinite(beta)
+        mx = float(np.max(np.abs(c))) if c.size else 0.0
+        brk = not (beta > 1e-13 * max(1.0, mx))
+        H[: j + 1, j] = torch.from_numpy(c)
+        H[j, : j + 1] = torch.from_numpy(c)
+        H[j + 1, j] = H[j, j + 1] = 0.0 if brk else beta
+        if brk and int(flags[0]) < 0:
+            flags[0] = j
+        if bad:
+            flags[1] = 1
+        q.copy_(w * (0.0 if brk else 1.0 / beta))
+
+    def lz_restart_h(self, m1, ell, theta, H):
+        H.zero_()
+        for u in range(ell):
+            H[u, u] = theta[u]
+
     def small_eigh(self, a, vals, vecs):
         lam, q = O.eigh_desc(a.numpy())
         vals.copy_(torch.from_numpy(lam))

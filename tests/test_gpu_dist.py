@@ -149,3 +149,72 @@ def test_entry_shard_solve_world1_matches_single_gpu():
     f2 = np.array([r.f_y for r in rec2])
     np.testing.assert_allclose(f2[:4], f1[:4], rtol=1e-8)
     assert [r.step for r in rec1] == [r.step for r in rec2]
+
+
+class _ForcedComm:
+    """A Comm whose collectives always go through torch.distributed (a
+    one-rank NCCL group here), so the sharded Lanczos's allreduces and
+    allgathers really run on NCCL."""
+
+    def __init__(self):
+        from paper_2312_11801_b200.dist import Comm
+        self._c = Comm(2)  # world > 1: collectives issued
+        self.world = 1     # but the engine treats it as the (single) rank's communicator
+        self.group = None
+
+    def allreduce_sum(self, t):
+        import torch.distributed as dist
+        dist.all_reduce(t)
+        return t
+
+    def allreduce_max(self, t):
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t
+
+    def allgather_rows(self, local, out, shard):
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(out, local.contiguous())
+        return out
+
+
+def test_sharded_lanczos_cycle_issues_no_host_sync():
+    """within a restart cycle the sharded
+    Lanczos enqueues SpMV, NCCL allgather / allreduces and the step epilogue
+    without a synchronising call (torch sync-debug mode 'error' raises on any
+    .item() / .cpu() / blocking copy); results equal the oracle's."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_11801_b200.dist import ShardedDeviceProblem, Shard, lanczos_sharded
+    from paper_2312_11801_b200.engine import Engine
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29617")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    p = inst.baseline_config("C4", small=True).problem
+    shard = Shard.balanced(p.cost.indptr, 1, 0)
+    comm = _ForcedComm()
+    sdp = ShardedDeviceProblem(p, shard, comm)
+    eng = Engine(sdp, None)
+    eng.comm = comm  # collectives through NCCL
+    y = np.random.default_rng(4).standard_normal(p.m) * 1e-3
+    sdp.assemble(sdp.rt.upload(y))
+    torch.cuda.synchronize()
+
+    class Strict:
+        def __enter__(self):
+            torch.cuda.set_sync_debug_mode("error")
+
+        def __exit__(self, *exc):
+            torch.cuda.set_sync_debug_mode("default")
+
+    with Strict():  # the guard does catch a synchronising call
+        with pytest.raises(RuntimeError):
+            torch.ones(1, device="cuda").item()
+    r = lanczos_sharded(eng, sdp, 1, 10, seed=0, sync_guard=Strict)
+    ro = O.lanczos(O.slack_op(p, y), 10, seed=0)
+    assert r.restarts == ro.restarts and r.matvecs == ro.matvecs
+    np.testing.assert_allclose(r.eigenvalues, ro.eigenvalues, rtol=1e-12)
