@@ -19,26 +19,42 @@ namespace usbs {
 
 // ------------------------------------------------------------- K5 images
 // out[i] = beta*base[i] + A_i(V S V^T); S full k x k (sdiag=0) or diag (sdiag=1)
-__global__ void k_image_diag(int64_t n, const double* __restrict__ V, int64_t ldv, int k,
-                             const double* __restrict__ S, int sdiag, double sscale, const double* beta_dev,
-                             double beta, const double* __restrict__ base, double* __restrict__ out) {
-  __shared__ double Ss[64 * 64];
+__global__ void __launch_bounds__(256) k_image_diag(int64_t n, const double* __restrict__ V, int64_t ldv, int k,
+                                                    const double* __restrict__ S, int sdiag, double sscale,
+                                                    const double* beta_dev, double beta,
+                                                    const double* __restrict__ base, double* __restrict__ out) {
+  // the block's 256 rows are staged with coalesced loads (odd row stride in
+  // shared memory: conflict-free row reads), then a thread per row
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Ss = (double*)smem_raw;          // k * k
+  double* rows = Ss + k * k;               // 256 * kp
+  const int kp = k | 1;
   for (int x = threadIdx.x; x < (sdiag ? k : k * k); x += blockDim.x) Ss[x] = sscale * S[x];
   if (beta_dev) beta *= beta_dev[0];
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double* v = V + i * ldv;
-    double acc = 0.0;
-    if (sdiag) {
-      for (int j = 0; j < k; ++j) acc = fma(v[j] * v[j], Ss[j], acc);
-    } else {
-      for (int j = 0; j < k; ++j) {
-        double t = 0.0;
-        for (int l = 0; l < k; ++l) t = fma(Ss[j * k + l], v[l], t);
-        acc = fma(v[j], t, acc);
-      }
+  for (int64_t r0 = (int64_t)blockIdx.x * 256; r0 < n; r0 += (int64_t)gridDim.x * 256) {
+    const int nr = (int)min((int64_t)256, n - r0);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * k; x += blockDim.x) {
+      const int r = x / k, c = x - r * k;
+      rows[r * kp + c] = V[(r0 + r) * ldv + c];
     }
-    out[i] = (base ? beta * base[i] : 0.0) + acc;
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < nr) {
+      const double* v = rows + t * kp;
+      double acc = 0.0;
+      if (sdiag) {
+        for (int j = 0; j < k; ++j) acc = fma(v[j] * v[j], Ss[j], acc);
+      } else {
+        for (int j = 0; j < k; ++j) {
+          double tt = 0.0;
+          for (int l = 0; l < k; ++l) tt = fma(Ss[j * k + l], v[l], tt);
+          acc = fma(v[j], tt, acc);
+        }
+      }
+      const int64_t i = r0 + t;
+      out[i] = (base ? beta * base[i] : 0.0) + acc;
+    }
   }
 }
 
@@ -863,8 +879,10 @@ usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* V, int
   USBS_API_BEGIN
   if (k < 1 || k > 64) fail(USBS_ERR_SHAPE, "cons_image: 1 <= k <= 64");
   if (p->diag_only) {
-    k_image_diag<<<nblocks(ctx, p->n), 256, 0, ctx->stream>>>(p->n, V, ldv, k, S, s_is_diag, s_scale, beta_dev, beta,
-                                                              base, out);
+    const size_t smi = (size_t)(k * k + 256 * (k | 1)) * sizeof(double);
+    smem_optin(ctx, (const void*)k_image_diag, (int)smi);
+    const int bl = (int)std::max<int64_t>(1, std::min<int64_t>((p->n + 255) / 256, 8 * ctx->num_sms));
+    k_image_diag<<<bl, 256, smi, ctx->stream>>>(p->n, V, ldv, k, S, s_is_diag, s_scale, beta_dev, beta, base, out);
   } else {
     const double* W = nullptr;
     if (!s_is_diag) {
@@ -904,6 +922,21 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
       launch_adjoint_values(ctx, p, vec, tval);
       launch_spmm_vals(ctx, p, tval, V, ldv, k, Y, k);
       launch_gram_tn(ctx, p->n, V, ldv, k, Y, k, k, G, true);
+      k_svec<<<1, 256, 0, ctx->stream>>>(k, G, u ? scale_w : scale_a, u ? w_out : a_out);
+      check_launch(ctx);
+    }
+    a_vec = nullptr;
+    w_vec = nullptr;
+    if (!gram_out) return USBS_OK;
+  }
+  if (p->diag_only && p->n >= 1024 && (a_vec || w_vec) && ((uintptr_t)V & 15) == 0 && ldv <= 128) {
+    // diagonal constraints: sum_i v_i svec(v_i v_i^T) = svec(V^T diag(v) V),
+    // a row-weighted Gram on the TMA Gram kernel (O(n k^2), memory-bound)
+    double* G = (double*)ctx->ws.get(WS_BOOK_G, (size_t)k * k * sizeof(double));
+    for (int u = 0; u < 2; ++u) {
+      const double* vec = u ? w_vec : a_vec;
+      if (!vec) continue;
+      launch_gram_tn(ctx, p->n, V, ldv, k, V, ldv, k, G, true, vec);
       k_svec<<<1, 256, 0, ctx->stream>>>(k, G, u ? scale_w : scale_a, u ? w_out : a_out);
       check_launch(ctx);
     }

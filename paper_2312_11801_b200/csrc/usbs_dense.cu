@@ -94,7 +94,8 @@ constexpr int GB_THREADS = 256;
 
 __global__ void __launch_bounds__(GB_THREADS, 2) k_gram_bulk(int64_t n, const double* __restrict__ A, int64_t lda,
                                                           int ka, const double* __restrict__ B, int64_t ldb, int kb,
-                                                          int R, int64_t rows_per_block, double* __restrict__ part) {
+                                                          int R, int64_t rows_per_block, double* __restrict__ part,
+                                                          const double* __restrict__ rw) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
   const int stA = R * (int)lda, stB = R * (int)ldb;
@@ -142,11 +143,13 @@ __global__ void __launch_bounds__(GB_THREADS, 2) k_gram_bulk(int64_t n, const do
     const double* sb = sa + stA;
     const int rows = (int)min((int64_t)R, r1 - (r0 + (int64_t)t * R));
     if (act) {
+      const int64_t row0 = r0 + (int64_t)t * R;
       for (int r = rg; r < rows; r += nrg) {
         double av[4], bv[4];
+        const double wr = rw ? rw[row0 + r] : 1.0;  // optional row weights: A^T diag(rw) B
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          av[u] = ia + u < ka ? sa[r * lda + ia + u] : 0.0;
+          av[u] = ia + u < ka ? sa[r * lda + ia + u] * wr : 0.0;
           bv[u] = ib + u < kb ? sb[r * ldb + ib + u] : 0.0;
         }
 #pragma unroll
@@ -176,10 +179,12 @@ __global__ void __launch_bounds__(GB_THREADS, 2) k_gram_bulk(int64_t n, const do
 }
 
 void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B, int64_t ldb,
-                    int kb, double* out, bool sym) {
+                    int kb, double* out, bool sym, const double* rw) {
   if (ka < 1 || kb < 1 || ka > 64 || kb > 64) fail(USBS_ERR_SHAPE, "gram: 1 <= k <= 64");
   if (sym && ka != kb) fail(USBS_ERR_SHAPE, "gram: symmetric output needs ka == kb");
   const char* eg = getenv("USBS_GRAM_V1");
+  if (rw && !(n >= 1024 && lda <= 128 && ldb <= 128 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0))
+    fail(USBS_ERR_SHAPE, "weighted gram needs the TMA path (aligned operands, n >= 1024)");
   if (n >= 1024 && lda <= 128 && ldb <= 128 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0 &&
       !(eg && eg[0] == '1')) {
     int R = (int)std::min<int64_t>(128, std::max<int64_t>(16, 4096 / (lda + ldb)));
@@ -193,13 +198,14 @@ void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int 
     if ((size_t)(GB_THREADS / nob) * ka * kb <= (size_t)GB_S * stride) {
       smem_optin(ctx, (const void*)k_gram_bulk, (int)sm);
       double* part = (double*)ctx->ws.get(WS_GRAM_PARTIAL, (size_t)nb * ka * kb * sizeof(double));
-      k_gram_bulk<<<nb, GB_THREADS, sm, ctx->stream>>>(n, A, lda, ka, B, ldb, kb, R, rpb, part);
+      k_gram_bulk<<<nb, GB_THREADS, sm, ctx->stream>>>(n, A, lda, ka, B, ldb, kb, R, rpb, part, rw);
       check_launch(ctx);
       k_gram_final<<<(ka * kb + 7) / 8, 256, 0, ctx->stream>>>(nb, ka, kb, part, out, sym ? 1 : 0);
       check_launch(ctx);
       return;
     }
   }
+  if (rw) fail(USBS_ERR_SHAPE, "weighted gram: shape outside the TMA path");
   // one block per SM for n >= 148 * 64 rows, else a 64-row chunk per block:
   // the partial pass is latency-bound per tile, so short chunks win
   int nb = (int)std::min<int64_t>(ctx->num_sms, std::max<int64_t>(1, (n + 63) / 64));

@@ -41,8 +41,8 @@ void launch_kron_apply(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t 
                        double beta);
 // out (ka x kb, row-major, dev) = A^T B for row-major n x ka A and n x kb B;
 // sym: out = 0.5 (G + G^T) (requires ka == kb)
-void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B,
-                    int64_t ldb, int kb, double* out, bool sym);
+void launch_gram_tn(usbs_ctx* ctx, int64_t n, const double* A, int64_t lda, int ka, const double* B, int64_t ldb,
+                    int kb, double* out, bool sym, const double* rw = nullptr);
 // deterministic sum-of-squares / dot over n (result in dev scalar)
 void launch_dot(usbs_ctx* ctx, int64_t n, const double* x, const double* y, double* out);
 
