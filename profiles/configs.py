@@ -55,6 +55,9 @@ def run(name, iters, budget, eps):
             "upload_and_cold_start_s": t_up, "iterations": its, "wall_s": wall, "iters_per_s": ips,
             "status": st.status, "rel_subopt": r.rel_subopt, "rel_infeas": r.rel_infeas, "dual_feas": r.dual_feas,
             "matvecs_per_iter": sum(rec["matvecs"]) / max(its, 1),
+            "time_to_eps_s": (wall if st.status == "converged" else None),
+            "f_y": st.f_y, "cost_ip": st.last_primal.cost_ip,
+            "objective_unscaled": float(p.unscale_objective(st.last_primal.cost_ip)),
             "descent_steps": st.descent_steps, "null_steps": st.null_steps}
 
 
