@@ -147,7 +147,7 @@ struct usbs_problem {
   double* aval = nullptr;  // A*(y) on the merged pattern (set by slack assembly)
   // TMA-pipelined grid Lanczos plan (usbs_lanczos_grid.cu), built on first use
   std::vector<int32_t> h_rowptr;  // host copy of rowptr (the plan's input)
-  int lzg_ready = 0, lzg_G = 0, lzg_npieces = 0, lzg_nsplit = 0;
+  int lzg_ready = 0, lzg_G = 0, lzg_npieces = 0, lzg_nsplit = 0, lzg_tail0 = 0, lzg_tail1 = 0;
   int* lzg_blk_row = nullptr;
   int* lzg_blk_item = nullptr;
   int4* lzg_items = nullptr;

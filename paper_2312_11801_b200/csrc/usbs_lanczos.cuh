@@ -55,6 +55,9 @@ struct LzArgs {
   const int* gsplit_first; //   first piece of each split row
   const int* gsplit_cnt;   //   its piece count
   const int* blk_gsplit;   // block b owns split rows [blk_gsplit[b], blk_gsplit[b+1])
+  int tail0, tail1;        // the shared SpMV item pool [tail0, tail1)
+  int* steal;              // its two claim counters (step parity)
+  int lz_opt;              // A/B switches of the TMA variant (bit 0: column sums from shared memory)
 };
 
 // Q element (row i, column t) in the row-blocked layout

@@ -45,6 +45,7 @@
 #include <vector>
 
 #include "usbs_common.cuh"
+#include "usbs_kernels.cuh"
 #include "usbs_lanczos.cuh"
 #include "usbs_tma.cuh"
 #include "usbs_tridiag.cuh"
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
   double* c2s = cs + 32;                     // 32: c'
   double* wacc = c2s + 32;                   // LG_WARPS * 32
   double* misc = wacc + LG_WARPS * 32;       // 8
-  uint64_t* fullb = (uint64_t*)(misc + 8);   // RING
+  double* wsm = misc + 8;                    // LG_WARPS * 32: a warp's row values for its column sums
+  uint64_t* fullb = (uint64_t*)(wsm + LG_WARPS * 32);  // RING
 
   const int m = a.m, M1 = m + 1, n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -260,10 +262,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
         const int* __restrict__ rowptr = a.rowptr;
         const int* __restrict__ colp = a.col;
         const double* __restrict__ valp = a.val;
-        int it = ib + warp;
-        int4 w = it < ie ? a.items[it] : make_int4(0, 0, 0, 0);
-        while (it < ie) {
-          const int4 wn = (it + LG_CONS < ie) ? a.items[it + LG_CONS] : make_int4(0, 0, 0, 0);
+        auto do_item = [&](const int4& w) {
           const int z0 = w.z, z1 = w.w;
           const bool rows = w.x >= 0;
           int rlo[2], rhi[2];
@@ -335,8 +334,28 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
             }
             __syncwarp();
           }
+        };
+        // the block's static items, ib + warp + 15 t, the next descriptor
+        // fetched while the current item is processed ...
+        int it = ib + warp;
+        int4 w = it < ie ? a.items[it] : make_int4(0, 0, 0, 0);
+        while (it < ie) {
+          const int4 wn = (it + LG_CONS < ie) ? a.items[it + LG_CONS] : make_int4(0, 0, 0, 0);
+          do_item(w);
           w = wn;
           it += LG_CONS;
+        }
+        // ... then the shared tail pool (every block's last items), claimed
+        // four at a time; the counter alternates with the step's parity
+        if (a.tail1 > a.tail0) {
+          int* ctr = a.steal + (matvecs & 1);
+          for (;;) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(ctr, 4);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (a.tail0 + base >= a.tail1) break;
+            for (int q = 0; q < 4 && a.tail0 + base + q < a.tail1; ++q) do_item(a.items[a.tail0 + base + q]);
+          }
         }
         if (ALIAS) fence_proxy_smem();  // staging writes before the slots' next copies
       }
@@ -356,6 +375,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
       }
       __syncthreads();
       ++matvecs;
+      if (b == 0 && tid == 0 && a.steal) a.steal[matvecs & 1] = 0;  // the next step's tail counter
       int bad = 0;
       if (cons) {
         double acc0 = 0.0, acc1 = 0.0;
@@ -381,11 +401,23 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
             sl[j * 32 + lane] = qv;
             __syncwarp();
           }
+          if (a.lz_opt & 1) {
+            double* ws = wsm + warp * 32;
+            ws[lane] = wr;
+            __syncwarp();
 #pragma unroll 8
-          for (int rr = 0; rr < 32; rr += 2) {
-            const int ra = (rr + lane) & 31, rb = (rr + 1 + lane) & 31;
-            acc0 = fma(sl[lane * 32 + ra], __shfl_sync(0xffffffffu, wr, ra), acc0);
-            acc1 = fma(sl[lane * 32 + rb], __shfl_sync(0xffffffffu, wr, rb), acc1);
+            for (int rr = 0; rr < 32; rr += 2) {
+              const int ra = (rr + lane) & 31, rb = (rr + 1 + lane) & 31;
+              acc0 = fma(sl[lane * 32 + ra], ws[ra], acc0);
+              acc1 = fma(sl[lane * 32 + rb], ws[rb], acc1);
+            }
+          } else {
+#pragma unroll 8
+            for (int rr = 0; rr < 32; rr += 2) {
+              const int ra = (rr + lane) & 31, rb = (rr + 1 + lane) & 31;
+              acc0 = fma(sl[lane * 32 + ra], __shfl_sync(0xffffffffu, wr, ra), acc0);
+              acc1 = fma(sl[lane * 32 + rb], __shfl_sync(0xffffffffu, wr, rb), acc1);
+            }
           }
           if (fillj) fence_proxy_smem();
           __syncwarp();
@@ -458,11 +490,23 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
           for (; t < jj; ++t) p0 = fma(sl[t * 32 + lane], cs[t], p0);
           const double w1 = w0 - ((p0 + p1) + (p2 + p3));
           if (row < n) Wcur[row] = w1;
+          if (a.lz_opt & 1) {
+            double* ws = wsm + warp * 32;
+            ws[lane] = w1;
+            __syncwarp();
 #pragma unroll 8
-          for (int rr = 0; rr < 32; rr += 2) {
-            const int ra = (rr + lane) & 31, rb = (rr + 1 + lane) & 31;
-            acc0 = fma(sl[lane * 32 + ra], __shfl_sync(0xffffffffu, w1, ra), acc0);
-            acc1 = fma(sl[lane * 32 + rb], __shfl_sync(0xffffffffu, w1, rb), acc1);
+            for (int rr = 0; rr < 32; rr += 2) {
+              const int ra = (rr + lane) & 31, rb = (rr + 1 + lane) & 31;
+              acc0 = fma(sl[lane * 32 + ra], ws[ra], acc0);
+              acc1 = fma(sl[lane * 32 + rb], ws[rb], acc1);
+            }
+          } else {
+#pragma unroll 8
+            for (int rr = 0; rr < 32; rr += 2) {
+              const int ra = (rr + lane) & 31, rb = (rr + 1 + lane) & 31;
+              acc0 = fma(sl[lane * 32 + ra], __shfl_sync(0xffffffffu, w1, ra), acc0);
+              acc1 = fma(sl[lane * 32 + rb], __shfl_sync(0xffffffffu, w1, rb), acc1);
+            }
           }
           __syncwarp();
           issue(P2, &P3, gc + (LG_SPW + 1) * NCW);
@@ -676,7 +720,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1) k_lanczos_tma(LzArgs a) {
 static size_t lz_tma_smem(int ncw, int seg, bool alias, int spw) {
   const int ring = ncw * spw, stg = std::max(LG_CONS * seg, LG_RRS);
   const int scr = alias ? LG_YS : stg + LG_YS;
-  return (size_t)(ring * LG_SLOT + scr + 32 + 32 + LG_WARPS * 32 + 8) * sizeof(double) + ring * sizeof(uint64_t);
+  return (size_t)(ring * LG_SLOT + scr + 32 + 32 + 2 * LG_WARPS * 32 + 8) * sizeof(double) + ring * sizeof(uint64_t);
 }
 
 struct LgVariant {
@@ -759,6 +803,31 @@ void lz_tma_plan(usbs_ctx* ctx, usbs_problem* p) {
     }
     for (int x = bb + 1; x <= G; ++x) blk_item[x] = (int32_t)items.size();
   }
+  // the last `tail` share of every block's items (by cost) goes to a pool the
+  // blocks drain dynamically after their static items (levels the SpMV
+  // phase; the items' results do not depend on who computes them)
+  double tail = 0.0;  // measured: a 12-25% pool levels the SpMV (max 59 -> 56 us) but slows the call (profiles/lz_opts.py)
+  if (const char* e = getenv("USBS_LZG_TAIL")) tail = std::max(0.0, std::min(0.9, atof(e)));
+  {
+    std::vector<int4> stat, pool;
+    std::vector<int32_t> nbi(G + 1, 0);
+    for (int bb = 0; bb < G; ++bb) {
+      double tot = 0.0;
+      for (int t = blk_item[bb]; t < blk_item[bb + 1]; ++t) tot += cost[t];
+      double acc = 0.0;
+      for (int t = blk_item[bb]; t < blk_item[bb + 1]; ++t) {
+        acc += cost[t];
+        if (acc <= (1.0 - tail) * tot || t == blk_item[bb]) stat.push_back(items[t]);
+        else pool.push_back(items[t]);
+      }
+      nbi[bb + 1] = (int32_t)stat.size();
+    }
+    p->lzg_tail0 = (int)stat.size();
+    stat.insert(stat.end(), pool.begin(), pool.end());
+    p->lzg_tail1 = (int)stat.size();
+    items.swap(stat);
+    blk_item.swap(nbi);
+  }
   std::vector<int32_t> blk_split(G + 1, 0);
   for (int bb = 0; bb <= G; ++bb)
     blk_split[bb] = (int32_t)(std::lower_bound(srow.begin(), srow.end(), blk_row[bb]) - srow.begin());
@@ -798,6 +867,12 @@ void lz_tma_launch(usbs_ctx* ctx, usbs_problem* p, LzArgs& a) {
   a.gsplit_first = p->lzg_split_first;
   a.gsplit_cnt = p->lzg_split_cnt;
   a.blk_gsplit = p->lzg_blk_split;
+  a.tail0 = p->lzg_tail0;
+  a.tail1 = p->lzg_tail1;
+  a.steal = (int*)ctx->ws.get(WS_LZ_FLAGS + 100, 2 * sizeof(int));
+  USBS_CUDA(cudaMemsetAsync(a.steal, 0, 2 * sizeof(int), ctx->stream));
+  a.lz_opt = 1;  // column sums from shared memory (1% faster than shuffles at C4)
+  if (const char* e = getenv("USBS_LZG_OPT")) a.lz_opt = atoi(e);
   const LgVariant v = lz_tma_variant();
   if (v.ncw == 8) lz_tma_launch_t<8, 512, true, 2>(ctx, p, a);
   else if (v.ncw == 15) lz_tma_launch_t<15, 512, true, 1>(ctx, p, a);
