@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
                                                         const double* __restrict__ V, int64_t ldv, int k, int d,
                                                         const double* __restrict__ avec,
                                                         const double* __restrict__ wvec, double* __restrict__ gpart,
-                                                        double* __restrict__ apart, double* __restrict__ wpart) {
+                                                        double* __restrict__ apart, double* __restrict__ wpart,
+                                                        int runs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // row stride = 8 (mod 16) doubles: the fragment loads (rows 4ks + q,
   // columns 8X + g) then hit every bank exactly twice
@@ -279,6 +280,19 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
   const int g = lane >> 2, q = lane & 3;
   const int n8 = (d + 7) >> 3, nt8 = n8 * (n8 + 1) / 2;
+  // tile u of this warp (-1: none): strided (t = y 16 + warp + 16 HY u) or a
+  // contiguous run per warp of the CTA's share
+  const int per_cta = (nt8 + (int)gridDim.y - 1) / (int)gridDim.y;
+  const int per_warp = (per_cta + 15) / 16;
+  const int cta_end = min(nt8, ((int)blockIdx.y + 1) * per_cta);
+  auto tile_t = [&](int u) -> int {
+    if (runs) {
+      const int t = (int)blockIdx.y * per_cta + warp * per_warp + u;
+      return (u < per_warp && t < cta_end) ? t : -1;
+    }
+    const int t = (int)blockIdx.y * 16 + warp + 16 * (int)gridDim.y * u;
+    return t < nt8 ? t : -1;
+  };
   if (tid == 0) {
     int p = 0;
     for (int j = 0; j < k; ++j)
@@ -349,18 +363,45 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
       ww[r] = (wvec && r < rows) ? wvec[base + r] : 0.0;
     }
     __syncthreads();
+    if (runs) {
+      // a contiguous run of lower-triangle tiles per warp: tiles of one tile
+      // row share the A fragment, loaded once per k-step and row; k-steps
+      // outer so the warp's tile chains interleave
 #pragma unroll
-    for (int u = 0; u < TPW; ++u) {
-      const int t = blockIdx.y * 16 + warp + 16 * (int)gridDim.y * u;
-      if (t < nt8) {
-        const unsigned e = ttab[t];
-        const int ca = 8 * (int)(e >> 8) + g, cb = 8 * (int)(e & 255u) + g;
-        const bool va = ca < d, vb = cb < d;
+      for (int ks = 0; ks < CTR / 4; ++ks) {
+        const double* row = tile + (4 * ks + q) * dp;
+        int iprev = -1;
+        double av = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < CTR / 4; ++ks) {
-          const double* row = tile + (4 * ks + q) * dp;
-          const double av = va ? row[ca] : 0.0, bv = vb ? row[cb] : 0.0;
-          dmma_m8n8k4(acc0[u], acc1[u], av, bv, acc0[u], acc1[u]);
+        for (int u = 0; u < TPW; ++u) {
+          const int t = tile_t(u);
+          if (t >= 0) {
+            const unsigned e = ttab[t];
+            const int I = (int)(e >> 8);
+            const int ca = 8 * I + g, cb = 8 * (int)(e & 255u) + g;
+            if (I != iprev) {
+              av = ca < d ? row[ca] : 0.0;
+              iprev = I;
+            }
+            const double bv = cb < d ? row[cb] : 0.0;
+            dmma_m8n8k4(acc0[u], acc1[u], av, bv, acc0[u], acc1[u]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int t = tile_t(u);
+        if (t >= 0) {
+          const unsigned e = ttab[t];
+          const int ca = 8 * (int)(e >> 8) + g, cb = 8 * (int)(e & 255u) + g;
+          const bool va = ca < d, vb = cb < d;
+#pragma unroll
+          for (int ks = 0; ks < CTR / 4; ++ks) {
+            const double* row = tile + (4 * ks + q) * dp;
+            const double av = va ? row[ca] : 0.0, bv = vb ? row[cb] : 0.0;
+            dmma_m8n8k4(acc0[u], acc1[u], av, bv, acc0[u], acc1[u]);
+          }
         }
       }
     }
@@ -383,8 +424,8 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
   }
 #pragma unroll
   for (int u = 0; u < TPW; ++u) {
-    const int t = blockIdx.y * 16 + warp + 16 * (int)gridDim.y * u;
-    if (t < nt8) {
+    const int t = tile_t(u);
+    if (t >= 0) {
       const unsigned e = ttab[t];
       const int P = 8 * (int)(e >> 8) + g, Q0 = 8 * (int)(e & 255u) + 2 * q;
       double* out = gpart + (int64_t)blockIdx.x * d * d;
@@ -964,6 +1005,8 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
   }
   const int n8 = (d + 7) / 8, nt8 = n8 * (n8 + 1) / 2;
   const char* emma = getenv("USBS_COMPRESSED_MMA");
+  const char* eruns = getenv("USBS_K4_RUNS");
+  const int runs = (eruns && eruns[0] == '1') ? 1 : 0;  // contiguous runs measured slower (profiles/k4_time.py)
   if (gram_out && nt8 <= 16 * 24 && !(emma && emma[0] == '0')) {
     // tensor-core Gram (d <= 216)
     const size_t smm = (size_t)(CTR * (d + 1 + ((8 - (d + 1)) & 15)) + 2 * CTR) * sizeof(double) + 1200 + 2 * nt8 + 16;
@@ -972,7 +1015,7 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
     smem_optin(ctx, (const void*)k_compressed_mma<T>, 200 * 1024);                                         \
     k_compressed_mma<T><<<dim3(nb, HY), 512, smm, ctx->stream>>>(p->m, p->diag_only ? 1 : 0, p->cptr, p->cent, p->e_row, \
                                                        p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, gpart, \
-                                                       apart, wpart);                                      \
+                                                       apart, wpart, runs);                                \
   }
     if (nt8 <= 16 * 3) USBS_COMP_MMA(3, 1)
     else if (nt8 <= 16 * 8) USBS_COMP_MMA(8, 1)
@@ -1147,6 +1190,8 @@ usbs_status usbs_cons_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const doubl
 
 usbs_status usbs_problem_pattern(usbs_problem* p, int64_t* rowptr, int32_t* col, int32_t* nent) {
   USBS_API_BEGIN
+  ensure_slot_lists(p->ctx, p);
+  USBS_CUDA(cudaStreamSynchronize(p->ctx->stream));
   std::vector<int32_t> rp(p->n + 1), ap(p->nnz + 1);
   USBS_CUDA(cudaMemcpy(rp.data(), p->rowptr, (p->n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
   USBS_CUDA(cudaMemcpy(col, p->col, p->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));

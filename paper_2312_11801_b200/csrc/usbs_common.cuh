@@ -66,6 +66,8 @@ struct usbs_ctx {
   double* pinned = nullptr;  // 4096 doubles of pinned host scratch
   int* pinned_i = nullptr;   // 256 ints
   unsigned char* stage[2] = {nullptr, nullptr};  // pinned upload staging (lazy)
+  void* lzq_ptr = nullptr;  // Lanczos basis / W workspaces last zeroed (usbs_lanczos_top)
+  void* lzw_ptr = nullptr;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 

@@ -33,6 +33,7 @@ void launch_spmm(usbs_ctx* ctx, usbs_problem* p, int which, const double* V, int
 void launch_spmm_vals(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,
                       double* Y, int64_t ldy);
 void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, double* tval);
+void ensure_slot_lists(usbs_ctx* ctx, usbs_problem* p);
 bool kron_enabled(const usbs_problem* p);
 bool spmm_tiles_ok(const usbs_problem* p, int k);
 void launch_spmm_tiles(usbs_ctx* ctx, usbs_problem* p, const double* val, const double* V, int64_t ldv, int k,

@@ -1512,6 +1512,15 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   int* flags = (int*)ctx->ws.get(WS_LZ_FLAGS, 64 * sizeof(int));
   double* out = (double*)ctx->ws.get(WS_LZ_OUT, (size_t)(m + m * m + m + max_restarts + 1 + 8) * sizeof(double));
   double* tmp = (double*)ctx->ws.get(WS_LZ_TMP, (size_t)(ldq + 128) * sizeof(double));
+  // a (re)allocated basis / W workspace may hold the bytes of freed
+  // allocations (NaN patterns): the kernels multiply not-yet-written columns
+  // by zero coefficients, so zero them once per allocation
+  if (ctx->lzq_ptr != (void*)Q || ctx->lzw_ptr != (void*)W) {
+    USBS_CUDA(cudaMemsetAsync(Q, 0, (size_t)ldq * (m + 1) * sizeof(double), st));
+    USBS_CUDA(cudaMemsetAsync(W, 0, (size_t)2 * ldq * sizeof(double), st));
+    ctx->lzq_ptr = Q;
+    ctx->lzw_ptr = W;
+  }
   USBS_CUDA(cudaMemsetAsync(H, 0, (size_t)(m + 1) * (m + 1) * sizeof(double), st));
   USBS_CUDA(cudaMemsetAsync(flags, 0, 64 * sizeof(int), st));
   // padding rows of the last 32-row tile stay zero (the TMA variant streams
@@ -1538,6 +1547,9 @@ extern "C" usbs_status usbs_lanczos_top(usbs_ctx* ctx, usbs_problem* p, int whic
   const LzClusterPlan clp = lz_cached_plan(ctx, p, m);
   const char* ev1 = getenv("USBS_LZ_V1");
   const bool use_tma = clp.cs == 0 && m <= 32 && !(ev1 && ev1[0] == '1');
+  if (getenv("USBS_LZ_DEBUG"))
+    fprintf(stderr, "[lanczos] n=%lld m=%d cluster=%d R=%d hmax=%d smem=%zu tma=%d\n", (long long)n, m, clp.cs, clp.R,
+            clp.hmax, clp.smem, (int)use_tma);
   if (use_tma) lz_tma_plan(ctx, p);
   a.piece_sum = (double*)ctx->ws.get(
       WS_LZ_SPLIT, (size_t)std::max(1, std::max(p->lz_npieces, use_tma ? p->lzg_npieces : 0)) * sizeof(double));

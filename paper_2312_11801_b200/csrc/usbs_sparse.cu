@@ -496,22 +496,74 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
       for (auto& e : errs)
         if (!e.empty()) fail(USBS_ERR_SHAPE, e);
     };
-    run(false);
-    for (int64_t i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
-    col.resize(rowptr[n]);
-    cval.resize(rowptr[n]);
-    run(true);
+    // diagonal constraints (one x-entry per row, column i) with sorted cost
+    // rows without duplicates: the merged row is the cost row with the
+    // diagonal inserted -- no per-row sort
+    bool fast = diag_only && !directed;
+    if (fast) {
+      for (int64_t i = 0; i < n && fast; ++i)
+        for (int64_t z = c_indptr[i] + 1; z < c_indptr[i + 1]; ++z)
+          if (c_indices[z] <= c_indices[z - 1]) { fast = false; break; }
+    }
+    if (fast) {
+      for (int64_t i = 0; i < n; ++i) {
+        bool has = false;
+        for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) has |= (c_indices[z] == i);
+        rowptr[i + 1] = rowptr[i] + (c_indptr[i + 1] - c_indptr[i]) + (has ? 0 : 1);
+      }
+      col.resize(rowptr[n]);
+      cval.resize(rowptr[n]);
+      auto fill = [&](int64_t i0, int64_t i1) {
+        for (int64_t i = i0; i < i1; ++i) {
+          int64_t o = rowptr[i];
+          bool put = false;
+          for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) {
+            const int32_t c = c_indices[z];
+            if (c < 0 || c >= n_cols) continue;  // reported below
+            if (!put && c >= i) {
+              if (c != i) { col[o] = (int32_t)i; cval[o] = 0.0; ++o; }
+              slot_of_x[xcnt[i]] = c == i ? o : o - 1;
+              put = true;
+            }
+            col[o] = c;
+            cval[o] = c_data[z];
+            ++o;
+          }
+          if (!put) {
+            slot_of_x[xcnt[i]] = o;
+            col[o] = (int32_t)i;
+            cval[o] = 0.0;
+          }
+        }
+      };
+      for (int64_t z = 0; z < c_indptr[n]; ++z)
+        if (c_indices[z] < 0 || c_indices[z] >= n_cols) fail(USBS_ERR_SHAPE, "cost column index out of range");
+      std::vector<std::thread> ts;
+      for (int th = 0; th < nthr; ++th) ts.emplace_back(fill, n * th / nthr, n * (th + 1) / nthr);
+      for (auto& t : ts) t.join();
+    } else {
+      run(false);
+      for (int64_t i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
+      col.resize(rowptr[n]);
+      cval.resize(rowptr[n]);
+      run(true);
+    }
   }
   PT("merge C with the entries");
   p->nnz = (int64_t)col.size();
   if (p->nnz >= (1LL << 31) - 1) fail(USBS_ERR_SHAPE, "nnz exceeds int32 indexing");
   // --- slot -> entries (ascending entry id within a slot): counting pass
   // over the entries in order
-  std::vector<int32_t> aptr(p->nnz + 1, 0);
-  for (int64_t t = 0; t < (int64_t)slot_of_x.size(); ++t) aptr[slot_of_x[t] + 1]++;
-  for (int64_t s = 0; s < p->nnz; ++s) aptr[s + 1] += aptr[s];
-  std::vector<int32_t> aent(aptr[p->nnz]);
-  {
+  // (diagonal problems: built lazily on the device, ensure_slot_lists --
+  // only the constraint duck type's adjoint evaluations read them)
+  const bool lazy_slots = diag_only && !directed;
+  std::vector<int32_t> aptr(lazy_slots ? 1 : p->nnz + 1, 0);
+  if (!lazy_slots) {
+    for (int64_t t = 0; t < (int64_t)slot_of_x.size(); ++t) aptr[slot_of_x[t] + 1]++;
+    for (int64_t s = 0; s < p->nnz; ++s) aptr[s + 1] += aptr[s];
+  }
+  std::vector<int32_t> aent(lazy_slots ? 0 : aptr[p->nnz]);
+  if (!lazy_slots) {
     std::vector<int32_t> cur(aptr.begin(), aptr.end() - 1);
     for (int64_t e = 0; e < ne; ++e) {
       aent[cur[slot_of_x[xpos_r[e]]]++] = (int32_t)e;
@@ -660,8 +712,10 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->cval = dev_upload(p, cval.data(), cval.size());
   p->zval = dev_alloc<double>(p, p->nnz);
   USBS_CUDA(cudaMemcpy(p->zval, p->cval, p->nnz * sizeof(double), cudaMemcpyDeviceToDevice));
-  p->aptr = dev_upload(p, aptr.data(), aptr.size());
-  p->aent = dev_upload(p, aent.data(), aent.size());
+  if (!lazy_slots) {
+    p->aptr = dev_upload(p, aptr.data(), aptr.size());
+    p->aent = dev_upload(p, aent.data(), aent.size());
+  }
   {
     std::vector<int32_t> ei(ne), er(ne), ec(ne);
     for (int64_t e = 0; e < ne; ++e) {
@@ -816,7 +870,35 @@ __global__ void k_adjoint_values(int64_t nnz, const int* __restrict__ aptr, cons
   }
 }
 
+// slot -> entries lists of a diagonal problem, built on first use: row i's
+// single entry (id i) sits at diag_slot[i] (increasing in i), so
+// aptr[s] = #{i : diag_slot[i] < s} and aent[i] = i
+__global__ void k_diag_slot_lists(int64_t n, int64_t nnz, const int* __restrict__ dslot, int* __restrict__ aptr,
+                                  int* __restrict__ aent) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= nnz; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (dslot[mid] < s) lo = mid + 1;
+      else hi = mid;
+    }
+    aptr[s] = (int)lo;
+    if (s < n) aent[s] = (int)s;
+  }
+}
+
+void ensure_slot_lists(usbs_ctx* ctx, usbs_problem* p) {
+  if (p->aptr) return;
+  if (!p->diag_only || !p->diag_slot) fail(USBS_ERR_CONFIG, "slot lists missing");
+  p->aptr = dev_alloc<int>(p, p->nnz + 1);
+  p->aent = dev_alloc<int>(p, p->n);
+  const int bl = (int)std::min<int64_t>((p->nnz + 256) / 256, 8 * ctx->num_sms);
+  k_diag_slot_lists<<<std::max(bl, 1), 256, 0, ctx->stream>>>(p->n, p->nnz, p->diag_slot, p->aptr, p->aent);
+  check_launch(ctx);
+}
+
 void launch_adjoint_values(usbs_ctx* ctx, usbs_problem* p, const double* w, double* tval) {
+  ensure_slot_lists(ctx, p);
   int th = 256, bl = (int)std::min<int64_t>((p->nnz + th - 1) / th, 8 * ctx->num_sms);
   k_adjoint_values<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->nnz, p->aptr, p->aent, p->e_idx, p->e_val, w, tval);
   check_launch(ctx);

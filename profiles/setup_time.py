@@ -37,10 +37,8 @@ for rep in range(2):
                          eps=1e-12, max_iters=3, seed=cfg_b.seed)
     ds = S.DeviceSolver(p, cfg, dprob=dp)
     mark("DeviceSolver buffers")
-    psi = np.random.RandomState(123).standard_normal((p.n, cfg_b.sketch_rank))
-    mark("host Psi (legacy MT19937 normals)")
     st = ds.cold_start()
-    mark("cold_start (Lanczos on C + completion + Psi upload)")
+    mark("cold_start (Lanczos on C + completion; Psi on a worker thread)")
     its = []
     ds.solve(init=st, callback=lambda info: its.append(time.perf_counter()))
     mark("3 iterations")

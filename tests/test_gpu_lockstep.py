@@ -13,7 +13,9 @@ is compared with the oracle's iteration t+1:
 
   f_cand, model value, y_cand, nu_cand, a_x (primal image), tr X, <C,X>,
   eta, rel_infeas / rel_subopt / dual_gap   <= 1e-6 relative
-  lambda_max at y_cand                      <= 1e-8 relative
+  lambda_max at y_cand                      <= max(1e-8 relative, the Lanczos
+                                            residual tolerance 1e-9 (1 + |lambda|),
+                                            eigsolve.py:160-163)
   step decision                             exact
   next basis                                projector distance <= max(1e-6,
                                             10 x the oracle's own sensitivity)
@@ -154,6 +156,8 @@ def run_lockstep(name, inject, max_iters, small=False):
             "f_cand": rel(r.f_cand, o.f_cand),
             "model_val": rel(r.model_val, o.model_val),
             "lam_cand": rel(r.lam_cand, o.lam_cand),
+            "lam_cand_abs": abs(r.lam_cand - o.lam_cand),
+            "lam_tol": max(TOL_LAM * abs(o.lam_cand), 1e-9 * (1.0 + abs(o.lam_cand))),
             "y_cand": vrel(r.y_cand, o.y_cand),
             "nu_cand": vrel(r.nu_cand, o.nu_cand),
             "a_x": vrel(r.primal.constr_image, o.primal.constr_image),
@@ -173,7 +177,7 @@ def run_lockstep(name, inject, max_iters, small=False):
     if out_dir:
         os.makedirs(out_dir, exist_ok=True)
         worst = {k: max(float(x[k]) for x in rows) for k in rows[0]
-                 if k not in ("t", "step", "matvecs", "passes", "basis_sens")}
+                 if k not in ("t", "step", "matvecs", "passes", "basis_sens", "lam_tol")}
         with open(os.path.join(out_dir, f"lockstep_{name}.json"), "w") as f:
             json.dump({"config": name, "n": p.n, "m": p.m, "injections": [x["t"] for x in rows],
                        "oracle_seconds": t_oracle, "worst": worst, "rows": rows}, f, indent=1)
@@ -185,7 +189,10 @@ def run_lockstep(name, inject, max_iters, small=False):
             assert e[k] <= TOL, (name, t, k, e[k])
         assert e["matvecs"][0] == e["matvecs"][1] and e["passes"][0] == e["passes"][1], (name, t, e)
         assert e["basis_proj"] <= max(TOL, 10.0 * e["basis_sens"]), (name, t, e["basis_proj"], e["basis_sens"])
-        assert e["lam_cand"] <= TOL_LAM, (name, t, e["lam_cand"])
+        # a Ritz value is determined to its residual: when the Lanczos call ends
+        # unconverged in a cluster (C5), two faithful runs differ by up to the
+        # reference's own acceptance tolerance 1e-9 (1 + |theta_0|)
+        assert e["lam_cand_abs"] <= e["lam_tol"], (name, t, e["lam_cand"], e["lam_cand_abs"], e["lam_tol"])
     return rows
 
 
