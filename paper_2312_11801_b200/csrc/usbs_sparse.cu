@@ -262,6 +262,77 @@ __global__ void __launch_bounds__(256) k_spmm16x2(int n_items, const int* __rest
 }
 
 // combine the partials of split rows in a fixed order (deterministic)
+
+// 2 <= k <= 15: G-lane groups (G = 3, 4, 6, 8 for k <= 5, 7, 11, 15), 32/G
+// items per warp at once (the per-item index, col/val and V round trips of
+// several rows overlap).  A group gathers a row of V with 16-byte loads: the
+// k (+1) doubles from the row start rounded down to 16 bytes, lane c of the
+// group holding window elements 2c, 2c+1 -- columns 2c - s, 2c + 1 - s,
+// where s is the row start's 8-byte parity.  Products accumulate per parity
+// (even: ae0/ae1, odd: ao0/ao1); column 2c = ae0 + ao1 of lane c and column
+// 2c+1 = ae1 of lane c + ao0 of lane c+1, each parity summed in CSR order.
+// Any ldv and base alignment; vend = elements of V that may be read.
+template <int G>
+__global__ void __launch_bounds__(256) k_spmm_g(int n_items, const int* __restrict__ it_row,
+                                                const int* __restrict__ it_beg, const int* __restrict__ it_end,
+                                                const int* __restrict__ it_slot, const int* __restrict__ col,
+                                                const double* __restrict__ val, const double* __restrict__ V,
+                                                int64_t ldv, int64_t vend, int k, double* __restrict__ Y,
+                                                int64_t ldy, double* __restrict__ partial) {
+  constexpr int NG = 32 / G;
+  const int lane = threadIdx.x & 31, g = lane / G, c = lane % G;
+  const bool live = g < NG;
+  const int warps_total = (gridDim.x * blockDim.x) >> 5;
+  const uintptr_t vb = (uintptr_t)V;
+  for (int it0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NG; it0 < n_items; it0 += warps_total * NG) {
+    const int it = it0 + g;
+    const bool on = live && it < n_items;
+    int b = 0, e = 0;
+    if (on) { b = __ldg(it_beg + it); e = __ldg(it_end + it); }
+    double ae0 = 0.0, ae1 = 0.0, ao0 = 0.0, ao1 = 0.0;
+    int len = e - b;
+    // warp-uniform trip count: the longest item of the warp
+    int mx = len;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int u = 0; u < mx; u += 2) {
+      const bool h0 = u < len, h1 = u + 1 < len;
+      const int j0 = h0 ? __ldg(col + b + u) : 0, j1 = h1 ? __ldg(col + b + u + 1) : 0;
+      const double v0 = h0 ? __ldg(val + b + u) : 0.0, v1 = h1 ? __ldg(val + b + u + 1) : 0.0;
+      const int64_t r0 = (int64_t)j0 * ldv, r1 = (int64_t)j1 * ldv;
+      const int s0 = (int)(((vb >> 3) + r0) & 1), s1 = (int)(((vb >> 3) + r1) & 1);
+      const int64_t w0 = r0 - s0 + 2 * c, w1 = r1 - s1 + 2 * c;  // window element of this lane
+      double2 x0 = make_double2(0.0, 0.0), x1 = make_double2(0.0, 0.0);
+      if (h0 && 2 * c - s0 < k) {
+        if (w0 + 1 < vend) x0 = __ldg(reinterpret_cast<const double2*>(V + w0));
+        else if (w0 >= 0 && w0 < vend) x0.x = __ldg(V + w0);
+      }
+      if (h1 && 2 * c - s1 < k) {
+        if (w1 + 1 < vend) x1 = __ldg(reinterpret_cast<const double2*>(V + w1));
+        else if (w1 >= 0 && w1 < vend) x1.x = __ldg(V + w1);
+      }
+      if (h0) {
+        if (s0) { ao0 = fma(v0, x0.x, ao0); ao1 = fma(v0, x0.y, ao1); }
+        else { ae0 = fma(v0, x0.x, ae0); ae1 = fma(v0, x0.y, ae1); }
+      }
+      if (h1) {
+        if (s1) { ao0 = fma(v1, x1.x, ao0); ao1 = fma(v1, x1.y, ao1); }
+        else { ae0 = fma(v1, x1.x, ae0); ae1 = fma(v1, x1.y, ae1); }
+      }
+    }
+    const double nxt = __shfl_down_sync(0xffffffffu, ao0, 1);  // lane c+1's odd-parity column 2c+1
+    if (on) {
+      const int c0 = 2 * c, c1 = 2 * c + 1;
+      const double y0 = ae0 + ao1;
+      const double y1 = ae1 + (c + 1 < G ? nxt : 0.0);
+      const int sl = __ldg(it_slot + it);
+      double* out = sl < 0 ? Y + (int64_t)__ldg(it_row + it) * ldy : partial + (int64_t)sl * k;
+      if (c0 < k) out[c0] = y0;
+      if (c1 < k) out[c1] = y1;
+    }
+  }
+}
+
 __global__ void k_spmm_combine(int n_sr, const int* __restrict__ sr_row, const int* __restrict__ sr_first,
                                const int* __restrict__ sr_count, const double* __restrict__ partial,
                                int k, double* __restrict__ Y, int64_t ldy) {
@@ -922,6 +993,22 @@ k_spmv_fused<1024, 256, 6><<<(unsigned)nb, 256, 0, ctx->stream>>>(
       check_launch(ctx);
     }
     return;
+  } else if (k <= 15 && p->nnz <= 16 * p->n && !getenv("USBS_SPMM_16X2")) {
+    // short rows (C4: 9 per row): grouped 16-byte-gather kernel, several rows
+    // per warp; long rows (C5: 41) keep the half-warp kernel, which is faster
+    // there (profiles/spmm_ab.py; A/B: USBS_SPMM_16X2=1)
+    const int G = k <= 5 ? 3 : k <= 7 ? 4 : k <= 11 ? 6 : 8;
+    const int per = (th / 32) * (32 / G);
+    int bl = (int)std::min<int64_t>((p->n_items + per - 1) / per, 16 * ctx->num_sms);
+    const int64_t vend = (int64_t)(p->n - 1) * ldv + k;
+    auto args = [&](auto kern) {
+      kern<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,
+                                                    p->col, val, V, ldv, vend, k, Y, ldy, partial);
+    };
+    if (G == 3) args(k_spmm_g<3>);
+    else if (G == 4) args(k_spmm_g<4>);
+    else if (G == 6) args(k_spmm_g<6>);
+    else args(k_spmm_g<8>);
   } else if (k <= 16) {
     int bl = (int)std::min<int64_t>((p->n_items + 7) / 8, 16 * ctx->num_sms);
     k_spmm16x2<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,

@@ -1,6 +1,8 @@
-"""K1 at k = 1, 11, 20 on a config: the block-tiled SpMM vs the v1 warp-per-row
-kernel (USBS_SPMM_V1=1); CUDA-event medians with L2 flushed, achieved GB/s of
-B_apply(k) = 12 nnz + 4 (n+1) + 16 n k."""
+"""K1 on a config, CUDA-event medians with L2 flushed, achieved GB/s of
+B_apply(k) = 12 nnz + 4 (n+1) + 16 n k, for each SpMM variant:
+  g      grouped 16-byte-gather kernel (k <= 15, default)
+  16x2   half-warp-per-nonzero kernel (USBS_SPMM_16X2=1)
+  tiles  block CSR-stream kernel (USBS_SPMM_V1=0)"""
 import os
 import sys
 
@@ -20,12 +22,14 @@ nnz = dp.info().nnz_z
 y = np.random.default_rng(1234).standard_normal(p.m) * 1e-3
 dp.assemble(rt.upload(y))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=rt.device)
-for k in (11, 20):
+VARIANTS = {"g": {}, "16x2": {"USBS_SPMM_16X2": "1"}, "tiles": {"USBS_SPMM_V1": "0"}}
+for k in (2, 5, 11, 15, 20):
     V = rt.upload(np.linalg.qr(np.random.default_rng(k).standard_normal((p.n, k)))[0])
     out = {}
-    for tag, env in (("v1", "1"), ("tiles", "0")):
-        os.environ["USBS_SPMM_L2"] = os.environ.get("L2", "1")
-        os.environ["USBS_SPMM_V1"] = env
+    for tag, env in VARIANTS.items():
+        for key in ("USBS_SPMM_16X2", "USBS_SPMM_V1"):
+            os.environ.pop(key, None)
+        os.environ.update(env)
         Y = dp.apply(1, V)
         ts = []
         for _ in range(7):
@@ -38,6 +42,7 @@ for k in (11, 20):
             ts.append(e0.elapsed_time(e1))
         out[tag] = (float(np.median(ts)), Y.cpu().numpy())
     b = 12 * nnz + 4 * (p.n + 1) + 16 * p.n * k
-    d = np.abs(out["v1"][1] - out["tiles"][1]).max() / np.abs(out["v1"][1]).max()
-    print(f"{name} k={k}: v1 {out['v1'][0]*1e3:.1f} us ({b/out['v1'][0]/1e6:.0f} GB/s)  tiles "
-          f"{out['tiles'][0]*1e3:.1f} us ({b/out['tiles'][0]/1e6:.0f} GB/s)  max rel diff {d:.1e}", flush=True)
+    ref = out["16x2"][1]
+    line = "  ".join(f"{t} {ms*1e3:.1f} us ({b/ms/1e6:.0f} GB/s, diff {np.abs(y_ - ref).max() / np.abs(ref).max():.0e})"
+                     for t, (ms, y_) in out.items())
+    print(f"{name} k={k}: {line}", flush=True)

@@ -81,6 +81,37 @@ def test_op_apply_matches_oracle(name, k):
     np.testing.assert_allclose(rt.download(g), cq, rtol=1e-12, atol=1e-14 * max(1e-300, np.abs(cq).max()))
 
 
+@pytest.mark.parametrize("name", ["C4s", "C5s", "mixed40"])
+def test_spmm_grouped_gather_any_k_and_view(name, monkeypatch):
+    """K1 for 2 <= k <= 15 (grouped 16-byte gathers, usbs_sparse.cu k_spmm_g):
+    every group width (k = 2 .. 15), V a contiguous tensor and an offset,
+    strided column view (row starts alternate 8-byte parity, ld = k + 3),
+    within the dot-product bound and equal to the half-warp kernel up to
+    summation order."""
+    eigen, runtime = dev()
+    p = case_problem(name)
+    rng = np.random.default_rng(77)
+    dp = runtime.DeviceProblem(p)
+    rt = dp.rt
+    c_abs = abs(p.cost)
+    rownnz = np.diff(p.cost.indptr)
+    for k in (2, 3, 5, 6, 7, 9, 11, 12, 15):
+        v = rng.standard_normal((p.n, k))
+        want = p.cost @ v
+        big = rt.upload(np.zeros((p.n, k + 3)))
+        view = big[:, 1:k + 1]
+        view.copy_(rt.upload(v))
+        for V in (rt.upload(v), view):
+            monkeypatch.delenv("USBS_SPMM_16X2", raising=False)
+            got = rt.download(dp.apply(0, V))
+            bound_check(got, want, c_abs, np.abs(v), rownnz)
+            monkeypatch.setenv("USBS_SPMM_16X2", "1")
+            ref = rt.download(dp.apply(0, V))
+            bound_check(ref, want, c_abs, np.abs(v), rownnz)
+            np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-13 * np.abs(want).max())
+        monkeypatch.delenv("USBS_SPMM_16X2", raising=False)
+
+
 def test_slack_pattern_holds_cost_bit_exact():
     """The uploaded cost values/columns equal prob.cost (bit-exact), checked
     through C e_j products on a few columns."""
