@@ -443,6 +443,217 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
   }
 }
 
+// Single-entry flattening for the pipelined K4: per constraint row the
+// (row, col, value) of its entry when it has exactly one (C3: 99%, C5: all),
+// else (-1, -1) and the row is generated from the entry list.
+__global__ void k_c1_flatten(int64_t m, const int* __restrict__ cptr, const int* __restrict__ cent,
+                             const int* __restrict__ erow, const int* __restrict__ ecol,
+                             const double* __restrict__ eval, int2* __restrict__ rc, double* __restrict__ cv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int t0 = cptr[i], t1 = cptr[i + 1];
+    if (t1 - t0 == 1) {
+      const int e = cent[t0];
+      rc[i] = make_int2(erow[e], ecol[e]);
+      cv[i] = eval[e];
+    } else {
+      rc[i] = make_int2(-1, -1);
+      cv[i] = 0.0;
+    }
+  }
+}
+
+// K4 with the row generation pipelined behind the tensor-core Gram.  The
+// 32-row tiles of generated rows are double buffered in smem and the
+// generation of tile i+1 runs in the same barrier interval as the MMAs of
+// tile i; its global loads are issued ahead: the constraints' single entries
+// (row, col, value) three tiles ahead and their two V rows two tiles ahead,
+// in flight while the warp runs its MMAs.  Warp w owns rows w and w + 16 of
+// every tile.  Rows with several entries are generated from the entry list
+// (synchronously).  The Gram is computed in 16 x 16 blocks of the lower
+// triangle (2 x 2 tiles of 8, three on the diagonal), BPW blocks per warp
+// strided over the warps of gridDim.y CTAs per row range: per k-step the
+// warp loads two A and two B fragments for four m8n8k4 MMAs.
+template <int BPW>
+__global__ void __launch_bounds__(512, 1) k_compressed_mma_pipe(int64_t m, int diag_only,
+    const int2* __restrict__ c1rc, const double* __restrict__ c1v, const int* __restrict__ cptr,
+    const int* __restrict__ cent, const int* __restrict__ erow, const int* __restrict__ ecol,
+    const double* __restrict__ eval, const double* __restrict__ V, int64_t ldv, int k, int d,
+    double* __restrict__ gpart) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int dp = d + 1 + ((8 - (d + 1)) & 15);
+  double* tbuf = (double*)smem_raw;  // 2 x CTR * dp
+  unsigned char* pi = (unsigned char*)(tbuf + 2 * CTR * dp);
+  unsigned char* pj = pi + 600;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int n16 = (d + 15) >> 4, nb16 = n16 * (n16 + 1) / 2;
+  // block u of this warp: (BI, BK), BK <= BI, or BI = -1
+  int bI[BPW], bK[BPW];
+#pragma unroll
+  for (int u = 0; u < BPW; ++u) {
+    const int t = (int)blockIdx.y * 16 + warp + 16 * (int)gridDim.y * u;
+    if (t < nb16) {
+      int I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+      while (I * (I + 1) / 2 > t) --I;
+      while ((I + 1) * (I + 2) / 2 <= t) ++I;
+      bI[u] = I;
+      bK[u] = t - I * (I + 1) / 2;
+    } else {
+      bI[u] = -1;
+      bK[u] = 0;
+    }
+  }
+  if (tid == 0) {
+    int p = 0;
+    for (int j = 0; j < k; ++j)
+      for (int i = j; i < k; ++i) { pi[p] = (unsigned char)i; pj[p] = (unsigned char)j; ++p; }
+  }
+  const int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = blockIdx.x * chunk, c1 = min(m, c0 + chunk);
+  const int ntile = (int)((max((int64_t)0, c1 - c0) + CTR - 1) / CTR);
+  double acc[BPW][4][2];
+#pragma unroll
+  for (int u = 0; u < BPW; ++u)
+#pragma unroll
+    for (int x = 0; x < 4; ++x) acc[u][x][0] = acc[u][x][1] = 0.0;
+
+  // prefetch state per owned row slot s (rows warp, warp + 16 of a tile):
+  // A = entries of tile i+3, B = V rows of tile i+2, C = V rows of tile i+1
+  int2 rcA[2], rcB[2], rcC[2];
+  double vA[2], vB[2], vC[2], vrB[2], vcB[2], vrC[2], vcC[2];
+  auto row_of = [&](int tl, int s) -> int64_t { return c0 + (int64_t)tl * CTR + warp + 16 * s; };
+  auto load_info = [&](int tl) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int64_t i = row_of(tl, s);
+      if (tl < ntile && i < c1) {
+        if (diag_only) { rcA[s] = make_int2((int)i, (int)i); vA[s] = 1.0; }
+        else { rcA[s] = __ldg(c1rc + i); vA[s] = __ldg(c1v + i); }
+      } else {
+        rcA[s] = make_int2(-2, -2);  // no row
+        vA[s] = 0.0;
+      }
+    }
+  };
+  // B -> C, then A -> B with B's V rows issued
+  auto advance = [&]() {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      rcC[s] = rcB[s]; vC[s] = vB[s]; vrC[s] = vrB[s]; vcC[s] = vcB[s];
+      rcB[s] = rcA[s]; vB[s] = vA[s];
+      const bool ok = rcA[s].x >= 0 && lane < k;
+      vrB[s] = ok ? __ldg(V + (int64_t)rcA[s].x * ldv + lane) : 0.0;
+      vcB[s] = ok ? __ldg(V + (int64_t)rcA[s].y * ldv + lane) : 0.0;
+    }
+  };
+  // the lane's 7 svec slots (a, b) and weights, fixed for the kernel
+  int pab[7];
+#pragma unroll
+  for (int jj = 0; jj < 7; ++jj) pab[jj] = 0;
+  // products of one entry into the lane's 7 svec slots; a diagonal entry
+  // (row == col) needs two shuffles per slot: (ra cb + ca rb) / 2 = ra rb
+  // exactly when a_r == a_c
+  auto entry = [&](double a_r, double a_c, bool same, double val, double (&accp)[7]) {
+#pragma unroll
+    for (int jj = 0; jj < 7; ++jj) {
+      const int aa = pab[jj] & 255, bb = pab[jj] >> 8;
+      const double wpp = aa == bb ? 1.0 : 1.4142135623730951;
+      const double ra = __shfl_sync(0xffffffffu, a_r, aa), rb = __shfl_sync(0xffffffffu, a_r, bb);
+      double gg;
+      if (same) {
+        gg = ra * rb;
+      } else {
+        const double cb = __shfl_sync(0xffffffffu, a_c, bb), ca = __shfl_sync(0xffffffffu, a_c, aa);
+        gg = ra * cb + ca * rb;
+      }
+      accp[jj] += gg * val * wpp;
+    }
+  };
+  // generate tile tl (stage C) into buf
+  auto build = [&](int tl, double* buf) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int r = warp + 16 * s;
+      double accp[7];
+#pragma unroll
+      for (int jj = 0; jj < 7; ++jj) accp[jj] = 0.0;
+      if (rcC[s].x >= 0) {
+        entry(vrC[s], vcC[s], rcC[s].x == rcC[s].y, vC[s], accp);
+      } else if (rcC[s].x == -1) {  // several entries: from the list
+        const int64_t i = row_of(tl, s);
+        for (int t = cptr[i]; t < cptr[i + 1]; ++t) {
+          const int e = cent[t];
+          const int rr = erow[e], cc2 = ecol[e];
+          const double a_r = lane < k ? V[(int64_t)rr * ldv + lane] : 0.0;
+          const double a_c = lane < k ? V[(int64_t)cc2 * ldv + lane] : 0.0;
+          entry(a_r, a_c, rr == cc2, eval[e], accp);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 7; ++jj) {
+        const int pp = lane + 32 * jj;
+        if (pp < d) buf[r * dp + pp] = accp[jj];
+      }
+    }
+  };
+
+  __syncthreads();  // tables
+#pragma unroll
+  for (int jj = 0; jj < 7; ++jj) {
+    const int pp = lane + 32 * jj;
+    pab[jj] = pp < d ? (pi[pp] | (pj[pp] << 8)) : 0;
+  }
+  load_info(0);
+  advance();          // B = tile 0
+  load_info(1);
+  advance();          // C = tile 0, B = tile 1
+  load_info(2);
+  if (ntile > 0) build(0, tbuf);
+  advance();          // C = tile 1, B = tile 2
+  load_info(3);
+  __syncthreads();
+  for (int tl = 0; tl < ntile; ++tl) {
+    const double* cur = tbuf + (tl & 1) * CTR * dp;
+    double* nxt = tbuf + ((tl + 1) & 1) * CTR * dp;
+    // G += T^T T on the current tile (rows beyond the range are zero)
+#pragma unroll
+    for (int u = 0; u < BPW; ++u) {
+      if (bI[u] >= 0) {
+        const int ra0 = 16 * bI[u] + g, ra1 = ra0 + 8, rb0 = 16 * bK[u] + g, rb1 = rb0 + 8;
+        const bool diagb = bI[u] == bK[u];
+#pragma unroll
+        for (int ks = 0; ks < CTR / 4; ++ks) {
+          const double* row = cur + (4 * ks + q) * dp;
+          const double a0 = ra0 < d ? row[ra0] : 0.0, a1 = ra1 < d ? row[ra1] : 0.0;
+          const double b0 = rb0 < d ? row[rb0] : 0.0, b1 = rb1 < d ? row[rb1] : 0.0;
+          dmma_m8n8k4(acc[u][0][0], acc[u][0][1], a0, b0, acc[u][0][0], acc[u][0][1]);
+          dmma_m8n8k4(acc[u][2][0], acc[u][2][1], a1, b0, acc[u][2][0], acc[u][2][1]);
+          dmma_m8n8k4(acc[u][3][0], acc[u][3][1], a1, b1, acc[u][3][0], acc[u][3][1]);
+          if (!diagb) dmma_m8n8k4(acc[u][1][0], acc[u][1][1], a0, b1, acc[u][1][0], acc[u][1][1]);
+        }
+      }
+    }
+    if (tl + 1 < ntile) {
+      build(tl + 1, nxt);  // stage C: V rows loaded two intervals ago
+      advance();
+      load_info(tl + 4);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < BPW; ++u) {
+    if (bI[u] < 0) continue;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int P = 16 * bI[u] + 8 * (x >> 1) + g, Q0 = 16 * bK[u] + 8 * (x & 1) + 2 * q;
+      double* out = gpart + (int64_t)blockIdx.x * d * d;
+      if (P < d && Q0 < d && Q0 <= P) out[(int64_t)P * d + Q0] = acc[u][x][0];
+      if (P < d && Q0 + 1 < d && Q0 + 1 <= P) out[(int64_t)P * d + Q0 + 1] = acc[u][x][1];
+    }
+  }
+}
+
+
 // sum block partials in fixed order; gram output mirrored to full symmetric
 __global__ void k_compressed_final(int nb, int d, const double* __restrict__ gpart, const double* __restrict__ apart,
                                    const double* __restrict__ wpart, double sg, double sa, double sw,
@@ -943,6 +1154,7 @@ usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* V, int
   USBS_API_END
 }
 
+
 __global__ void k_svec(int k, const double* __restrict__ A, double scale, double* __restrict__ out);
 
 usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k,
@@ -1017,9 +1229,35 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
                                                        p->e_col, p->e_val, V, ldv, k, d, a_vec, w_vec, gpart, \
                                                        apart, wpart, runs);                                \
   }
+    const char* ev1 = getenv("USBS_K4_V1");
+    if (!a_vec && !w_vec && !(ev1 && ev1[0] == '1')) {
+      // pipelined row generation (A/B: USBS_K4_V1=1)
+      if (!p->diag_only && !p->c1_rc) {
+        p->c1_rc = dev_alloc<int2>(p, (size_t)p->m);
+        p->c1_val = dev_alloc<double>(p, (size_t)p->m);
+        k_c1_flatten<<<nblocks(ctx, p->m), 256, 0, ctx->stream>>>(p->m, p->cptr, p->cent, p->e_row, p->e_col,
+                                                                  p->e_val, p->c1_rc, p->c1_val);
+        check_launch(ctx);
+      }
+      const size_t smp = (size_t)(2 * CTR * (d + 1 + ((8 - (d + 1)) & 15))) * sizeof(double) + 1200 + 16;
+      const int n16 = (d + 15) / 16, nb16 = n16 * (n16 + 1) / 2;
+#define USBS_COMP_PIPE(T, HY)                                                                              \
+  {                                                                                                        \
+    smem_optin(ctx, (const void*)k_compressed_mma_pipe<T>, 200 * 1024);                                    \
+    k_compressed_mma_pipe<T><<<dim3(nb, HY), 512, smp, ctx->stream>>>(                                     \
+        p->m, p->diag_only ? 1 : 0, p->c1_rc, p->c1_val, p->cptr, p->cent, p->e_row, p->e_col, p->e_val, V, \
+        ldv, k, d, gpart);                                                                                 \
+  }
+      if (nb16 <= 16) USBS_COMP_PIPE(1, 1)
+      else if (nb16 <= 32) USBS_COMP_PIPE(2, 1)
+      else if (nb16 <= 64) USBS_COMP_PIPE(2, 2)
+      else USBS_COMP_PIPE(4, 2)  // d = 210: 105 blocks over two CTAs per row range (four: 7% slower)
+#undef USBS_COMP_PIPE
+    } else {
     if (nt8 <= 16 * 3) USBS_COMP_MMA(3, 1)
     else if (nt8 <= 16 * 8) USBS_COMP_MMA(8, 1)
     else USBS_COMP_MMA(12, 2)  // the tiles split over two CTAs per row range: 24 accumulators a lane, no spill
+    }
 #undef USBS_COMP_MMA
   } else if (tpt <= 1) USBS_COMP(1)
   else if (tpt <= 2) USBS_COMP(2)

@@ -86,6 +86,8 @@ struct usbs_problem {
   int* aent = nullptr;   // entry ids
   // constraint -> entries (ascending entry id), for row-wise constraint kernels
   int* cptr = nullptr;  // m + 1
+  int2* c1_rc = nullptr;      // per constraint: (row, col) of its single entry, (-1, -1) if it has several
+  double* c1_val = nullptr;   // that entry's value (lazy, first compressed-Gram call)
   int* cent = nullptr;  // ne
   int max_entries_per_cons = 0;
   // flat constraint entries (device copies)

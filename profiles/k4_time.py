@@ -1,5 +1,5 @@
-"""K4 compressed Gram (d x d, DMMA) timing on C4 / C5 / C3: strided tile
-assignment (USBS_K4_RUNS=0) vs contiguous tile runs with A-fragment reuse."""
+"""K4 compressed Gram (d x d, DMMA) timing on C4 / C5 / C3: the pipelined
+kernel (default) vs the round-1 kernel (USBS_K4_V1=1, strided tiles)."""
 import json
 import os
 import sys
@@ -27,7 +27,7 @@ for name in sys.argv[1:] or ["C4", "C5", "C3"]:
     G = rt.empty(d, d)
     res = {}
     for runs in ("0", "1"):
-        os.environ["USBS_K4_RUNS"] = runs
+        os.environ["USBS_K4_V1"] = "1" if runs == "0" else "0"
         for _ in range(2):
             eng.compressed(V, scale_gram=1.0, gram_out=G)
         ts = []
@@ -42,6 +42,6 @@ for name in sys.argv[1:] or ["C4", "C5", "C3"]:
         res[runs] = (float(np.median(ts)), G.cpu().numpy().copy())
     flop = p.m * d * (d + 1)
     diff = np.abs(res["0"][1] - res["1"][1]).max() / np.abs(res["0"][1]).max()
-    print(f"{name} d={d}: strided {res['0'][0]:.3f} ms ({flop / res['0'][0] / 1e9:.1f} TF/s)  runs "
+    print(f"{name} d={d}: v1 {res['0'][0]:.3f} ms ({flop / res['0'][0] / 1e9:.1f} TF/s)  pipelined "
           f"{res['1'][0]:.3f} ms ({flop / res['1'][0] / 1e9:.1f} TF/s, {flop / res['1'][0] / 1e9 / peak:.0%} of "
           f"{peak} DMMA peak)  max rel diff {diff:.1e}", flush=True)
