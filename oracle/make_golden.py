@@ -24,6 +24,8 @@ Fixtures:
   rounding.npz       maxcut_round / qap_round (rounding.py) on seeded factors
   state.npz          USBS v1 state-file bytes (save_state) of solved states,
                      warm_start_pad outputs and the warm-started trajectory
+  cli.json           front end: instance readers on valid/malformed files,
+                     writers, perturb outputs, solve CSV rows and round output
 """
 from __future__ import annotations
 
@@ -417,12 +419,118 @@ def state_cases():
     np.savez_compressed(OUT / "state.npz", **data)
 
 
+# instance files for the front-end fixtures: (name, text); valid and malformed
+MM_FILES = [
+    ("k3_pattern", "%%MatrixMarket matrix coordinate pattern symmetric\n3 3 3\n2 1\n3 1\n3 2\n"),
+    ("general_mirrored", "%%MatrixMarket matrix coordinate real general\n% a comment\n\n4 4 6\n1 2 0.5\n2 1 0.5\n"
+     "3 4 -2.25\n4 3 -2.25\n2 2 7\n1 1 3\n"),
+    ("integer_dups_diag", "%%MatrixMarket matrix coordinate integer symmetric\n5 5 6\n2 1 3\n1 2 4\n5 5 9\n"
+     "4 3 -1\n5 1 2\n3 4 1\n"),
+    ("empty", ""),
+    ("no_header", "3 3 1\n2 1\n"),
+    ("array", "%%MatrixMarket matrix array real general\n2 2\n1\n2\n3\n4\n"),
+    ("complex", "%%MatrixMarket matrix coordinate complex symmetric\n2 2 1\n2 1 1 0\n"),
+    ("hermitian", "%%MatrixMarket matrix coordinate real hermitian\n2 2 1\n2 1 1\n"),
+    ("no_size", "%%MatrixMarket matrix coordinate real symmetric\n% only comments\n"),
+    ("size_fields", "%%MatrixMarket matrix coordinate real symmetric\n3 3\n"),
+    ("size_bad", "%%MatrixMarket matrix coordinate real symmetric\n3 x 1\n2 1 1\n"),
+    ("not_square", "%%MatrixMarket matrix coordinate real symmetric\n3 4 1\n2 1 1\n"),
+    ("few_fields", "%%MatrixMarket matrix coordinate real symmetric\n3 3 1\n2 1\n"),
+    ("bad_value", "%%MatrixMarket matrix coordinate real symmetric\n3 3 1\n2 1 abc\n"),
+    ("out_of_range", "%%MatrixMarket matrix coordinate real symmetric\n3 3 1\n4 1 1\n"),
+    ("count", "%%MatrixMarket matrix coordinate real symmetric\n3 3 2\n2 1 1\n"),
+    ("no_mirror", "%%MatrixMarket matrix coordinate real general\n3 3 2\n2 1 1\n3 1 1\n"),
+    ("mirror_mismatch", "%%MatrixMarket matrix coordinate real general\n3 3 2\n2 1 1\n1 2 2\n"),
+]
+QAP_FILES = [
+    ("qap3", "3\n\n0 1 2\n1 0\n3\n2 3 0\n\n0 5 6 5 0 7\n6 7 0\n"),
+    ("empty", ""),
+    ("bad_size", "x\n0 1\n1 0\n"),
+    ("nonpositive", "0\n"),
+    ("short", "2\n0 1 1 0\n0 2\n"),
+    ("trailing", "1\n0\n0\n5\n"),
+    ("bad_entry", "2\n0 1 1 0\n0 2 q 0\n"),
+    ("asymmetric", "2\n0 1 2 0\n0 2 2 0\n"),
+]
+
+
+def cli_cases():
+    """Front end (cli.py, problem.py:546-681) of the unmodified reference:
+    the readers on valid and malformed files (edges or the error text and
+    line), the writers' bytes, perturb outputs, and solve/round runs (CSV
+    rows without the time column, stdout)."""
+    import contextlib
+    import io
+    import tempfile
+    from conftest import random_graph, random_qap
+    from specbundle import cli as sbc
+    out = {"mm": {}, "qap": {}, "files": {"mm": MM_FILES, "qap": QAP_FILES}}
+    with tempfile.TemporaryDirectory() as d:
+        def put(name, text):
+            path = os.path.join(d, name)
+            with open(path, "w") as fh:
+                fh.write(text)
+            return path
+
+        for name, text in MM_FILES:
+            try:
+                g = sbp.parse_graph_mm(put(name + ".mtx", text))
+                out["mm"][name] = {"n": g.n, "u": g.edges_u.tolist(), "v": g.edges_v.tolist(), "w": g.edges_w.tolist()}
+            except sbp.ParseError as exc:
+                out["mm"][name] = {"error": str(exc), "line": exc.line}
+        for name, text in QAP_FILES:
+            try:
+                q = sbp.parse_qaplib(put(name + ".dat", text))
+                out["qap"][name] = {"W": q.weights.tolist(), "D": q.distances.tolist()}
+            except sbp.ParseError as exc:
+                out["qap"][name] = {"error": str(exc), "line": exc.line}
+        g = random_graph(50, 0.2, 2)
+        gp = os.path.join(d, "g.mtx")
+        sbp.write_graph_mm(g, gp)
+        out["write_graph"] = open(gp).read()
+        q = random_qap(4, 1)
+        qp = os.path.join(d, "q.dat")
+        sbp.write_qaplib(q, qp)
+        out["write_qap"] = open(qp).read()
+        out["perturb"] = {}
+        for kind, src, frac in (("maxcut", gp, "0.1"), ("qap", qp, "0.5")):
+            si, sm = os.path.join(d, f"sub_{kind}"), os.path.join(d, f"map_{kind}.json")
+            with contextlib.redirect_stdout(io.StringIO()) as so:
+                rc = sbc.main(["perturb", "--problem", kind, "--input", src, "--fraction", frac,
+                               "--out-instance", si, "--out-mapping", sm])
+            out["perturb"][kind] = {"rc": rc, "instance": open(si).read(), "mapping": json.load(open(sm)),
+                                    "stdout": so.getvalue().splitlines()[0]}
+        k3 = put("k3.mtx", MM_FILES[0][1])
+        q3 = put("q3.dat", QAP_FILES[0][1])
+        out["solve"] = {}
+        for tag, argv in (
+                ("k3_round", ["solve", "--problem", "maxcut", "--input", k3, "--eps", "1e-3", "--round", "--seed", "5"]),
+                ("k3_budget", ["solve", "--problem", "maxcut", "--input", k3, "--max-iters", "0"]),
+                ("g50", ["solve", "--problem", "maxcut", "--input", gp, "--max-iters", "25", "--round"]),
+                ("qap3", ["solve", "--problem", "qap", "--input", q3, "--max-iters", "20", "--round",
+                          "--optimum", "40"])):
+            csvp = os.path.join(d, tag + ".csv")
+            st = os.path.join(d, tag + ".bin")
+            with contextlib.redirect_stdout(io.StringIO()) as so:
+                rc = sbc.main(argv + ["--out", csvp, "--save-state", st])
+            rows = [r.split(",") for r in open(csvp).read().splitlines()]
+            rows = [[c for i, c in enumerate(r) if i != 1] for r in rows]
+            res = {"rc": rc, "rows": rows, "stdout": so.getvalue().splitlines()}
+            kind = argv[2]
+            with contextlib.redirect_stdout(io.StringIO()) as so2:
+                res["round_rc"] = sbc.main(["round", "--problem", kind, "--input", argv[4], "--state", st])
+            res["round_stdout"] = so2.getvalue().splitlines()
+            out["solve"][tag] = res
+    with open(OUT / "cli.json", "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
     which = sys.argv[1:] or ["builders", "quad", "lanczos", "ipm", "cons", "sketch", "traj", "lockstep", "rounding", "state"]
     fn = {"builders": builders, "builders_full": builders_full, "quad": quad_oracle, "lanczos": lanczos_cases, "ipm": ipm_cases,
           "cons": cons_cases, "sketch": sketch_cases, "traj": trajectories, "lockstep": lockstep,
-          "rounding": rounding_cases, "state": state_cases}
+          "rounding": rounding_cases, "state": state_cases, "cli": cli_cases}
     for w in which:
         fn[w]()
         print("wrote", w)

@@ -1000,7 +1000,7 @@ k_spmv_fused<1024, 256, 6><<<(unsigned)nb, 256, 0, ctx->stream>>>(
     const int G = k <= 5 ? 3 : k <= 7 ? 4 : k <= 11 ? 6 : 8;
     const int per = (th / 32) * (32 / G);
     int bl = (int)std::min<int64_t>((p->n_items + per - 1) / per, 16 * ctx->num_sms);
-    const int64_t vend = (int64_t)(p->n - 1) * ldv + k;
+    const int64_t vend = (int64_t)(p->n_cols - 1) * ldv + k;  // V has n_cols rows (local + ghost for shards)
     auto args = [&](auto kern) {
       kern<<<std::max(bl, 1), th, 0, ctx->stream>>>(p->n_items, p->it_row, p->it_beg, p->it_end, p->it_slot,
                                                     p->col, val, V, ldv, vend, k, Y, ldy, partial);

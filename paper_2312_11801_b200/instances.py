@@ -95,6 +95,11 @@ class Graph:
     def num_edges(self) -> int:
         return int(self.ew.size)
 
+    def subgraph(self, keep: int) -> "Graph":
+        """Induced subgraph on vertices 0 .. keep-1 (problem.py:104-108)."""
+        sel = (self.eu < keep) & (self.ev < keep)
+        return Graph.from_arrays(keep, self.eu[sel], self.ev[sel], self.ew[sel])
+
     def laplacian(self) -> sp.csr_matrix:
         # COO assembly order matches problem.py:93-102 so duplicate summation
         # inside tocsr() rounds identically
@@ -127,6 +132,26 @@ class Qap:
     @property
     def size(self) -> int:
         return self.weights.shape[0]
+
+    def shrink(self) -> "Qap":
+        """The instance without its last facility/location (problem.py:131-133)."""
+        return Qap(self.weights[:-1, :-1].copy(), self.distances[:-1, :-1].copy())
+
+
+def qap_labels(q: Qap) -> list:
+    """Labels of the lifted assignment constraints in builder order
+    (problem.py:392-426): ("tr1", k, l), ("tr2", i, j), ("G", a, b),
+    ("diagY", a), ("rowsum", k), ("colsum", i), ("B", a), ("corner",),
+    ("trY",); used to map constraints between instance sizes."""
+    l = q.size
+    out = [("tr1", k, kk) for k in range(l) for kk in range(k, l)]
+    out += [("tr2", i, j) for i in range(l) for j in range(i, l)]
+    ka, kb = np.nonzero(np.kron(q.distances, q.weights))
+    out += [("G", int(a), int(b)) for a, b in zip(ka, kb)]
+    out += [("diagY", a) for a in range(l * l)]
+    out += [("rowsum", k) for k in range(l)] + [("colsum", i) for i in range(l)]
+    out += [("B", a) for a in range(l * l)] + [("corner",), ("trY",)]
+    return out
 
 
 # ---------------------------------------------------------------------------

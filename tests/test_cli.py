@@ -1,0 +1,220 @@
+"""Front end (paper_2312_11801_b200.cli / formats) against the reference's
+own front end (cli.py, problem.py:546-681), pinned by tests/golden/cli.json
+(oracle/make_golden.py cli): instance readers on valid and malformed files,
+writers, perturb outputs, exit codes; on the GPU the solve CSV and the
+round output (the reference test_cli.py cases plus fixture comparisons)."""
+from __future__ import annotations
+
+import csv
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, cuda_ok
+from helpers import random_graph, random_qap
+from paper_2312_11801_b200 import cli, formats
+
+FIX = json.loads((GOLDEN / "cli.json").read_text())
+K3_MTX = "%%MatrixMarket matrix coordinate pattern symmetric\n3 3 3\n2 1\n3 1\n3 2\n"
+
+
+def _mm_files():
+    """The instance files the fixture was recorded on (name, text)."""
+    return FIX["files"]["mm"], FIX["files"]["qap"]
+
+
+def test_readers_match_reference(tmp_path):
+    mm, qap = _mm_files()
+    for name, text in mm:
+        p = tmp_path / f"{name}.mtx"
+        p.write_text(text)
+        want = FIX["mm"][name]
+        if "error" in want:
+            with pytest.raises(formats.ParseError) as ei:
+                formats.parse_graph_mm(p)
+            assert (str(ei.value), ei.value.line) == (want["error"], want["line"]), name
+        else:
+            g = formats.parse_graph_mm(p)
+            assert g.n == want["n"], name
+            assert g.eu.tolist() == want["u"] and g.ev.tolist() == want["v"] and g.ew.tolist() == want["w"], name
+    for name, text in qap:
+        p = tmp_path / f"{name}.dat"
+        p.write_text(text)
+        want = FIX["qap"][name]
+        if "error" in want:
+            with pytest.raises(formats.ParseError) as ei:
+                formats.parse_qaplib(p)
+            assert (str(ei.value), ei.value.line) == (want["error"], want["line"]), name
+        else:
+            q = formats.parse_qaplib(p)
+            assert q.weights.tolist() == want["W"] and q.distances.tolist() == want["D"]
+
+
+def test_writers_match_reference_and_round_trip(tmp_path):
+    g = random_graph(50, 0.2, 2)
+    formats.write_graph_mm(g, tmp_path / "g.mtx")
+    assert (tmp_path / "g.mtx").read_text() == FIX["write_graph"]
+    g2 = formats.parse_graph_mm(tmp_path / "g.mtx")
+    assert np.array_equal(g2.eu, g.eu) and np.array_equal(g2.ev, g.ev) and np.array_equal(g2.ew, g.ew)
+    q = random_qap(4, 1)
+    formats.write_qaplib(q, tmp_path / "q.dat")
+    assert (tmp_path / "q.dat").read_text() == FIX["write_qap"]
+    q2 = formats.parse_qaplib(tmp_path / "q.dat")
+    assert np.array_equal(q2.weights, q.weights) and np.array_equal(q2.distances, q.distances)
+
+
+@pytest.mark.parametrize("kind,frac", [("maxcut", "0.1"), ("qap", "0.5")])
+def test_perturb_matches_reference(tmp_path, capsys, kind, frac):
+    src = tmp_path / "src"
+    src.write_text(FIX["write_graph"] if kind == "maxcut" else FIX["write_qap"])
+    si, sm = tmp_path / "sub", tmp_path / "map.json"
+    rc = cli.main(["perturb", "--problem", kind, "--input", str(src), "--fraction", frac,
+                   "--out-instance", str(si), "--out-mapping", str(sm)])
+    want = FIX["perturb"][kind]
+    assert rc == want["rc"] == 0
+    assert si.read_text() == want["instance"]
+    assert json.loads(sm.read_text()) == want["mapping"]
+    assert capsys.readouterr().out.splitlines()[0] == want["stdout"]
+
+
+def test_perturb_thousand_vertices(tmp_path):
+    """test_cli.py: 1% of 1000 vertices dropped, identity vertex map."""
+    formats.write_graph_mm(random_graph(1000, 0.004, 3), tmp_path / "big.mtx")
+    assert cli.main(["perturb", "--problem", "maxcut", "--input", str(tmp_path / "big.mtx"), "--fraction", "0.01",
+                     "--out-instance", str(tmp_path / "s.mtx"), "--out-mapping", str(tmp_path / "m.json")]) == 0
+    assert formats.parse_graph_mm(tmp_path / "s.mtx").n == 990
+    assert json.loads((tmp_path / "m.json").read_text())["vertex_map"] == list(range(990))
+
+
+def test_usage_and_parse_error_codes(tmp_path):
+    k3 = tmp_path / "k3.mtx"
+    k3.write_text(K3_MTX)
+    assert cli.main([]) == 64
+    assert cli.main(["solve", "--problem", "maxcut"]) == 64
+    assert cli.main(["solve", "--problem", "nosuch", "--input", str(k3)]) == 64
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(tmp_path / "missing.mtx")]) == 64
+    bad = tmp_path / "bad.mtx"
+    bad.write_text("junk\n")
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(bad)]) == 1
+    cfg = tmp_path / "cfg"
+    cfg.write_text("nonsense = 1\n")
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3), "--config", str(cfg)]) == 64
+    cfg.write_text("no equals sign\n")
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3), "--config", str(cfg)]) == 64
+    for frac in ("0", "1", "-0.5"):
+        assert cli.main(["perturb", "--problem", "maxcut", "--input", str(k3), "--fraction", frac,
+                         "--out-instance", str(tmp_path / "o"), "--out-mapping", str(tmp_path / "m")]) == 64
+
+
+def test_config_precedence_and_defaults(tmp_path):
+    """Flags > config file > per-problem defaults (cli.py:151-182)."""
+    cfgf = tmp_path / "cfg"
+    cfgf.write_text("eps = 0.5\nseed = 3\nkc = 4\nlinf_check = yes\n# comment\n")
+    ap = cli.build_parser()
+    g = random_graph(20, 0.3, 1)
+    args = ap.parse_args(["solve", "--problem", "maxcut", "--input", "x", "--config", str(cfgf), "--eps", "1e-3"])
+    c = cli.resolve_config(args, "maxcut", g)
+    assert (c.eps, c.seed, c.k_c, c.k_p, c.rho, c.sketch_rank, c.linf_check) == (1e-3, 3, 4, 1, 0.01, 10, True)
+    q = random_qap(3, 1)
+    args = ap.parse_args(["solve", "--problem", "qap", "--input", "x"])
+    c = cli.resolve_config(args, "qap", q)
+    assert (c.k_c, c.k_p, c.rho, c.sketch_rank, c.max_iters) == (2, 0, 0.005, 3, 1000)
+
+
+# ----------------------------------------------------------------- GPU
+
+def rows_of(path):
+    with open(path) as fh:
+        return list(csv.reader(fh))
+
+
+@pytest.fixture
+def k3_file(tmp_path):
+    p = tmp_path / "k3.mtx"
+    p.write_text(K3_MTX)
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")
+def test_solve_k3_end_to_end_and_codes(tmp_path, k3_file, capsys):
+    out = tmp_path / "m.csv"
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3_file), "--eps", "1e-3", "--out", str(out),
+                     "--round"]) == 0
+    rows = rows_of(out)
+    assert rows[0] == cli.CSV_HEADER
+    assert float(rows[-1][4]) <= 1e-3 and rows[-1][7] in ("descent", "null") and float(rows[-1][8]) == 2.0
+    z = tmp_path / "z.csv"
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3_file), "--max-iters", "0",
+                     "--out", str(z)]) == 2
+    assert len(rows_of(z)) == 1
+    # CSV deterministic modulo time
+    runs = []
+    for name in ("r1.csv", "r2.csv"):
+        assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3_file), "--seed", "5",
+                         "--out", str(tmp_path / name)]) == 0
+        runs.append([[c for i, c in enumerate(r) if i != 1] for r in rows_of(tmp_path / name)])
+    assert runs[0] == runs[1]
+    # config file loose, flag tight
+    cfgf = tmp_path / "cfg"
+    cfgf.write_text("eps = 0.5\nseed = 3\n")
+    c = tmp_path / "c.csv"
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3_file), "--config", str(cfgf), "--eps", "1e-3",
+                     "--out", str(c)]) == 0
+    assert float(rows_of(c)[-1][4]) <= 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")
+def test_state_warm_start_round_and_fingerprint(tmp_path, k3_file, capsys):
+    st = tmp_path / "s.bin"
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3_file), "--save-state", str(st),
+                     "--out", str(tmp_path / "a.csv")]) == 0
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(k3_file), "--warm-start", str(st),
+                     "--out", str(tmp_path / "b.csv")]) == 0
+    assert len(rows_of(tmp_path / "b.csv")) - 1 <= 2
+    capsys.readouterr()
+    assert cli.main(["round", "--problem", "maxcut", "--input", str(k3_file), "--state", str(st)]) == 0
+    assert "cut value: 2" in capsys.readouterr().out
+    other = tmp_path / "other.mtx"
+    formats.write_graph_mm(random_graph(5, 0.8, 1), other)
+    assert cli.main(["round", "--problem", "maxcut", "--input", str(other), "--state", str(st)]) == 65
+    assert cli.main(["solve", "--problem", "maxcut", "--input", str(other), "--warm-start", str(st),
+                     "--out", str(tmp_path / "y.csv")]) == 65
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")
+@pytest.mark.parametrize("tag", ["k3_round", "k3_budget", "g50", "qap3"])
+def test_solve_and_round_match_reference(tmp_path, capsys, tag):
+    """The reference CLI's runs (cli.json): same exit codes, iteration and
+    step columns, rounded values and round output; f_y to 1e-6 relative and
+    the residual columns to 1e-4 (free-running trajectories)."""
+    want = FIX["solve"][tag]
+    files = {"k3": ("maxcut", K3_MTX), "g50": ("maxcut", FIX["write_graph"]), "qap3": ("qap", None)}
+    key = tag.split("_")[0]
+    kind, text = files[key]
+    src = tmp_path / "inst"
+    if text is None:
+        _, qap = _mm_files()
+        text = dict(qap)["qap3"]
+    src.write_text(text)
+    argv = {"k3_round": ["--eps", "1e-3", "--round", "--seed", "5"], "k3_budget": ["--max-iters", "0"],
+            "g50": ["--max-iters", "25", "--round"], "qap3": ["--max-iters", "20", "--round", "--optimum", "40"]}[tag]
+    out, st = tmp_path / "m.csv", tmp_path / "s.bin"
+    rc = cli.main(["solve", "--problem", kind, "--input", str(src)] + argv + ["--out", str(out), "--save-state", str(st)])
+    assert rc == want["rc"]
+    rows = [[c for i, c in enumerate(r) if i != 1] for r in rows_of(out)]
+    assert len(rows) == len(want["rows"]) and rows[0] == want["rows"][0]
+    for a, b in zip(rows[1:], want["rows"][1:]):
+        assert a[0] == b[0] and a[6] == b[6], (a, b)
+        assert a[7] == b[7], (a, b)
+        # free-running trajectories (no state injection): f_y to 1e-6, the
+        # printed residuals (7 digits) to 1e-4 relative
+        assert abs(float(a[1]) - float(b[1])) <= 1e-6 * abs(float(b[1])) + 1e-12, (a, b)
+        for x, y in zip(a[2:6], b[2:6]):
+            assert abs(float(x) - float(y)) <= 1e-4 * abs(float(y)) + 1e-9, (a, b)
+    capsys.readouterr()
+    assert cli.main(["round", "--problem", kind, "--input", str(src), "--state", str(st)]) == want["round_rc"]
+    assert capsys.readouterr().out.splitlines()[:1] == want["round_stdout"][:1]
