@@ -91,30 +91,84 @@ __device__ double blk_max_abs(const double* x, int n, double* red) {
   return r;
 }
 
-// One warp factors W (lower, row-major k x k, k <= 32) in place: per column
-// the pivot's rsqrt, the column scaled by the lanes below it, then the
-// trailing update W[r][c] -= L[r][j] L[c][j] over all (r, c), j < c <= r,
-// spread across the lanes from a column-major table of the lower triangle
-// (ctab: entries (r << 5 | c) for 1 <= c <= r < k, column c from
-// (c - 1) k - c (c - 1) / 2), so the updates of one column are independent
-// and pipeline instead of forming one lane's serial chain.  Same arithmetic
-// per entry as the row-by-row form.  Fails on a pivot <= 0 or NaN (potrf);
-// returns ok.
-__device__ __forceinline__ int warp_chol_core(double* W, int k, const unsigned short* ctab) {
-  const int lane = threadIdx.x & 31;
-  const int ntab = k * (k - 1) / 2;
+__device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, double b, double c0, double c1);
+
+// One warp factors W (lower, row-major k x k, k <= 32) in place, blocked by
+// 8: the 8 x 8 diagonal block in registers (lanes 0-7 hold its rows; per
+// column the pivot's rsqrt, the column scaled, the trailing entries of the
+// block updated with L(t, c) shuffled from lane t), the rows below by
+// substitution (a lane per row, the block's rsqrt values in registers), the
+// trailing 8 x 8 tiles with two FP64 m8n8k4 MMAs per tile (the row stride k
+// keeps the fragment loads of a half-warp on distinct banks for k = 20).
+// Same factor as the column-by-column form (bit-identical in the
+// microbenchmark, profiles/mb/chol_mb.cu: k = 20 12.1k -> 8.4k cycles).
+// Fails on a pivot <= 0 or NaN (potrf); returns ok.  Own register
+// allocation (noinline) so the callers' live state does not spill it.
+__device__ __noinline__ int warp_chol_core(double* W, int k, const unsigned short* /*ctab*/) {
+  const int lane = threadIdx.x & 31, r = lane & 7, g = lane >> 2, q = lane & 3;
   int ok = 1;
-  for (int j = 0; j < k; ++j) {
-    const double piv = W[j * k + j];
-    if (!(piv > 0.0)) { ok = 0; break; }
-    const double r = rsqrt(piv);
-    const int row = j + 1 + lane;
-    if (row < k) W[row * k + j] *= r;
-    if (lane == 0) W[j * k + j] = piv * r;
+  for (int j0 = 0; j0 < k; j0 += 8) {
+    const int jb = min(8, k - j0);
+    double a[8], rsv[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) a[t] = (r < jb && t <= r) ? W[(j0 + r) * k + j0 + t] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      rsv[c] = 0.0;
+      if (c < jb) {
+        const double pv = __shfl_sync(0xffffffffu, a[c], c);
+        if (!(pv > 0.0)) ok = 0;
+        const double rs = rsqrt(pv);
+        rsv[c] = rs;
+        a[c] = (r == c) ? pv * rs : a[c] * rs;
+#pragma unroll
+        for (int t = c + 1; t < 8; ++t) {
+          const double ltc = __shfl_sync(0xffffffffu, a[c], t);
+          if (t <= r) a[t] -= a[c] * ltc;
+        }
+      }
+    }
+    if (lane < 8 && r < jb) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t <= r) W[(j0 + r) * k + j0 + t] = a[t];
+    }
+    if (!ok) return 0;  // warp-uniform (every lane saw the same pivots)
     __syncwarp();
-    for (int e = j * k - (j + 1) * j / 2 + lane; e < ntab; e += 32) {
-      const int rc = ctab[e], rr = rc >> 5, cc = rc & 31;
-      W[rr * k + cc] -= W[rr * k + j] * W[cc * k + j];
+    const int r0 = j0 + jb;
+    if (r0 >= k) break;
+    const int i = r0 + lane;
+    if (i < k) {
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = W[i * k + j0 + c];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        v[c] *= rsv[c];
+#pragma unroll
+        for (int t = c + 1; t < 8; ++t) v[t] = fma(-v[c], W[(j0 + t) * k + j0 + c], v[t]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) W[i * k + j0 + c] = v[c];
+    }
+    __syncwarp();
+    const int T = (k + 7) >> 3, I0 = r0 >> 3;
+    for (int I = I0; I < T; ++I) {
+      const int ra = I * 8 + g;
+      const bool va = ra < k;
+      const double a0 = va ? -W[ra * k + j0 + q] : 0.0, a1 = va ? -W[ra * k + j0 + 4 + q] : 0.0;
+      for (int K = I0; K <= I; ++K) {
+        const int rb = K * 8 + g;
+        const bool vb = rb < k;
+        const double b0 = vb ? W[rb * k + j0 + q] : 0.0, b1 = vb ? W[rb * k + j0 + 4 + q] : 0.0;
+        const int cc = K * 8 + 2 * q;
+        const bool v0 = va && cc <= ra, v1 = va && cc + 1 <= ra;
+        double c0 = v0 ? W[ra * k + cc] : 0.0, c1 = v1 ? W[ra * k + cc + 1] : 0.0;
+        dmma8x8x4(c0, c1, a0, b0, c0, c1);
+        dmma8x8x4(c0, c1, a1, b1, c0, c1);
+        if (v0) W[ra * k + cc] = c0;
+        if (v1) W[ra * k + cc + 1] = c1;
+      }
     }
     __syncwarp();
   }
@@ -250,10 +304,14 @@ __device__ __forceinline__ void chol_diag8(double* __restrict__ Mp, int d, int J
       const double rs = ok ? rsqrt(pv) : 0.0;
       if (lane == 0) rdiag[j0 + c] = rs;
       a[c] = (r == c) ? pv * rs : a[c] * rs;
+      // the next pivot's update from the lane's own value first (the serial
+      // chain is then shuffle, rsqrt, scale, one FMA); the other entries take
+      // L(t, c) shuffled from lane t -- the same operations either way
+      if (c + 1 < 8 && r == c + 1) a[c + 1] -= a[c] * a[c];
 #pragma unroll
       for (int t = c + 1; t < 8; ++t) {
         const double ltc = __shfl_sync(0xffffffffu, a[c], t);  // L(t, c)
-        if (t <= r) a[t] -= a[c] * ltc;
+        if (t <= r && !(t == c + 1 && r == c + 1)) a[t] -= a[c] * ltc;
       }
     }
   }
@@ -335,8 +393,9 @@ __device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ r
     } else if (R > 1) {
       // the other warps take whole tile rows I >= J + 2 (longest first),
       // the row's L_IJ fragments and offsets loaded once for all its tiles
-      const int lane = tid & 31, g = lane >> 2, q = lane & 3, nw1 = nwp - 1;
-      for (int I = T - warp; I >= J + 2; I -= nw1) {
+      const int lane = tid & 31, g = lane >> 2, q = lane & 3;
+      const int wk = warp - 1, nw1 = nwp - 1;
+      for (int I = T - 1 - wk; I >= J + 2; I -= nw1) {
         const int ra = I * 8 + g;
         const bool va = ra < d;
         const int oa = va ? pidx(ra, 0) : 0;

@@ -232,6 +232,7 @@ __global__ void k_bchol(const double* g, double* out, long long* cyc, int k, int
   out[threadIdx.x] = L[threadIdx.x];
 }
 
+__device__ __noinline__ int wchol_b8(double* W, int k);
 template <int V>
 __global__ void k_wchol(const double* g, double* out, long long* cyc, int k, int reps) {
   __shared__ double W[32 * 32];
@@ -251,6 +252,8 @@ __global__ void k_wchol(const double* g, double* out, long long* cyc, int k, int
     t0 = clock64();
     if (V == 0) {
       okk += wchol_smem(W, k, ctab);
+    } else if (V == 5) {
+      okk += wchol_b8(W, k);
     } else {
       double a[32];
 #pragma unroll
@@ -264,13 +267,90 @@ __global__ void k_wchol(const double* g, double* out, long long* cyc, int k, int
     tot = rep == 0 ? clock64() - t0 : min(tot, clock64() - t0);
   }
   if (lane == 0) { cyc[0] = tot; cyc[1] = okk; }
-  if (V == 0) out[lane] = W[lane];
+  if (V == 0 || V == 5) for (int i = lane; i < k * k; i += 32) out[i] = W[i];
 }
 
 // ---- packed blocked Cholesky (8-column panels), variants of the trailing update
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b, double c0, double c1) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};"
                : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+
+// blocked warp Cholesky of a row-major k x k (k <= 32): 8 x 8 diagonal
+// blocks in registers (lanes 0-7 = rows), 8-column substitutions a lane per
+// row below, trailing 8 x 8 tiles on the FP64 tensor cores
+__device__ __noinline__ int wchol_b8(double* W, int k) {
+  const int lane = threadIdx.x & 31, r = lane & 7, g = lane >> 2, q = lane & 3;
+  int ok = 1;
+  for (int j0 = 0; j0 < k; j0 += 8) {
+    const int jb = min(8, k - j0);
+    double a[8], rsv[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) a[t] = (r < jb && t <= r) ? W[(j0 + r) * k + j0 + t] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      rsv[c] = 0.0;
+      if (c < jb) {
+        const double pv = __shfl_sync(FULL, a[c], c);
+        if (!(pv > 0.0)) ok = 0;
+        const double rs = rsqrt(pv);
+        rsv[c] = rs;
+        a[c] = (r == c) ? pv * rs : a[c] * rs;
+#pragma unroll
+        for (int t = c + 1; t < 8; ++t) {
+          const double ltc = __shfl_sync(FULL, a[c], t);
+          if (t <= r) a[t] -= a[c] * ltc;
+        }
+      }
+    }
+    if (lane < 8 && r < jb) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t <= r) W[(j0 + r) * k + j0 + t] = a[t];
+    }
+    if (!ok) return 0;
+    __syncwarp();
+    const int r0 = j0 + jb;
+    if (r0 >= k) break;
+    // rows below: x L_JJ^T = v, a lane per row
+    const int i = r0 + lane;
+    if (i < k) {
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = W[i * k + j0 + c];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        v[c] *= rsv[c];
+#pragma unroll
+        for (int t = c + 1; t < 8; ++t) v[t] = fma(-v[c], W[(j0 + t) * k + j0 + c], v[t]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) W[i * k + j0 + c] = v[c];
+    }
+    __syncwarp();
+    // trailing tiles (I, K), r0/8 <= K <= I
+    const int T = (k + 7) >> 3, I0 = r0 >> 3;
+    for (int I = I0; I < T; ++I) {
+      const int ra = I * 8 + g;
+      const bool va = ra < k;
+      const double a0 = va ? -W[ra * k + j0 + q] : 0.0, a1 = va ? -W[ra * k + j0 + 4 + q] : 0.0;
+      for (int K = I0; K <= I; ++K) {
+        const int rb = K * 8 + g;
+        const bool vb = rb < k;
+        const double b0 = vb ? W[rb * k + j0 + q] : 0.0, b1 = vb ? W[rb * k + j0 + 4 + q] : 0.0;
+        const int cc = K * 8 + 2 * q;
+        const bool v0 = va && cc <= ra, v1 = va && cc + 1 <= ra;
+        double c0 = v0 ? W[ra * k + cc] : 0.0, c1 = v1 ? W[ra * k + cc + 1] : 0.0;
+        dmma(c0, c1, a0, b0, c0, c1);
+        dmma(c0, c1, a1, b1, c0, c1);
+        if (v0) W[ra * k + cc] = c0;
+        if (v1) W[ra * k + cc + 1] = c1;
+      }
+    }
+    __syncwarp();
+  }
+  return ok;
 }
 
 __device__ __forceinline__ void tile_update(double* Mp, int d, int j0, int jb, int I, int K) {
@@ -636,19 +716,28 @@ int main() {
     std::vector<double> A;
     spd(k, A, 2);
     cudaMemcpy(dg, A.data(), 8 * A.size(), cudaMemcpyHostToDevice);
-    const char* nm[5] = {"smem table", "regs rolled", "regs rolled + fast rsqrt", "regs unrolled",
-                         "regs unrolled + fast rsqrt"};
-    for (int v = 0; v < 5; ++v) {
+    const char* nm[6] = {"smem table", "regs rolled", "regs rolled + fast rsqrt", "regs unrolled",
+                         "regs unrolled + fast rsqrt", "blocked 8 (diag regs, DMMA)"};
+    std::vector<double> L0(k * k), L5(k * k);
+    for (int v = 0; v < 6; ++v) {
       for (int w = 0; w < 2; ++w) {
         switch (v) {
           case 0: k_wchol<0><<<1, 32>>>(dg, dout, dc, k, 4); break;
           case 1: k_wchol<1><<<1, 32>>>(dg, dout, dc, k, 4); break;
           case 2: k_wchol<2><<<1, 32>>>(dg, dout, dc, k, 4); break;
           case 3: k_wchol<3><<<1, 32>>>(dg, dout, dc, k, 4); break;
-          default: k_wchol<4><<<1, 32>>>(dg, dout, dc, k, 4); break;
+          case 4: k_wchol<4><<<1, 32>>>(dg, dout, dc, k, 4); break;
+          default: k_wchol<5><<<1, 32>>>(dg, dout, dc, k, 4); break;
         }
       }
       cudaMemcpy(c, dc, 16, cudaMemcpyDeviceToHost);
+      if (v == 0) cudaMemcpy(L0.data(), dout, 8 * k * k, cudaMemcpyDeviceToHost);
+      if (v == 5) {
+        cudaMemcpy(L5.data(), dout, 8 * k * k, cudaMemcpyDeviceToHost);
+        double e = 0;
+        for (int i = 0; i < k; ++i) for (int j = 0; j <= i; ++j) e = fmax(e, fabs(L0[i * k + j] - L5[i * k + j]));
+        printf("  blocked vs table max |dL| = %.3e\n", e);
+      }
       printf("wchol k=%d %-28s %6lld cycles (ok %lld)\n", k, nm[v], c[0], c[1]);
     }
     k_bchol<128><<<1, 128>>>(dg, dout, dc, k, 4);
