@@ -314,7 +314,7 @@ def run_device(args):
     cs, rows = dp.lanczos_plan(max(32, k_c + 1))
     lz_kernel = (f"k_lanczos_cl (one {cs}-CTA thread-block cluster, Q resident in shared memory, "
                  f"{rows} rows per CTA; 1 launch per lanczos_top)" if cs else
-                 "k_lanczos (persistent cooperative grid, Q streamed from HBM; 1 launch per lanczos_top)")
+                 "k_lanczos_tma (persistent cooperative grid, Q tiles streamed by cp.async.bulk; 1 launch per lanczos_top)")
     traffic = None
     if tr is not None and tr_alg:
         traffic = tr * (avg_bytes / tr_alg)  # captured DRAM/algorithmic ratio applied to the average launch
