@@ -11,8 +11,13 @@ then K timed iterations, each timed with CUDA events on the launching
 stream; the C4 working set (Z 108 MB, Lanczos basis 264 MB, V/P/Psi 88/80/80
 MB) exceeds L2 and L2 is also flushed (256 MiB write) between timed
 iterations.  For N > 1 (torchrun) each rank runs an independent replica
-(value = all ranks' iterations / max-over-ranks time); the row-sharded C4
-path is dist.py.
+(scaling "weak", value = all ranks' iterations / max-over-ranks time): at
+C4's size one GPU holds the whole problem and the single-GPU persistent
+Lanczos beats the row-sharded path.  --mode sharded
+runs ONE row-sharded solve over the N GPUs instead (dist.py: row blocks of
+Z, V, Q, the sketch and the m-vectors per rank; NCCL allgather before each
+SpMV, allreduces of the k x k / d x d Grams and norms; scaling "strong",
+value = outer iterations of the whole problem per second).
 
 --impl reference times the reference algorithm on the host cores (the CPU
 oracle port of the pure-Python reference; the reference itself cannot travel
@@ -224,14 +229,14 @@ def _solver_cfg(S, cfg_b, **kw):
     return S.SolverConfig(**base)
 
 
-def timed_solve(S, rt, cfg_b, warmup, steps, flush, dp=None, world=1, clocks=None):
+def timed_solve(S, rt, cfg_b, warmup, steps, flush, dp=None, world=1, clocks=None, comm=None):
     """W untimed then K timed outer iterations of a device-resident solve
     (problem uploaded and cold start done before timing); per-iteration CUDA
     events on the launching stream, L2 flushed before each timed iteration."""
     import torch
     p = cfg_b.problem
     cfg = _solver_cfg(S, cfg_b, eps=1e-12, max_iters=warmup + steps)
-    ds = S.DeviceSolver(p, cfg, dprob=dp)
+    ds = S.DeviceSolver(p, cfg, dprob=dp, comm=comm)
     ds.lz_probe = []
     evs = []
     launches0 = [None]
@@ -408,6 +413,92 @@ def run_device(args):
         torch.distributed.destroy_process_group()
 
 
+def run_sharded(args):
+    """N > 1 on a sharded config: one row-sharded solve over all ranks."""
+    import datetime
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    # test hook: USBS_BENCH_GLOO=1 puts every rank on cuda:0 with a gloo group
+    # (a real exchange through host memory; NCCL needs distinct devices)
+    gloo = os.environ.get("USBS_BENCH_GLOO") == "1"
+    if gloo:
+        local = 0
+    torch.cuda.set_device(local)
+    # a stuck collective raises after 10 minutes instead of hanging the job
+    tmo = datetime.timedelta(minutes=10)
+    if gloo:
+        dist.init_process_group("gloo", timeout=tmo)
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=tmo)
+    from paper_2312_11801_b200 import solver as S
+    from paper_2312_11801_b200.dist import Comm, Shard, ShardedDeviceProblem
+    from paper_2312_11801_b200.runtime import runtime
+
+    rt = runtime()
+    cfg_b = baseline(args.config)
+    p = cfg_b.problem
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=rt.device)
+    shard = Shard.balanced(p.cost.indptr, world, rank)
+    comm = Comm(world)
+    sdp = ShardedDeviceProblem(p, shard, comm)
+    clocks = ClockSampler(local)
+    _, it_ms, launches, clk = timed_solve(S, rt, cfg_b, max(1, args.warmup), args.steps, flush, dp=sdp, world=world,
+                                          clocks=clocks, comm=comm)
+    t = torch.tensor([float(np.sum(it_ms))], device=rt.device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    steps = len(it_ms)
+    value = steps / (total_ms / 1e3)
+
+    # e2e: shard upload + planning from the host problem, cold start and
+    # the iterations with a D2H of the rank's dual block every iteration
+    d2h = {"bytes": 0}
+
+    def cb_e2e(info):
+        d2h["bytes"] += info.y.nbytes + 8 * 16
+
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    sdp_e = ShardedDeviceProblem(p, shard, comm)
+    st_e, _ = S.DeviceSolver(p, _solver_cfg(S, cfg_b, eps=1e-12, max_iters=args.steps), dprob=sdp_e,
+                             comm=comm).solve(callback=cb_e2e)
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], device=rt.device, dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = st_e.iterations / float(te.item())
+    rows = shard.rows
+    nnz_local = int(p.cost.indptr[shard.r1] - p.cost.indptr[shard.r0])
+    h2d = nnz_local * 12 + 8 * (rows + 1) + 4 * 8 * rows
+    if rank == 0:
+        line = {
+            "metric": metric_name(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / max(steps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config],
+                       "parallelism": f"row-sharded x{world} ({'gloo test group' if gloo else 'NCCL'} allgather per "
+                                      f"SpMV, allreduce of Grams/norms)",
+                       "l2": "inputs larger than L2; also flushed (256 MiB write) between timed iterations",
+                       "step": "one USBS outer iteration of the whole problem",
+                       "rows_per_rank": [int(x) for x in np.diff(shard.bounds)]},
+            "roofline": None,
+            "cpu_baseline": None,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / max(st_e.iterations, 1),
+                    "d2h_bytes_per_step": d2h["bytes"] / max(st_e.iterations, 1),
+                    "note": "rank 0's shard upload + planning from the host problem, cold start and a D2H of its "
+                            "dual block every iteration; wall clock, max over ranks"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "iter_ms": {"min": float(np.min(it_ms)), "median": float(np.median(it_ms)), "max": float(np.max(it_ms))},
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def _event_time(rt, fn, flush, reps=5, warm=2):
     import torch
     for _ in range(warm):
@@ -485,9 +576,14 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="timed CPU work of the cpu_baseline leg (s)")
     ap.add_argument("--ref-budget", type=float, default=120.0, help="timed CPU work of the reference arm (s)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["sharded", "replicas"],
+                    help="N > 1: independent replicas (default) or one row-sharded solve")
     args = ap.parse_args()
+    _, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "sharded":
+        run_sharded(args)
     else:
         run_device(args)
 
