@@ -731,6 +731,47 @@ __global__ void k_rowgemm(int64_t n, const double* __restrict__ X, int64_t ldx, 
   }
 }
 
+// Row-per-thread form of k_rowgemm for kb <= KBM: a thread keeps its output
+// row in registers (every column of X read once per row instead of once per
+// output entry); B (ka x kb, scaled by xs) in shared memory, read as
+// broadcasts.  Same sums in the same order as k_rowgemm.
+template <int KBM>
+__global__ void __launch_bounds__(256) k_rowgemm_rt(int64_t n, const double* __restrict__ X, int64_t ldx, int ka,
+                                                    const double* __restrict__ B, int64_t ldb, int kb,
+                                                    const double* __restrict__ xs, double alpha, double beta,
+                                                    const double* Y0, int64_t ldy0, double* Y, int64_t ldy) {
+  __shared__ double Bs[64 * KBM];
+  __shared__ double xsv[64];
+  for (int x = threadIdx.x; x < ka * KBM; x += blockDim.x) {
+    const int u = x / KBM, c = x % KBM;
+    Bs[x] = c < kb ? B[(int64_t)u * ldb + c] : 0.0;
+  }
+  for (int u = threadIdx.x; u < ka; u += blockDim.x) xsv[u] = xs ? xs[u] : 1.0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* xr = X + i * ldx;
+    double o[KBM];
+#pragma unroll
+    for (int c = 0; c < KBM; ++c) o[c] = 0.0;
+    for (int u = 0; u < ka; ++u) {
+      const double xv = xs ? xr[u] * xsv[u] : xr[u];
+      const double* br = Bs + u * KBM;
+#pragma unroll
+      for (int c = 0; c < KBM; ++c) o[c] = fma(xv, br[c], o[c]);
+    }
+    double* yr = Y + i * ldy;
+    const double* y0r = Y0 ? Y0 + i * ldy0 : nullptr;
+#pragma unroll
+    for (int c = 0; c < KBM; ++c) {
+      if (c < kb) {
+        double v = alpha * o[c];
+        if (y0r) v += beta * y0r[c];
+        yr[c] = v;
+      }
+    }
+  }
+}
+
 // sum_i sum_j F[i,j] G[i,j] w[j]  (deterministic two-pass)
 __global__ void k_wcoldot_partial(int64_t n, const double* __restrict__ F, int64_t ldf,
                                   const double* __restrict__ G, int64_t ldg, int k,
@@ -1279,8 +1320,20 @@ usbs_status usbs_rowgemm(usbs_ctx* ctx, int64_t n, const double* X, int64_t ldx,
                          int64_t ldy0, double* Y, int64_t ldy) {
   USBS_API_BEGIN
   if (ka < 1 || kb < 1 || ka > 64 || ka * kb > 4096) fail(USBS_ERR_SHAPE, "rowgemm: ka <= 64, ka*kb <= 4096");
-  k_rowgemm<<<nblocks(ctx, n * kb), 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y,
-                                                           ldy);
+  const char* ev = getenv("USBS_ROWGEMM_V1");
+  if (kb <= 32 && !(ev && ev[0] == '1')) {
+    // a thread per output row (A/B: USBS_ROWGEMM_V1=1 -> a thread per entry)
+    const int bl = nblocks(ctx, n);
+    if (kb <= 4) k_rowgemm_rt<4><<<bl, 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y, ldy);
+    else if (kb <= 8) k_rowgemm_rt<8><<<bl, 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y, ldy);
+    else if (kb <= 12) k_rowgemm_rt<12><<<bl, 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y, ldy);
+    else if (kb <= 16) k_rowgemm_rt<16><<<bl, 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y, ldy);
+    else if (kb <= 24) k_rowgemm_rt<24><<<bl, 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y, ldy);
+    else k_rowgemm_rt<32><<<bl, 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y, ldy);
+  } else {
+    k_rowgemm<<<nblocks(ctx, n * kb), 256, 0, ctx->stream>>>(n, X, ldx, ka, B, ldb, kb, xs, alpha, beta, Y0, ldy0, Y,
+                                                             ldy);
+  }
   check_launch(ctx);
   USBS_API_END
 }
