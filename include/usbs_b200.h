@@ -278,6 +278,13 @@ usbs_status usbs_gather_rows(usbs_ctx* ctx, int64_t n, int k, const int64_t* idx
                              int64_t lds, double* dst_dev, int64_t ldd);
 
 /* ---- rounding -------------------------------------- */
+/* make_test_matrix (sketch.py:25-27): rows [row0, row1) of
+ * np.random.RandomState(seed & 0x7FFFFFFF).standard_normal((n, r)) into
+ * host memory out (C order), bit-identical to numpy's legacy MT19937 +
+ * polar Gaussian.  Host-only (no device, no context): native so the fill
+ * runs outside the Python GIL while the problem is planned. */
+usbs_status usbs_make_test_matrix(int64_t seed, int64_t n, int r, int64_t row0, int64_t row1, double* out);
+
 /* maxcut_round (rounding.py:34-51): for every column j of the factor U
  * (n x r, dev, row-major, ld >= r, r <= 64) the cut value of
  * x = sign(U[:, j]) (zero signs to +1), 0.25 x^T L x = sum_e w_e [x_u != x_v]

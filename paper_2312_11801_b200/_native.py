@@ -75,6 +75,7 @@ PROTOS = {
     "usbs_cons_compressed_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _i64]),
     "usbs_perm_rows": (_i32, [_p, _i32, _p, _p, _p, _p]),
     "usbs_maxcut_round": (_i32, [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i32, _pd, _pi, _p]),
+    "usbs_make_test_matrix": (_i32, [_i64, _i64, _i32, _i64, _i64, _p]),
 }
 
 # VecOp codes (csrc/usbs_book.cu)

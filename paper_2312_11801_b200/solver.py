@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -117,12 +118,63 @@ class Residuals:
 _PSI_POOL = None
 
 
+def make_test_matrix_rows(n, r, seed, r0, r1) -> np.ndarray:
+    """Rows [r0, r1) of make_test_matrix(n, r, seed) (sketch.py:25-27),
+    filled by the library's native restatement of numpy's legacy generator
+    (usbs_make_test_matrix, bit-identical; the ctypes call releases the GIL,
+    so the fill overlaps the Python-side setup instead of contending with
+    it)."""
+    from ._native import check, load
+    out = np.empty((r1 - r0, r), dtype=np.float64)
+    check(load().usbs_make_test_matrix(int(seed), int(n), int(r), int(r0), int(r1), out.ctypes.data),
+          "make_test_matrix")
+    return out
+
+
 def _psi_async(n, r, seed, r0, r1):
     global _PSI_POOL
     if _PSI_POOL is None:
         from concurrent.futures import ThreadPoolExecutor
         _PSI_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="usbs-psi")
-    return _PSI_POOL.submit(lambda: np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))[r0:r1])
+    return _PSI_POOL.submit(make_test_matrix_rows, n, r, seed, r0, r1)
+
+
+# tall factors from this many rows on take the device thin SVD at exit
+DEVICE_SVD_MIN_ROWS = 65536
+
+
+def thin_svd_device(eng, B):
+    """Thin SVD of a tall device matrix B (n x c) as U (host) and the singular
+    values: CholQR2 on the device (two Gram + row-GEMM rounds, B = Q R with
+    R = R2 R1, both Cholesky factors from the c x c Grams on the host), then
+    LAPACK's SVD of the c x c R on the host and U = Q U_R on the device --
+    the O(n c^2) work on the GPU, O(c^3) on the host (the reference's
+    np.linalg.svd of the whole n x c factor costs ~0.2 s at n = 10^6).
+    Column signs follow LAPACK's SVD of R, not of B (singular vectors are
+    defined up to sign; the sign-insensitive MaxCut rounding is the large-n
+    use).  Returns None when a Gram is not numerically positive definite
+    (condition number beyond CholQR2's ~1e8), and the caller falls back to
+    the host SVD."""
+    import scipy.linalg as sla
+
+    rt = eng.rt
+    n, c = B.shape
+    G = rt.empty(c, c)
+    eng.gram(B, B, G, sym=True)
+    try:
+        r1 = np.linalg.cholesky(G.cpu().numpy()).T  # G = R1^T R1
+    except np.linalg.LinAlgError:
+        return None
+    eye = np.eye(c)
+    Q1 = eng.rowgemm(B, rt.upload(sla.solve_triangular(r1, eye)), rt.empty(n, c))
+    eng.gram(Q1, Q1, G, sym=True)
+    try:
+        r2 = np.linalg.cholesky(G.cpu().numpy()).T
+    except np.linalg.LinAlgError:
+        return None
+    ur, sv, _ = np.linalg.svd(r2 @ r1)
+    U = eng.rowgemm(Q1, rt.upload(sla.solve_triangular(r2, eye) @ ur), rt.empty(n, c))
+    return U.cpu().numpy(), sv
 
 
 class DeviceSketchStore:
@@ -213,6 +265,11 @@ class DeviceSketchStore:
             full = rt.empty(n, half.shape[1])
             self.comm.allgather_rows(half, full, self.shard)
             half = full
+        elif half.shape[0] >= DEVICE_SVD_MIN_ROWS and not os.environ.get("USBS_HOST_SVD"):
+            res = thin_svd_device(eng, half)
+            if res is not None:
+                u, sv = res
+                return u, np.maximum(sv ** 2 - shift, 0.0)
         u, sv, _ = np.linalg.svd(half.cpu().numpy(), full_matrices=False)
         return u, np.maximum(sv ** 2 - shift, 0.0)
 

@@ -50,3 +50,22 @@ def test_status_mapping_matches_reference_exceptions():
         with pytest.raises(exc):
             _native.check(code, "probe")
     _native.check(0)
+
+
+def test_make_test_matrix_bit_exact_with_numpy():
+    """usbs_make_test_matrix (host-only entry point, callable without a GPU)
+    equals make_test_matrix (sketch.py:25-27) = numpy's legacy
+    RandomState(seed & 0x7FFFFFFF).standard_normal((n, r)) bit for bit, for
+    row slices (the sharded sketch) and seeds above 2^31."""
+    import numpy as np
+
+    from paper_2312_11801_b200 import _native
+    if not _native.LIB_PATH.exists():
+        pytest.skip("library not built (run __graft_entry__.build())")
+    from paper_2312_11801_b200.solver import make_test_matrix_rows
+    for n, r, seed, r0, r1 in ((1000, 10, 5, 0, 1000), (1001, 7, 2**31 + 17, 3, 900), (1, 1, 0, 0, 1),
+                               (0, 5, 1, 0, 0), (20000, 20, 123456789, 100, 19999)):
+        want = np.random.RandomState(int(seed) & 0x7FFFFFFF).standard_normal((n, r))[r0:r1]
+        assert np.array_equal(make_test_matrix_rows(n, r, seed, r0, r1), want)
+    with pytest.raises(ValueError):
+        make_test_matrix_rows(10, 2, 0, 5, 11)

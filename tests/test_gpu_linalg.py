@@ -6,7 +6,9 @@ import numpy as np
 import pytest
 
 from conftest import cuda_ok
+from helpers import random_graph
 from oracle import usbs_cpu as O
+from paper_2312_11801_b200 import instances as inst
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
 
@@ -66,3 +68,27 @@ def test_sketch_update_and_reconstruct_match_oracle():
         L.sketch_update(s, -1.0, v, qm, lams)
     with pytest.raises(ValueError):
         L.sketch_update(s, 1.0, v, qm, -lams)
+
+
+@pytest.mark.parametrize("kappa", [1e2, 1e6])
+def test_thin_svd_device_vs_lapack(kappa):
+    """Exit-time thin SVD of a tall factor on the device (CholQR2 + the c x c
+    SVD on the host, solver.thin_svd_device) against LAPACK on the whole
+    matrix: singular values to rounding, U orthonormal, each singular
+    vector equal up to sign."""
+    from paper_2312_11801_b200 import solver as S
+    from paper_2312_11801_b200.engine import Engine
+    from paper_2312_11801_b200.runtime import DeviceProblem
+    rng = np.random.default_rng(5)
+    n, c = 100_000, 10
+    qa, _ = np.linalg.qr(rng.standard_normal((n, c)))
+    qb, _ = np.linalg.qr(rng.standard_normal((c, c)))
+    sv = np.logspace(0, -np.log10(kappa), c)
+    b = (qa * sv) @ qb.T
+    dp = DeviceProblem(inst.maxcut_problem(random_graph(50, 0.2, 1)))
+    eng = Engine(dp)
+    u, s = S.thin_svd_device(eng, dp.rt.upload(b))
+    u0, s0, _ = np.linalg.svd(b, full_matrices=False)
+    np.testing.assert_allclose(s, s0, rtol=1e-10, atol=1e-15 * s0[0])
+    assert np.abs(u.T @ u - np.eye(c)).max() <= 1e-12
+    np.testing.assert_allclose(np.abs(np.sum(u * u0, axis=0)), np.ones(c), atol=1e-9)
