@@ -18,6 +18,27 @@
 #include "usbs_common.cuh"
 #include "usbs_kernels.cuh"
 
+// std::allocator whose value construction default-initialises (no zero fill
+// for arithmetic types): for host arrays that are written completely anyway
+template <typename T>
+struct DefaultInitAlloc : std::allocator<T> {
+  template <typename U>
+  struct rebind {
+    using other = DefaultInitAlloc<U>;
+  };
+  DefaultInitAlloc() = default;
+  template <typename U>
+  DefaultInitAlloc(const DefaultInitAlloc<U>&) {}
+  template <typename U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <typename U, typename... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+
 namespace usbs {
 void staged_h2d(usbs_ctx* ctx, void* dst, const void* src, size_t bytes) {
   constexpr size_t CH = 8u << 20;
@@ -514,8 +535,9 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   std::vector<int64_t> slot_of_x(xcnt[n]);
   const int nthr = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
                                                               n / 4096 + 1));
-  std::vector<int32_t> col;
-  std::vector<double> cval;
+  // merged columns / values: filled completely below, so not zero-initialised
+  std::vector<int32_t, DefaultInitAlloc<int32_t>> col;
+  std::vector<double, DefaultInitAlloc<double>> cval;
   {
     std::vector<std::string> errs(nthr);
     auto merge_rows = [&](int th, int64_t i0, int64_t i1, bool write) {
@@ -572,16 +594,31 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     // diagonal inserted -- no per-row sort
     bool fast = diag_only && !directed;
     if (fast) {
-      for (int64_t i = 0; i < n && fast; ++i)
-        for (int64_t z = c_indptr[i] + 1; z < c_indptr[i + 1]; ++z)
-          if (c_indices[z] <= c_indices[z - 1]) { fast = false; break; }
+      // one threaded pass: rows strictly increasing (sorted, no duplicates),
+      // columns in range, merged row lengths (the diagonal added if absent)
+      std::vector<char> ok(nthr, 1), inrange(nthr, 1);
+      auto scan = [&](int th, int64_t i0, int64_t i1) {
+        for (int64_t i = i0; i < i1; ++i) {
+          bool has = false;
+          for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) {
+            const int32_t c = c_indices[z];
+            if (c < 0 || c >= n_cols) inrange[th] = 0;
+            if (z > c_indptr[i] && c <= c_indices[z - 1]) ok[th] = 0;
+            has |= (c == i);
+          }
+          rowptr[i + 1] = (c_indptr[i + 1] - c_indptr[i]) + (has ? 0 : 1);
+        }
+      };
+      std::vector<std::thread> ts;
+      for (int th = 0; th < nthr; ++th) ts.emplace_back(scan, th, n * th / nthr, n * (th + 1) / nthr);
+      for (auto& t : ts) t.join();
+      for (int th = 0; th < nthr; ++th) {
+        if (!inrange[th]) fail(USBS_ERR_SHAPE, "cost column index out of range");
+        fast = fast && ok[th];
+      }
     }
     if (fast) {
-      for (int64_t i = 0; i < n; ++i) {
-        bool has = false;
-        for (int64_t z = c_indptr[i]; z < c_indptr[i + 1]; ++z) has |= (c_indices[z] == i);
-        rowptr[i + 1] = rowptr[i] + (c_indptr[i + 1] - c_indptr[i]) + (has ? 0 : 1);
-      }
+      for (int64_t i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
       col.resize(rowptr[n]);
       cval.resize(rowptr[n]);
       auto fill = [&](int64_t i0, int64_t i1) {
@@ -607,12 +644,11 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
           }
         }
       };
-      for (int64_t z = 0; z < c_indptr[n]; ++z)
-        if (c_indices[z] < 0 || c_indices[z] >= n_cols) fail(USBS_ERR_SHAPE, "cost column index out of range");
       std::vector<std::thread> ts;
       for (int th = 0; th < nthr; ++th) ts.emplace_back(fill, n * th / nthr, n * (th + 1) / nthr);
       for (auto& t : ts) t.join();
     } else {
+      std::fill(rowptr.begin(), rowptr.end(), 0);
       run(false);
       for (int64_t i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
       col.resize(rowptr[n]);
@@ -783,6 +819,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->cval = dev_upload(p, cval.data(), cval.size());
   p->zval = dev_alloc<double>(p, p->nnz);
   USBS_CUDA(cudaMemcpy(p->zval, p->cval, p->nnz * sizeof(double), cudaMemcpyDeviceToDevice));
+  PT("  upload C pattern + values");
   if (!lazy_slots) {
     p->aptr = dev_upload(p, aptr.data(), aptr.size());
     p->aent = dev_upload(p, aent.data(), aent.size());
@@ -797,6 +834,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     p->e_col = dev_upload(p, ec.data(), ne);
     p->e_val = dev_upload(p, e_vals, ne);
   }
+  PT("  upload entries");
   if (p->diag_only) p->diag_slot = dev_upload(p, diag_slot.data(), n);
   {
     std::vector<int32_t> cptr(m + 1, 0), cent(ne);
@@ -809,6 +847,7 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
     p->cent = dev_upload(p, cent.data(), cent.size());
     p->max_entries_per_cons = mx;
   }
+  PT("  constraint lists");
   {
     std::vector<int32_t> lr, lb, le, ls;
     for (size_t t = 0; t < irow.size(); ++t) {
