@@ -424,7 +424,133 @@ __device__ int chol_tiled(double* __restrict__ Mp, int d, double* __restrict__ r
   return 1;
 }
 
+// C_IK -= sum over DEPTH columns c0.. of L_I L_K^T for up to NT consecutive
+// tiles K0.. of tile row I (independent accumulator chains, the row's
+// fragments loaded once); rows/columns >= N masked
+template <int DEPTH, int NT>
+__device__ __forceinline__ void tiles_update(double* __restrict__ Mp, int N, int c0, int I, int K0, int nt) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int ra = I * 8 + g;
+  const bool va = ra < N;
+  const int oa = va ? pidx(ra, 0) : 0;
+  double af[DEPTH / 4];
+#pragma unroll
+  for (int s = 0; s < DEPTH / 4; ++s) af[s] = va ? -Mp[oa + c0 + 4 * s + q] : 0.0;
+  double c0v[NT], c1v[NT];
+  int ob[NT];
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int rb = (K0 + u) * 8 + g;
+    ob[u] = (u < nt && rb < N) ? pidx(rb, 0) : -1;
+    const int cc = (K0 + u) * 8 + 2 * q;
+    c0v[u] = (u < nt && va && cc <= ra) ? Mp[oa + cc] : 0.0;
+    c1v[u] = (u < nt && va && cc + 1 <= ra) ? Mp[oa + cc + 1] : 0.0;
+  }
+#pragma unroll
+  for (int s = 0; s < DEPTH / 4; ++s) {
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+      if (u < nt) {
+        const double b = ob[u] >= 0 ? Mp[ob[u] + c0 + 4 * s + q] : 0.0;
+        dmma8x8x4(c0v[u], c1v[u], af[s], b, c0v[u], c1v[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int cc = (K0 + u) * 8 + 2 * q;
+    if (u < nt && va && cc <= ra) Mp[oa + cc] = c0v[u];
+    if (u < nt && va && cc + 1 <= ra) Mp[oa + cc + 1] = c1v[u];
+  }
+}
+
+// The 16 x 16 diagonal block at j0 by warp 0 alone (no block barrier):
+// diag8, the 8 rows below it by substitution (a lane per row), their 8 x 8
+// tile update on the tensor cores, diag8.  Sets *flag (potrf semantics).
+__device__ void chol_diag16_warp(double* __restrict__ Mp, int N, int j0, double* __restrict__ rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int JB = min(16, N - j0);
+  chol_diag8(Mp, N, j0 >> 3, rdiag, flag);
+  __syncwarp();
+  if (JB <= 8 || !*(volatile int*)flag) return;
+  const int i = j0 + 8 + lane;
+  if (lane < JB - 8) {
+    double v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = Mp[pidx(i, j0 + c)];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      v[c] *= rdiag[j0 + c];
+#pragma unroll
+      for (int t = c + 1; t < 8; ++t) v[t] = fma(-v[c], Mp[pidx(j0 + t, j0 + c)], v[t]);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) Mp[pidx(i, j0 + c)] = v[c];
+  }
+  __syncwarp();
+  tiles_update<8, 1>(Mp, N, j0, (j0 + 8) >> 3, (j0 + 8) >> 3, 1);
+  __syncwarp();
+  chol_diag8(Mp, N, (j0 + 8) >> 3, rdiag, flag);
+  __syncwarp();
+}
+
+// Blocked right-looking Cholesky of the packed lower N x N matrix in
+// 16-column panels (profiles/mb/chol_mb.cu: d + 1 = 211 150.9k -> 122.1k
+// cycles against the 8-column form): warp 0 factors the diagonal block
+// without block barriers, all threads solve the panel rows (x L_JJ^T = v, a
+// thread per row, right-looking inside the row: the substitution's
+// operations in its order), the trailing update is 16 deep (four m8n8k4
+// per tile, groups of four tiles per warp); warp 0 looks ahead: it updates
+// the next diagonal block's tiles first and factors it while the other
+// warps run the rest of the trailing update.  Two barriers per panel.
+// rdiag[j] = 1 / L_jj.  Returns 0 on failure (uniform).  Own register
+// allocation (noinline).
+__device__ __noinline__ int chol_p16(double* __restrict__ Mp, int N, double* __restrict__ rdiag, int* flag) {
+  const int tid = threadIdx.x, warp = tid >> 5, nwp = blockDim.x >> 5, nth = blockDim.x;
+  const int T = (N + 7) >> 3;
+  if (warp == 0) chol_diag16_warp(Mp, N, 0, rdiag, flag);
+  __syncthreads();
+  if (!*flag) return 0;
+  for (int j0 = 0; j0 < N; j0 += 16) {
+    const int JB = min(16, N - j0), r0 = j0 + JB;
+    if (r0 >= N) break;  // JB == 16 from here on
+    for (int i = r0 + tid; i < N; i += nth) {
+      double* ri = Mp + pidx(i, j0);
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = ri[c];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        v[c] *= rdiag[j0 + c];
+#pragma unroll
+        for (int t = c + 1; t < 16; ++t) v[t] = fma(-v[c], Mp[pidx(j0 + t, j0 + c)], v[t]);
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) ri[c] = v[c];
+    }
+    __syncthreads();
+    const int a = r0 >> 3;  // first trailing tile row
+    if (warp == 0) {
+      tiles_update<16, 1>(Mp, N, j0, a, a, 1);
+      if (a + 1 < T) tiles_update<16, 2>(Mp, N, j0, a + 1, a, 2);
+      __syncwarp();
+      chol_diag16_warp(Mp, N, r0, rdiag, flag);
+    } else {
+      for (int I = T - warp; I >= a + 2; I -= nwp - 1)
+        for (int K0 = a; K0 <= I; K0 += 4) tiles_update<16, 4>(Mp, N, j0, I, K0, min(4, I - K0 + 1));
+    }
+    __syncthreads();
+    if (!*flag) return 0;
+  }
+  return 1;
+}
+
 // ---------------------------------------------------------------- kernel
+// P16: the 16-column-panel Cholesky (d + 1 >= 100: C3 / C5, d = 210); the
+// 8-column form otherwise (d = 66: 15.3 vs 18.8 us).  Two instantiations so
+// each kernel carries one factorisation (code size and register allocation
+// of the kernel otherwise cost the gain).
+template <bool P16>
 __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int k = a.k, d = a.d, kk = k * k, tid = threadIdx.x, nth = blockDim.x;
@@ -655,7 +781,10 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       // 8-column panels with the trailing update on the FP64 tensor cores;
       // rdiag keeps 1 / L_jj for the solves (f1 is dead once rhs is formed)
       double* rdiag = sm.f1;
-      if (!chol_tiled(Mp, d + 1, rdiag, &sm.flg[5])) fail = 1;
+      int chol_ok;
+      if constexpr (P16) chol_ok = chol_p16(Mp, d + 1, rdiag, &sm.flg[5]);
+      else chol_ok = chol_tiled(Mp, d + 1, rdiag, &sm.flg[5]);
+      if (!chol_ok) fail = 1;
       IPM_MARK(4);
       if (!fail) {
         const int lane = tid & 31;
@@ -857,10 +986,15 @@ size_t ipm_smem_bytes(int k) {
 }
 
 void launch_ipm(usbs_ctx* ctx, const IpmArgs& a) {
-  smem_optin(ctx, (const void*)k_ipm, 227 * 1024);
   size_t sm = ipm_smem_bytes(a.k);
   IpmArgs b = a;
-  k_ipm<<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+  if (a.d + 1 >= 100) {
+    smem_optin(ctx, (const void*)k_ipm<true>, 227 * 1024);
+    k_ipm<true><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+  } else {
+    smem_optin(ctx, (const void*)k_ipm<false>, 227 * 1024);
+    k_ipm<false><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+  }
   check_launch(ctx);
 }
 

@@ -634,6 +634,158 @@ __device__ int chol_r32(double* Mp, int N, double* rdiag, int* flag) {
   return 1;
 }
 
+
+// 16-column panels: warp 0 factors the 16 x 16 diagonal block without block
+// barriers (diag8, an 8-row substitution, one DMMA tile update, diag8), all
+// threads solve the panel rows (16-column right-looking row solves), the
+// trailing update is 16 deep; warp 0 looks ahead (updates and factors the
+// next diagonal block while the other warps run the trailing update)
+__device__ void diag16_warp(double* Mp, int N, int j0, double* rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int JB = min(16, N - j0);
+  diag8<4>(Mp, j0, rdiag, flag, N);
+  __syncwarp();
+  if (JB <= 8 || !*(volatile int*)flag) return;
+  const int i = j0 + 8 + lane;
+  if (lane < JB - 8) {
+    double v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = Mp[pidx(i, j0 + c)];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      v[c] *= rdiag[j0 + c];
+#pragma unroll
+      for (int t = c + 1; t < 8; ++t) v[t] = fma(-v[c], Mp[pidx(j0 + t, j0 + c)], v[t]);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) Mp[pidx(i, j0 + c)] = v[c];
+  }
+  __syncwarp();
+  tiles_update<8, 1>(Mp, N, j0, (j0 + 8) >> 3, (j0 + 8) >> 3, 1);
+  __syncwarp();
+  diag8<4>(Mp, j0 + 8, rdiag, flag, N);
+  __syncwarp();
+}
+
+__device__ int chol_p16(double* Mp, int N, double* rdiag, int* flag) {
+  const int tid = threadIdx.x, warp = tid >> 5, nwp = blockDim.x >> 5, nth = blockDim.x;
+  const int T = (N + 7) >> 3;
+  if (warp == 0) diag16_warp(Mp, N, 0, rdiag, flag);
+  __syncthreads();
+  if (!*flag) return 0;
+  for (int j0 = 0; j0 < N; j0 += 16) {
+    const int JB = min(16, N - j0), r0 = j0 + JB;
+    if (r0 >= N) break;
+    // panel rows below: x L_JJ^T = v, 16 columns, a thread per row
+    for (int i = r0 + tid; i < N; i += nth) {
+      double* ri = Mp + pidx(i, j0);
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = ri[c];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        v[c] *= rdiag[j0 + c];
+#pragma unroll
+        for (int t = c + 1; t < 16; ++t) v[t] = fma(-v[c], Mp[pidx(j0 + t, j0 + c)], v[t]);
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) ri[c] = v[c];
+    }
+    __syncthreads();
+    const int a = r0 >> 3;  // first trailing tile row
+    if (warp == 0) {
+      // rows a, a+1 of the trailing update (the next diagonal block), then its factorisation
+      tiles_update<16, 1>(Mp, N, j0, a, a, 1);
+      if (a + 1 < T) tiles_update<16, 2>(Mp, N, j0, a + 1, a, 2);
+      __syncwarp();
+      diag16_warp(Mp, N, r0, rdiag, flag);
+    } else {
+      // rows a+2 .. T-1 (all their tiles K = a .. I), longest first, in
+      // groups of four tiles
+      for (int I = T - warp; I >= a + 2; I -= nwp - 1)
+        for (int K0 = a; K0 <= I; K0 += 4) tiles_update<16, 4>(Mp, N, j0, I, K0, min(4, I - K0 + 1));
+    }
+    __syncthreads();
+    if (!*flag) return 0;
+  }
+  return 1;
+}
+
+
+// generic W-column panels (W = 8 nb): warp 0 factors the W x W diagonal
+// block as nb diag8 steps with in-warp substitutions and DMMA tile updates
+template <int W>
+__device__ void diagW_warp(double* Mp, int N, int j0, double* rdiag, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int JB = min(W, N - j0);
+  for (int s = 0; s * 8 < JB; ++s) {
+    const int c0 = j0 + 8 * s;
+    diag8<4>(Mp, c0, rdiag, flag, N);
+    __syncwarp();
+    if (!*(volatile int*)flag) return;
+    const int rb = c0 + 8, re = j0 + JB;  // rows of the block below sub-block s
+    if (rb >= re) break;
+    for (int i = rb + lane; i < re; i += 32) {
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = Mp[pidx(i, c0 + c)];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        v[c] *= rdiag[c0 + c];
+#pragma unroll
+        for (int t = c + 1; t < 8; ++t) v[t] = fma(-v[c], Mp[pidx(c0 + t, c0 + c)], v[t]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Mp[pidx(i, c0 + c)] = v[c];
+    }
+    __syncwarp();
+    const int a = rb >> 3, e = (re + 7) >> 3;
+    for (int I = a; I < e; ++I) tiles_update<8, 4>(Mp, re, c0, I, a, I - a + 1);
+    __syncwarp();
+  }
+}
+
+template <int W>
+__device__ int chol_pw(double* Mp, int N, double* rdiag, int* flag) {
+  const int tid = threadIdx.x, warp = tid >> 5, nwp = blockDim.x >> 5, nth = blockDim.x;
+  const int T = (N + 7) >> 3;
+  if (warp == 0) diagW_warp<W>(Mp, N, 0, rdiag, flag);
+  __syncthreads();
+  if (!*flag) return 0;
+  for (int j0 = 0; j0 < N; j0 += W) {
+    const int JB = min(W, N - j0), r0 = j0 + JB;
+    if (r0 >= N) break;
+    for (int i = r0 + tid; i < N; i += nth) {
+      double* ri = Mp + pidx(i, j0);
+      double v[W];
+#pragma unroll
+      for (int c = 0; c < W; ++c) v[c] = ri[c];
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        v[c] *= rdiag[j0 + c];
+#pragma unroll
+        for (int t = c + 1; t < W; ++t) v[t] = fma(-v[c], Mp[pidx(j0 + t, j0 + c)], v[t]);
+      }
+#pragma unroll
+      for (int c = 0; c < W; ++c) ri[c] = v[c];
+    }
+    __syncthreads();
+    const int a = r0 >> 3, nb = W / 8;
+    const int ad = min(T, a + nb);  // tile rows of the next diagonal block
+    if (warp == 0) {
+      for (int I = a; I < ad; ++I) tiles_update<W, 4>(Mp, N, j0, I, a, I - a + 1);
+      __syncwarp();
+      diagW_warp<W>(Mp, N, r0, rdiag, flag);
+    } else {
+      for (int I = T - warp; I >= ad; I -= nwp - 1)
+        for (int K0 = a; K0 <= I; K0 += 4) tiles_update<W, 4>(Mp, N, j0, I, K0, min(4, I - K0 + 1));
+    }
+    __syncthreads();
+    if (!*flag) return 0;
+  }
+  return 1;
+}
+
 template <int V>
 __global__ void __launch_bounds__(512, 1) k_chol(const double* g, double* out, long long* cyc, int d, int reps) {
   extern __shared__ double M[];
@@ -646,6 +798,10 @@ __global__ void __launch_bounds__(512, 1) k_chol(const double* g, double* out, l
     __syncthreads();
     long long t0 = clock64();
     if (V == 2) chol_r32(M, d, rd, &flag);
+    else if (V == 3) chol_p16(M, d, rd, &flag);
+    else if (V == 4) chol_pw<16>(M, d, rd, &flag);
+    else if (V == 5) chol_pw<24>(M, d, rd, &flag);
+    else if (V == 6) chol_pw<32>(M, d, rd, &flag);
     else chol_tiled<V>(M, d, rd, &flag);
     __syncthreads();
     tot = min(tot, clock64() - t0);
@@ -758,10 +914,18 @@ int main() {
     cudaFuncSetAttribute(k_chol<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_chol<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_chol<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    for (int v = 0; v < 3; ++v) {
+    cudaFuncSetAttribute(k_chol<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_chol<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_chol<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_chol<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    for (int v = 0; v < 7; ++v) {
       if (v == 0) k_chol<0><<<1, 512, sm>>>(dg, dout, dc, d, 3);
       else if (v == 1) k_chol<1><<<1, 512, sm>>>(dg, dout, dc, d, 3);
-      else k_chol<2><<<1, 512, sm>>>(dg, dout, dc, d, 3);
+      else if (v == 2) k_chol<2><<<1, 512, sm>>>(dg, dout, dc, d, 3);
+      else if (v == 3) k_chol<3><<<1, 512, sm>>>(dg, dout, dc, d, 3);
+      else if (v == 4) k_chol<4><<<1, 512, sm>>>(dg, dout, dc, d, 3);
+      else if (v == 5) k_chol<5><<<1, 512, sm>>>(dg, dout, dc, d, 3);
+      else k_chol<6><<<1, 512, sm>>>(dg, dout, dc, d, 3);
       cudaError_t e = cudaDeviceSynchronize();
       cudaMemcpy(c, dc, 8, cudaMemcpyDeviceToHost);
       cudaMemcpy(L.data(), dout, 8 * L.size(), cudaMemcpyDeviceToHost);
