@@ -23,6 +23,7 @@
 
 #include "usbs_common.cuh"
 #include "usbs_kernels.cuh"
+#include "usbs_tma.cuh"
 
 namespace usbs {
 
@@ -41,6 +42,7 @@ struct IpmArgs {
   double* state;       // out state (may alias warm)
   double* result;      // [value, newton_iters, exact, eta_opt, failures]
   double* gM;          // global scratch for M when d > SMEM_D
+  double* gQp;         // global scratch: Q11 packed lower (k_ipm<true>, d <= SMEM_D)
   IpmOpts o;
   unsigned long long* prof;  // optional phase timers (ns), thread 0
 };
@@ -74,6 +76,7 @@ struct IpmSmem {
   double* red;   // 32
   double* sc;    // scalars 64
   int* flg;      // 16
+  uint64_t* bar; // packed-Q11 copy barrier
   double* M;
 };
 
@@ -227,6 +230,30 @@ __device__ void blk_gemv_q11(const double* Q, const double* x, int d, double* y)
         const double xq = x[q];
 #pragma unroll
         for (int u = 0; u < 4; ++u) s[u] = fma(qv[u], xq, s[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double t = warp_sum(s[u]);
+      if (lane == 0 && p0 + u < d) y[p0 + u] = t;
+    }
+  }
+}
+
+// y = Q x for a symmetric Q stored packed lower in shared memory: row p is
+// Q[p][0..p] (contiguous) and Q[q][p] for q > p (column p of the lower part);
+// four rows per warp in flight
+__device__ void blk_gemv_packed(const double* __restrict__ Mp, const double* __restrict__ x, int d,
+                                double* __restrict__ y) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int p0 = 4 * w; p0 < d; p0 += 4 * nw) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = lane; q < d; q += 32) {
+      const double xq = x[q];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = p0 + u;
+        if (p < d) s[u] = fma(q <= p ? Mp[pidx(p, q)] : Mp[pidx(q, p)], xq, s[u]);
       }
     }
 #pragma unroll
@@ -557,17 +584,20 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   const int has_eta = a.has_eta;
   IpmSmem sm;
   double* base = (double*)smem_raw;
-  sm.S = base; sm.T = sm.S + kk; sm.H = sm.T + kk; sm.dS = sm.H + kk; sm.dT = sm.dS + kk;
+  const bool m_in_smem = d <= SMEM_D;
+  // P16: M first (16-byte aligned for the bulk copy of packed Q11 into it)
+  const int mfirst = (P16 && m_in_smem) ? (((d + 1) * (d + 2) / 2 + 1) & ~1) : 0;
+  sm.S = base + mfirst; sm.T = sm.S + kk; sm.H = sm.T + kk; sm.dS = sm.H + kk; sm.dT = sm.dS + kk;
   sm.W1 = sm.dT + kk; sm.W2 = sm.W1 + kk; sm.X1 = sm.W2 + kk; sm.X2 = sm.X1 + kk;
   sm.s = sm.X2 + kk; sm.t = sm.s + d; sm.vI = sm.t + d; sm.h = sm.vI + d; sm.g = sm.h + d;
   sm.f1 = sm.g + d; sm.rhs = sm.f1 + d + 1;  // f1: d + 1 entries (rdiag of the augmented factor)
   sm.ds = sm.rhs + d; sm.dt = sm.ds + d; sm.rd = sm.dt + d;
   sm.tmp = sm.rd + d; sm.cb0 = sm.tmp + d; sm.cb1 = sm.cb0 + d;
   sm.red = sm.cb1 + d; sm.sc = sm.red + 32;
-  sm.M = sm.sc + 64;
-  const bool m_in_smem = d <= SMEM_D;
+  sm.bar = (uint64_t*)(sm.sc + 64);  // P16 only (the 8-column kernel keeps M right after sc)
+  sm.M = (P16 && m_in_smem) ? base : sm.sc + 64;
   double* Mp = m_in_smem ? sm.M : a.gM;
-  unsigned char* ub = (unsigned char*)(sm.M + (m_in_smem ? (d + 1) * (d + 2) / 2 : 0));
+  unsigned char* ub = (unsigned char*)(sm.sc + (P16 ? 66 : 64) + ((m_in_smem && !P16) ? (d + 1) * (d + 2) / 2 : 0));
   sm.pi = ub; sm.pj = ub + 600;
   sm.flg = (int*)(ub + 1200);
   sm.ctab = (unsigned short*)(ub + 1264);
@@ -583,6 +613,10 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     int p = 0;
     for (int j = 0; j < k; ++j)
       for (int i = j; i < k; ++i) { sm.pi[p] = (unsigned char)i; sm.pj[p] = (unsigned char)j; ++p; }
+    if (P16) {
+      mbar_init(sm.bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   }
   __syncthreads();
   for (int p = tid; p < d; p += nth) {
@@ -637,11 +671,37 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   }
   __syncthreads();
   mu = blk_compl(sm, k, eta, zeta, omega, has_eta) / (2.0 * pairs);
-  // ---- coefficient scale (subqp.py:376-382)
+  // ---- coefficient scale (subqp.py:376-382).  P16: Q11 also packed lower
+  // into gQp (bulk-copied into M's slot every Newton step, where it serves
+  // the stationarity product and the base of M; 16-byte multiples, so one
+  // pad entry, landing on row d's first entry, which the right-hand side
+  // overwrites) and checked for exact symmetry (the packed product assumes
+  // it; an asymmetric Q11 is read row-wise from global)
+  const bool packed = P16 && a.Q11 && m_in_smem && a.gQp;
+  const uint32_t qbytes = (uint32_t)(((d * (d + 1) / 2 + 1) & ~1) * sizeof(double));
+  int asym = 0;
   double qmax = 0.0;
   if (a.Q11) {
     double v = 0.0;
-    for (int x = tid; x < d * d; x += nth) v = fmax(v, fabs(a.Q11[x]));
+    if (packed) {
+      const int lane = tid & 31, warp = tid >> 5, nwp = nth >> 5;
+      int bad = 0;
+      for (int p = warp; p < d; p += nwp) {
+        const double* qr = a.Q11 + (int64_t)p * d;
+        for (int q = lane; q < d; q += 32) {
+          const double x = __ldg(qr + q);
+          v = fmax(v, fabs(x));
+          if (q <= p) {
+            a.gQp[pidx(p, q)] = x;
+            if (x != __ldg(a.Q11 + (int64_t)q * d + p)) bad = 1;
+          }
+        }
+      }
+      fence_proxy_global();
+      asym = __syncthreads_or(bad);
+    } else {
+      for (int x = tid; x < d * d; x += nth) v = fmax(v, fabs(a.Q11[x]));
+    }
     v = warp_max(v);
     __syncthreads();
     if ((tid & 31) == 0) sm.red[tid >> 5] = v;
@@ -649,6 +709,27 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     for (int w = 0; w < nth / 32; ++w) qmax = fmax(qmax, sm.red[w]);
     __syncthreads();
   }
+  // the per-step copy of packed Q11 into M's slot (issued when M is dead)
+  uint32_t ph = 0;
+  bool pending = false;
+  auto issue_q = [&]() {
+    if (packed && !pending) {
+      fence_proxy_smem();  // every thread's generic accesses to M before the async-proxy write
+      __syncthreads();
+      if (tid == 0) {
+        mbar_expect_tx(sm.bar, qbytes);
+        bulk_g2s(sm.M, a.gQp, qbytes, sm.bar);
+      }
+      pending = true;
+    }
+  };
+  auto wait_q = [&]() {
+    if (pending) {
+      mbar_wait(sm.bar, ph);
+      ph ^= 1u;
+      pending = false;
+    }
+  };
   const double hmax = blk_max_abs(sm.h, d, sm.red);
   const double gmax = blk_max_abs(sm.g, d, sm.red);
   const double coeff_scale = 1.0 + fmax(fmax(fmax(hmax, fabs(h2)), qmax), fmax(gmax, fabs(q22e)));
@@ -659,11 +740,17 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   if (a.prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ipm_last));
   const double SQ2 = 1.4142135623730951;
   for (it = 1; it <= a.o.max_newton; ++it) {
+    issue_q();  // M is dead here
     // ---- stationarity (subqp.py:210-219)
     blk_svec(sm.S, k, d, sm, sm.s);
     blk_svec(sm.T, k, d, sm, sm.t);
     __syncthreads();
-    blk_gemv_q11(a.Q11, sm.s, d, sm.f1);
+    if (packed && !asym) {
+      wait_q();
+      blk_gemv_packed(sm.M, sm.s, d, sm.f1);
+    } else {
+      blk_gemv_q11(a.Q11, sm.s, d, sm.f1);
+    }
     __syncthreads();
     for (int p = tid; p < d; p += nth) {
       double f = sm.f1[p] + sm.h[p] - sm.t[p] + omega * sm.vI[p];
@@ -741,6 +828,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       }
       IPM_MARK(2);
       // M (packed lower): Q11 + E + low-rank; warp per row p, lanes over q <= p
+      // (Q11 already in place when packed)
+      wait_q();
       {
         const int lane = tid & 31, wid = tid >> 5, nwp = nth >> 5;
         const double* Hm = sm.H;
@@ -751,11 +840,11 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           const int i = sm.pi[p], j = sm.pj[p];
           const double wp = (i == j) ? 1.0 : SQ2;
           const double gp = sm.g[p], vp = sm.vI[p];
-          const double* qrow = a.Q11 ? a.Q11 + (int64_t)p * d : nullptr;
+          const double* qrow = (a.Q11 && !packed) ? a.Q11 + (int64_t)p * d : nullptr;
           const int base = p * (p + 1) / 2;
           double qn = (qrow && lane <= p) ? __ldg(qrow + lane) : 0.0;
           for (int q = lane; q <= p; q += 32) {
-            const double qv = qn;
+            const double qv = packed ? Mp[base + q] : qn;
             qn = (qrow && q + 32 <= p) ? __ldg(qrow + q + 32) : 0.0;
             const int kq = sm.pi[q], l = sm.pj[q];
             const double wq = (kq == l) ? 1.0 : SQ2;
@@ -825,6 +914,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           }
           __syncthreads();
         }
+        issue_q();  // M is dead: the next step's Q11 copy overlaps the rest of this step
         IPM_MARK(5);
         // E ds = svec((H D G + G D H)/2), D = smat(ds), G = T
         blk_smat(sm.ds, k, d, sm, sm.W1);
@@ -944,6 +1034,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
     if (failures > a.o.max_step_failures) break;
     mu = fmax(mu * 10.0, 10.0 * a.o.mu_tol);
   }
+  wait_q();  // no bulk copy may be outstanding at exit
   if (it > a.o.max_newton) it = a.o.max_newton;
   if (a.prof && tid == 0)
     for (int s = 0; s < 10; ++s) a.prof[s] += ipm_acc[s];
@@ -981,7 +1072,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
 
 size_t ipm_smem_bytes(int k) {
   const int d = k * (k + 1) / 2, kk = k * k;
-  size_t doubles = 9 * kk + 13 * d + 1 + 32 + 64 + (d <= SMEM_D ? (d + 1) * (d + 2) / 2 : 0);
+  size_t doubles = 9 * kk + 13 * d + 1 + 32 + 64 + 2 + (d <= SMEM_D ? ((d + 1) * (d + 2) / 2 + 1) : 0);
   return doubles * sizeof(double) + 1264 + 2 * (k * (k - 1) / 2 + 1) + 64;
 }
 
@@ -1019,6 +1110,9 @@ extern "C" usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const d
   a.state = state_out;
   a.result = result;
   a.gM = a.d > SMEM_D ? (double*)ctx->ws.get(WS_IPM, (size_t)(a.d + 1) * (a.d + 2) / 2 * sizeof(double)) : nullptr;
+  a.gQp = (Q11 && a.d <= SMEM_D && a.d + 1 >= 100)
+              ? (double*)ctx->ws.get(WS_IPM + 2, (size_t)((a.d * (a.d + 1) / 2 + 1) & ~1) * sizeof(double))
+              : nullptr;
   a.prof = nullptr;
   if (getenv("USBS_IPM_PROF")) {
     static bool zeroed = false;
