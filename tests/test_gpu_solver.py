@@ -59,15 +59,22 @@ def test_ipm_matches_reference_golden():
         np.testing.assert_allclose(e.s_opt, z[pre + "/evalS"], atol=1e-6)
 
 
-@pytest.mark.parametrize("k", [11, 20])
-def test_ipm_large_k_vs_oracle(k):
-    """d = 66 and d = 210 (the BASELINE bundle sizes), warm start included."""
+@pytest.mark.parametrize("k,skew", [(11, 0.0), (20, 0.0), (14, 0.0), (17, 0.0), (24, 0.0), (32, 0.0), (20, 1e-13)])
+def test_ipm_large_k_vs_oracle(k, skew):
+    """d = 66 and d = 210 (the BASELINE bundle sizes), warm start included;
+    the kernel variants by size: 8-column Cholesky (d + 1 < 100), 16-column
+    panels with Q11 bulk-copied into shared memory (d = 105, 153, 210), M in
+    global memory (d = 300, 528); an asymmetric Q11 (skew) takes the
+    row-wise stationarity product."""
     _, _, _, sp = mods()
     rng = np.random.default_rng(k)
     d = k * (k + 1) // 2
     a = rng.standard_normal((d + 5, d))
     zz = rng.standard_normal(d + 5)
-    q = O.Coeffs(a.T @ a / (d + 5), a.T @ zz / (d + 5), float(zz @ zz / (d + 5)), rng.standard_normal(d),
+    q11 = a.T @ a / (d + 5)
+    if skew:
+        q11[3, 1] += skew * abs(q11[3, 1])
+    q = O.Coeffs(q11, a.T @ zz / (d + 5), float(zz @ zz / (d + 5)), rng.standard_normal(d),
                  float(rng.standard_normal()), True, k)
     ro = O.ipm(q)
     r = sp.ipm_quad(q)
