@@ -11,8 +11,9 @@ from pathlib import Path
 LIB = Path(__file__).resolve().parents[1] / "paper_2312_11801_b200" / "_lib" / "libusbs_b200.so"
 CLASSES = ["DMMA", "DFMA", "DMUL", "DADD", "UBLKCP", "SYNCS", "LDG", "STG", "LDS", "STS", "LDGSTS", "SHFL",
            "BAR", "MEMBAR", "FENCE", "CCTL", "ATOM", "RED"]
-KEEP = ["k_lanczos_tma", "k_lanczos_cl", "k_lanczos", "k_spmv_fused", "k_spmm16x2", "k_gram_bulk", "k_kron_apply",
-        "k_compressed_mma", "k_ipm", "k_image_diag", "k_image_entries", "k_rowgemm", "k_lz_step_finish"]
+KEEP = ["k_lanczos_tma", "k_lanczos_cl", "k_lanczos", "k_spmv_fused", "k_spmm16x2", "k_spmm_g", "k_gram_bulk", "k_kron_apply",
+        "k_compressed_mma", "k_compressed_mma_pipe", "k_ipm", "chol_p16", "warp_chol_core", "k_image_diag", "k_image_entries",
+        "k_rowgemm", "k_rowgemm_rt", "k_lz_step_finish"]
 
 
 def main():
