@@ -1,5 +1,8 @@
 """A/B of the TMA Lanczos switches on one config: SpMV tail pool share
-(USBS_LZG_TAIL) and column sums from shared memory (USBS_LZG_OPT=1)."""
+(USBS_LZG_TAIL) and USBS_LZG_OPT bits (1: column sums from shared memory).
+Measured and dropped this round: a shared-memory copy of x's 8192 leading
+(highest-degree) entries in the free slots during the SpMV -- 8.71 vs
+8.65 ms per C4 call (the hub lines already hit L1)."""
 import ctypes as C
 import os
 import sys
@@ -18,8 +21,8 @@ rt = R.runtime()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=rt.device)
 y = np.random.default_rng(1234).standard_normal(p.m) * 1e-3
 buf = (C.c_ulonglong * 1024)()
-for tail in ("0", "0.12", "0.25"):
-    for opt in ("0", "1"):
+for tail in sys.argv[2].split(",") if len(sys.argv) > 2 else ("0",):
+    for opt in sys.argv[3].split(",") if len(sys.argv) > 3 else ("0", "1"):
         os.environ["USBS_LZG_TAIL"], os.environ["USBS_LZG_OPT"] = tail, opt
         os.environ.pop("USBS_LZ_PROF", None)
         dp = R.DeviceProblem(p, rt)  # fresh plan for the tail share
