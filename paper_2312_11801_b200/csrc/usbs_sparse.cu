@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(256) k_spmm16x2(int n_items, const int* __rest
 // where s is the row start's 8-byte parity.  Products accumulate per parity
 // (even: ae0/ae1, odd: ao0/ao1); column 2c = ae0 + ao1 of lane c and column
 // 2c+1 = ae1 of lane c + ao0 of lane c+1, each parity summed in CSR order.
-// Any ldv and base alignment; vend = elements of V that may be read.
+// Any ldv; V's base 16-byte aligned (the launcher checks), so no window
+// starts before V's first entry; vend = elements of V that may be read.
 template <int G>
 __global__ void __launch_bounds__(256) k_spmm_g(int n_items, const int* __restrict__ it_row,
                                                 const int* __restrict__ it_beg, const int* __restrict__ it_end,
@@ -1032,7 +1033,8 @@ k_spmv_fused<1024, 256, 6><<<(unsigned)nb, 256, 0, ctx->stream>>>(
       check_launch(ctx);
     }
     return;
-  } else if (k <= 15 && p->nnz <= 16 * p->n && !getenv("USBS_SPMM_16X2")) {
+  } else if (k <= 15 && p->nnz <= 16 * p->n && ((uintptr_t)V & 15) == 0 && !getenv("USBS_SPMM_16X2")) {
+    // (a 16-byte-aligned base: no row's window starts before V's first entry)
     // short rows (C4: 9 per row): grouped 16-byte-gather kernel, several rows
     // per warp; long rows (C5: 41) keep the half-warp kernel, which is faster
     // there (profiles/spmm_ab.py; A/B: USBS_SPMM_16X2=1)

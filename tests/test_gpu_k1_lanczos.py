@@ -84,10 +84,11 @@ def test_op_apply_matches_oracle(name, k):
 @pytest.mark.parametrize("name", ["C4s", "C5s", "mixed40"])
 def test_spmm_grouped_gather_any_k_and_view(name, monkeypatch):
     """K1 for 2 <= k <= 15 (grouped 16-byte gathers, usbs_sparse.cu k_spmm_g):
-    every group width (k = 2 .. 15), V a contiguous tensor and an offset,
-    strided column view (row starts alternate 8-byte parity, ld = k + 3),
-    within the dot-product bound and equal to the half-warp kernel up to
-    summation order."""
+    every group width (k = 2 .. 15), V a contiguous tensor, a strided view
+    with an odd row stride (row starts alternate 8-byte parity) and an
+    offset view (8-byte base: the launcher falls back to the half-warp
+    kernel), within the dot-product bound and equal to the half-warp kernel
+    up to summation order."""
     eigen, runtime = dev()
     p = case_problem(name)
     rng = np.random.default_rng(77)
@@ -99,9 +100,13 @@ def test_spmm_grouped_gather_any_k_and_view(name, monkeypatch):
         v = rng.standard_normal((p.n, k))
         want = p.cost @ v
         big = rt.upload(np.zeros((p.n, k + 3)))
-        view = big[:, 1:k + 1]
+        view = big[:, 1:k + 1]  # 8-byte base offset: the launcher takes the half-warp kernel
         view.copy_(rt.upload(v))
-        for V in (rt.upload(v), view):
+        ldo = k + 2 if k % 2 else k + 3  # odd row stride: row starts alternate 8-byte parity
+        big2 = rt.upload(np.zeros((p.n, ldo)))
+        view2 = big2[:, :k]
+        view2.copy_(rt.upload(v))
+        for V in (rt.upload(v), view, view2):
             monkeypatch.delenv("USBS_SPMM_16X2", raising=False)
             got = rt.download(dp.apply(0, V))
             bound_check(got, want, c_abs, np.abs(v), rownnz)
