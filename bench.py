@@ -544,7 +544,7 @@ def operator_apply(rt, dp, cfg_b, flush):
     cs, _ = dp.lanczos_plan(m)
     out["lanczos_top"] = {"ms": ms, "matvecs": r.matvecs, "restarts": r.restarts, "algorithmic_bytes": b,
                           "achieved_gbs": b / (ms / 1e3) / 1e9, "frac_of_measured_peak": b / (ms / 1e3) / 1e9 / peak,
-                          "kernel": "k_lanczos_cl (cluster)" if cs else "k_lanczos (grid)"}
+                          "kernel": "k_lanczos_cl (cluster)" if cs else "k_lanczos_tma (grid)"}
     eng = Engine(dp)
     d = k * (k + 1) // 2
     vq, _ = np.linalg.qr(np.random.default_rng(1234).standard_normal((p.n, k)))
@@ -559,7 +559,7 @@ def operator_apply(rt, dp, cfg_b, flush):
     out["k4_compressed_gram"] = {"ms": ms, "m": p.m, "d": d, "flop": flop, "achieved_tflops": flop / (ms / 1e3) / 1e12,
                                  "peak_tflops": fp64, "peak_source": "measured FP64 DMMA (profiles/fp64_peak.json)",
                                  "frac": (flop / (ms / 1e3) / 1e12 / fp64) if fp64 else None,
-                                 "kernel": "k_compressed_mma (mma.sync m8n8k4 f64)"}
+                                 "kernel": "k_compressed_mma_pipe (mma.sync m8n8k4 f64, pipelined row generation)"}
     return out
 
 
