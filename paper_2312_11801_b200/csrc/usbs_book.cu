@@ -104,6 +104,101 @@ __global__ void __launch_bounds__(256) k_image_entries(int64_t m, const int* __r
   }
 }
 
+// k_image_entries for problems whose constraints mostly have ONE entry
+// (C3: 99%, C5: all): the entry comes from the flattened (row, col, value)
+// arrays (one load level instead of cptr -> cent -> entry), and four lanes
+// share a constraint's k-long dot product (lane t takes columns t, t + 4,
+// ...; one row read by the four lanes is one contiguous range), two shuffle
+// steps to combine, eight constraints per warp.  Constraints with a few
+// entries (rc.x == -1) are summed by the group's lanes from the entry list;
+// the ones with more than IMAGE_HEAVY entries (C3: one 400-entry row sum,
+// which alone set the kernel's duration when four lanes walked it) are
+// listed in heavy[1 .. heavy[0]] and each is summed by a whole block first:
+// 64 lane groups over its entries, a fixed shuffle + shared-memory tree.
+// Sum orders differ from k_image_entries (rounding level only).
+constexpr int IMAGE_HEAVY = 32;
+
+__global__ void __launch_bounds__(256) k_image_c1(int64_t m, const int2* __restrict__ c1rc,
+                                                  const double* __restrict__ c1v, const int* __restrict__ heavy,
+                                                  const int* __restrict__ cptr,
+                                                  const int* __restrict__ cent, const int* __restrict__ erow,
+                                                  const int* __restrict__ ecol, const double* __restrict__ eval,
+                                                  const double* __restrict__ V, int64_t ldv,
+                                                  const double* __restrict__ W, int64_t ldw, int k,
+                                                  const double* __restrict__ S, int sdiag, double sscale,
+                                                  const double* beta_dev, double beta,
+                                                  const double* __restrict__ base, double* __restrict__ out) {
+  __shared__ double Sd[64];
+  __shared__ double red[8];
+  if (sdiag)
+    for (int x = threadIdx.x; x < k; x += blockDim.x) Sd[x] = sscale * S[x];
+  if (beta_dev) beta *= beta_dev[0];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, gq = lane >> 2, t = lane & 3;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // columns j0, j0 + js, ... of the entry's k-long dot
+  auto pair = [&](int r, int c, int j0, int js) -> double {
+    double v = 0.0;
+    if (sdiag) {
+      const double* vr = V + (int64_t)r * ldv;
+      const double* vc = V + (int64_t)c * ldv;
+      for (int j = j0; j < k; j += js) v = fma(vr[j] * Sd[j], vc[j], v);
+    } else {
+      const double* wr = W + (int64_t)r * ldw;
+      const double* vc = V + (int64_t)c * ldv;
+      for (int j = j0; j < k; j += js) v = fma(wr[j], vc[j], v);
+    }
+    return v;
+  };
+  const int nh = heavy ? heavy[0] : 0;
+  for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+    const int i = heavy[1 + h];
+    double acc = 0.0;
+    for (int q = cptr[i] + (threadIdx.x >> 2); q < cptr[i + 1]; q += blockDim.x >> 2) {
+      const int e = cent[q];
+      const int r = erow[e], c = ecol[e];
+      acc = fma(pair(r, c, t, 4), (r == c) ? eval[e] : 2.0 * eval[e], acc);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      out[i] = (base ? beta * base[i] : 0.0) + s;
+    }
+    __syncthreads();
+  }
+  for (int64_t wb = wid * 8; wb < m; wb += nwarps * 8) {
+    const int64_t i = wb + gq;
+    double acc = 0.0;
+    bool own = i < m;
+    if (own) {
+      const int2 rc = __ldg(c1rc + i);
+      if (rc.x >= 0) {  // one entry: the four lanes split its dot
+        const double val = __ldg(c1v + i);
+        acc = pair(rc.x, rc.y, t, 4) * ((rc.x == rc.y) ? val : 2.0 * val);
+      } else {  // several: the lanes split the entries, a whole dot each
+        const int q0 = cptr[i], q1 = cptr[i + 1];
+        if (heavy && q1 - q0 > IMAGE_HEAVY) {
+          own = false;  // a block summed it
+        } else {
+          for (int q = q0 + t; q < q1; q += 4) {
+            const int e = cent[q];
+            const int r = erow[e], c = ecol[e];
+            acc = fma(pair(r, c, 0, 1), (r == c) ? eval[e] : 2.0 * eval[e], acc);
+          }
+        }
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1, 4);
+    if (own && t == 0) out[i] = (base ? beta * base[i] : 0.0) + acc;
+  }
+}
+
 // -------------------------------------------------- K4 / K4w compressed rows
 // Row i of the (never stored) compressed matrix: c_i[p] = svec(V^T A_i V)[p].
 // Tiles of TR constraints are generated into smem; each thread accumulates
@@ -448,9 +543,11 @@ __global__ void __launch_bounds__(512, 1) k_compressed_mma(int64_t m, int diag_o
 // else (-1, -1) and the row is generated from the entry list.
 __global__ void k_c1_flatten(int64_t m, const int* __restrict__ cptr, const int* __restrict__ cent,
                              const int* __restrict__ erow, const int* __restrict__ ecol,
-                             const double* __restrict__ eval, int2* __restrict__ rc, double* __restrict__ cv) {
+                             const double* __restrict__ eval, int2* __restrict__ rc, double* __restrict__ cv,
+                             int* __restrict__ heavy) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     const int t0 = cptr[i], t1 = cptr[i + 1];
+    if (heavy && t1 - t0 > IMAGE_HEAVY) heavy[1 + atomicAdd(heavy, 1)] = (int)i;
     if (t1 - t0 == 1) {
       const int e = cent[t0];
       rc[i] = make_int2(erow[e], ecol[e]);
@@ -1164,6 +1261,20 @@ static int nblocks(usbs_ctx* ctx, int64_t work, int per = 256, int mult = 8) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work + per - 1) / per, (int64_t)mult * ctx->num_sms));
 }
 
+// the flattened single-entry view of the constraint list (lazy, once)
+static void ensure_c1(usbs_ctx* ctx, usbs_problem* p) {
+  if (p->c1_rc) return;
+  p->c1_rc = dev_alloc<int2>(p, (size_t)p->m);
+  p->c1_val = dev_alloc<double>(p, (size_t)p->m);
+  if (p->max_entries_per_cons > IMAGE_HEAVY) {
+    p->c1_heavy = dev_alloc<int>(p, (size_t)p->m + 1);
+    USBS_CUDA(cudaMemsetAsync(p->c1_heavy, 0, sizeof(int), ctx->stream));
+  }
+  k_c1_flatten<<<nblocks(ctx, p->m), 256, 0, ctx->stream>>>(p->m, p->cptr, p->cent, p->e_row, p->e_col, p->e_val,
+                                                            p->c1_rc, p->c1_val, p->c1_heavy);
+  check_launch(ctx);
+}
+
 extern "C" {
 
 usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* V, int64_t ldv, int k, const double* S,
@@ -1187,9 +1298,17 @@ usbs_status usbs_cons_image(usbs_ctx* ctx, usbs_problem* p, const double* V, int
       check_launch(ctx);
       W = Wb;
     }
-    k_image_entries<<<nblocks(ctx, (p->m + 3) / 4 * 32), 256, 0, ctx->stream>>>(
-        p->m, p->cptr, p->cent, p->e_row, p->e_col, p->e_val, V, ldv, W, k, k, S, s_is_diag, s_scale, beta_dev,
-        beta, base, out);
+    const char* ev1 = getenv("USBS_IMAGE_V1");
+    if (!(ev1 && ev1[0] == '1')) {  // A/B: USBS_IMAGE_V1=1 -> eight lanes over each constraint's entry list
+      ensure_c1(ctx, p);
+      k_image_c1<<<nblocks(ctx, (p->m + 7) / 8 * 32), 256, 0, ctx->stream>>>(
+          p->m, p->c1_rc, p->c1_val, p->c1_heavy, p->cptr, p->cent, p->e_row, p->e_col, p->e_val, V, ldv, W, k, k, S, s_is_diag,
+          s_scale, beta_dev, beta, base, out);
+    } else {
+      k_image_entries<<<nblocks(ctx, (p->m + 3) / 4 * 32), 256, 0, ctx->stream>>>(
+          p->m, p->cptr, p->cent, p->e_row, p->e_col, p->e_val, V, ldv, W, k, k, S, s_is_diag, s_scale, beta_dev,
+          beta, base, out);
+    }
   }
   check_launch(ctx);
   USBS_API_END
@@ -1273,13 +1392,7 @@ usbs_status usbs_cons_compressed(usbs_ctx* ctx, usbs_problem* p, const double* V
     const char* ev1 = getenv("USBS_K4_V1");
     if (!a_vec && !w_vec && !(ev1 && ev1[0] == '1')) {
       // pipelined row generation (A/B: USBS_K4_V1=1)
-      if (!p->diag_only && !p->c1_rc) {
-        p->c1_rc = dev_alloc<int2>(p, (size_t)p->m);
-        p->c1_val = dev_alloc<double>(p, (size_t)p->m);
-        k_c1_flatten<<<nblocks(ctx, p->m), 256, 0, ctx->stream>>>(p->m, p->cptr, p->cent, p->e_row, p->e_col,
-                                                                  p->e_val, p->c1_rc, p->c1_val);
-        check_launch(ctx);
-      }
+      if (!p->diag_only) ensure_c1(ctx, p);
       const size_t smp = (size_t)(2 * CTR * (d + 1 + ((8 - (d + 1)) & 15))) * sizeof(double) + 1200 + 16;
       const int n16 = (d + 15) / 16, nb16 = n16 * (n16 + 1) / 2;
 #define USBS_COMP_PIPE(T, HY)                                                                              \

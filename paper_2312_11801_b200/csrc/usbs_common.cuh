@@ -88,6 +88,7 @@ struct usbs_problem {
   int* cptr = nullptr;  // m + 1
   int2* c1_rc = nullptr;      // per constraint: (row, col) of its single entry, (-1, -1) if it has several
   double* c1_val = nullptr;   // that entry's value (lazy, first compressed-Gram call)
+  int* c1_heavy = nullptr;    // [0] = count h, [1 .. h] = constraints with > IMAGE_HEAVY entries (any order)
   int* cent = nullptr;  // ne
   int max_entries_per_cons = 0;
   // flat constraint entries (device copies)
