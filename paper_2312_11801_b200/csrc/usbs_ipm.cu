@@ -96,6 +96,17 @@ __device__ double blk_max_abs(const double* x, int n, double* red) {
 
 __device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, double b, double c0, double c1);
 
+// A pointer known to lie in the kernel's dynamic shared memory, rebuilt from
+// the shared window so the compiler addresses it with LDS / STS (a pointer
+// that crossed a noinline call or a run-time select is generic: 64-bit
+// address arithmetic and LD.E / ST.E on every access).
+__device__ __forceinline__ double* as_shared(double* p) {
+  extern __shared__ __align__(16) unsigned char usbs_ipm_dyn_smem[];
+  const unsigned off = (unsigned)__cvta_generic_to_shared(p) - (unsigned)__cvta_generic_to_shared(usbs_ipm_dyn_smem);
+  return (double*)(usbs_ipm_dyn_smem + off);
+}
+
+
 // One warp factors W (lower, row-major k x k, k <= 32) in place, blocked by
 // 8: the 8 x 8 diagonal block in registers (lanes 0-7 hold its rows; per
 // column the pivot's rsqrt, the column scaled, the trailing entries of the
@@ -107,7 +118,8 @@ __device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, doub
 // microbenchmark, profiles/mb/chol_mb.cu: k = 20 12.1k -> 8.4k cycles).
 // Fails on a pivot <= 0 or NaN (potrf); returns ok.  Own register
 // allocation (noinline) so the callers' live state does not spill it.
-__device__ __noinline__ int warp_chol_core(double* W, int k, const unsigned short* /*ctab*/) {
+__device__ __noinline__ int warp_chol_core(double* Wg, int k, const unsigned short* /*ctab*/) {
+  double* W = as_shared(Wg);  // every caller passes a k x k block of the kernel's shared memory
   const int lane = threadIdx.x & 31, r = lane & 7, g = lane >> 2, q = lane & 3;
   int ok = 1;
   for (int j0 = 0; j0 < k; j0 += 8) {
@@ -532,7 +544,10 @@ __device__ void chol_diag16_warp(double* __restrict__ Mp, int N, int j0, double*
 // warps run the rest of the trailing update.  Two barriers per panel.
 // rdiag[j] = 1 / L_jj.  Returns 0 on failure (uniform).  Own register
 // allocation (noinline).
-__device__ __noinline__ int chol_p16(double* __restrict__ Mp, int N, double* __restrict__ rdiag, int* flag) {
+template <bool MSM>
+__device__ __noinline__ int chol_p16(double* __restrict__ Mg, int N, double* __restrict__ rdiag_g, int* flag) {
+  double* __restrict__ Mp = MSM ? as_shared(Mg) : Mg;
+  double* __restrict__ rdiag = as_shared(rdiag_g);
   const int tid = threadIdx.x, warp = tid >> 5, nwp = blockDim.x >> 5, nth = blockDim.x;
   const int T = (N + 7) >> 3;
   if (warp == 0) chol_diag16_warp(Mp, N, 0, rdiag, flag);
@@ -577,14 +592,14 @@ __device__ __noinline__ int chol_p16(double* __restrict__ Mp, int N, double* __r
 // 8-column form otherwise (d = 66: 15.3 vs 18.8 us).  Two instantiations so
 // each kernel carries one factorisation (code size and register allocation
 // of the kernel otherwise cost the gain).
-template <bool P16>
+template <bool P16, bool MSM>
 __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int k = a.k, d = a.d, kk = k * k, tid = threadIdx.x, nth = blockDim.x;
   const int has_eta = a.has_eta;
   IpmSmem sm;
   double* base = (double*)smem_raw;
-  const bool m_in_smem = d <= SMEM_D;
+  constexpr bool m_in_smem = MSM;  // d <= SMEM_D (launch_ipm)
   // P16: M first (16-byte aligned for the bulk copy of packed Q11 into it)
   const int mfirst = (P16 && m_in_smem) ? (((d + 1) * (d + 2) / 2 + 1) & ~1) : 0;
   sm.S = base + mfirst; sm.T = sm.S + kk; sm.H = sm.T + kk; sm.dS = sm.H + kk; sm.dT = sm.dS + kk;
@@ -596,7 +611,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   sm.red = sm.cb1 + d; sm.sc = sm.red + 32;
   sm.bar = (uint64_t*)(sm.sc + 64);  // P16 only (the 8-column kernel keeps M right after sc)
   sm.M = (P16 && m_in_smem) ? base : sm.sc + 64;
-  double* Mp = m_in_smem ? sm.M : a.gM;
+  double* Mp;
+  if constexpr (MSM) Mp = sm.M; else Mp = a.gM;
   unsigned char* ub = (unsigned char*)(sm.sc + (P16 ? 66 : 64) + ((m_in_smem && !P16) ? (d + 1) * (d + 2) / 2 : 0));
   sm.pi = ub; sm.pj = ub + 600;
   sm.flg = (int*)(ub + 1200);
@@ -825,7 +841,16 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
           r = sm.g[p] * ((rc + kappa1 * (f2 - re)) / cden) + sm.vI[p] * ((f2 - re - kappa2 * rc) / cden) -
               sm.f1[p] + sm.rd[p];
         sm.rhs[p] = r;
+        // the low-rank term's per-column factors, divided once per column
+        // instead of once per entry of M
+        if (!has_eta) {
+          sm.cb0[p] = sm.vI[p] / kappa1;
+        } else {
+          sm.cb0[p] = (kappa1 * sm.g[p] + sm.vI[p]) / cden;
+          sm.cb1[p] = (sm.g[p] - kappa2 * sm.vI[p]) / cden;
+        }
       }
+      __syncthreads();
       IPM_MARK(2);
       // M (packed lower): Q11 + E + low-rank; warp per row p, lanes over q <= p
       // (Q11 already in place when packed)
@@ -852,8 +877,8 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
                        Gm[i * k + kq] * Hm[l * k + j] + Gm[i * k + l] * Hm[kq * k + j];
             e *= (wp * wq) * 0.25;
             double v = qv + e;
-            if (!has_eta) v += vp * sm.vI[q] / kappa1;
-            else v -= (gp * (kappa1 * sm.g[q] + sm.vI[q]) + vp * (sm.g[q] - kappa2 * sm.vI[q])) / cden;
+            if (!has_eta) v = fma(vp, sm.cb0[q], v);
+            else v -= gp * sm.cb0[q] + vp * sm.cb1[q];
             Mp[base + q] = v;
           }
         }
@@ -871,7 +896,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
       // rdiag keeps 1 / L_jj for the solves (f1 is dead once rhs is formed)
       double* rdiag = sm.f1;
       int chol_ok;
-      if constexpr (P16) chol_ok = chol_p16(Mp, d + 1, rdiag, &sm.flg[5]);
+      if constexpr (P16) chol_ok = chol_p16<MSM>(Mp, d + 1, rdiag, &sm.flg[5]);
       else chol_ok = chol_tiled(Mp, d + 1, rdiag, &sm.flg[5]);
       if (!chol_ok) fail = 1;
       IPM_MARK(4);
@@ -879,6 +904,11 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
         const int lane = tid & 31;
         for (int q = tid; q < d; q += nth) sm.rhs[q] = Mp[pidx(d, q)];
         __syncthreads();
+        {
+        // generic pointer on purpose in the 16-panel kernel (measured at d = 210:
+        // this solve 18.2 us with LD.E, 24.4 us with LDS; d = 66: 6.4 vs 7.3 us the other way)
+        double* Mb = Mp;
+        if constexpr (P16) asm volatile("" : "+l"(Mb));
         // blocked backward solve: the 32-row diagonal triangles by warp 0
         // with shuffles, the off-diagonal updates by the whole block
         for (int Jend = d; Jend > 0; Jend -= 32) {  // backward: L^T x = y
@@ -888,7 +918,7 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
             const double rdl = lane < JB ? rdiag[J + lane] : 0.0;
             double Lc[32];
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) Lc[jj] = (lane < jj && jj < JB) ? Mp[pidx(J + jj, J + lane)] : 0.0;
+            for (int jj = 0; jj < 32; ++jj) Lc[jj] = (lane < jj && jj < JB) ? Mb[pidx(J + jj, J + lane)] : 0.0;
 #pragma unroll
             for (int jj = 31; jj >= 0; --jj) {
               if (jj < JB) {
@@ -904,15 +934,16 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
             int jj = 0;
             for (; jj + 3 < JB; jj += 4) {
-              s0 = fma(Mp[pidx(J + jj, i)], sm.ds[J + jj], s0);
-              s1 = fma(Mp[pidx(J + jj + 1, i)], sm.ds[J + jj + 1], s1);
-              s2 = fma(Mp[pidx(J + jj + 2, i)], sm.ds[J + jj + 2], s2);
-              s3 = fma(Mp[pidx(J + jj + 3, i)], sm.ds[J + jj + 3], s3);
+              s0 = fma(Mb[pidx(J + jj, i)], sm.ds[J + jj], s0);
+              s1 = fma(Mb[pidx(J + jj + 1, i)], sm.ds[J + jj + 1], s1);
+              s2 = fma(Mb[pidx(J + jj + 2, i)], sm.ds[J + jj + 2], s2);
+              s3 = fma(Mb[pidx(J + jj + 3, i)], sm.ds[J + jj + 3], s3);
             }
-            for (; jj < JB; ++jj) s0 = fma(Mp[pidx(J + jj, i)], sm.ds[J + jj], s0);
+            for (; jj < JB; ++jj) s0 = fma(Mb[pidx(J + jj, i)], sm.ds[J + jj], s0);
             sm.rhs[i] -= (s0 + s1) + (s2 + s3);
           }
           __syncthreads();
+        }
         }
         issue_q();  // M is dead: the next step's Q11 copy overlaps the rest of this step
         IPM_MARK(5);
@@ -1079,12 +1110,15 @@ size_t ipm_smem_bytes(int k) {
 void launch_ipm(usbs_ctx* ctx, const IpmArgs& a) {
   size_t sm = ipm_smem_bytes(a.k);
   IpmArgs b = a;
-  if (a.d + 1 >= 100) {
-    smem_optin(ctx, (const void*)k_ipm<true>, 227 * 1024);
-    k_ipm<true><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+  if (a.d + 1 >= 100 && a.d <= SMEM_D) {
+    smem_optin(ctx, (const void*)k_ipm<true, true>, 227 * 1024);
+    k_ipm<true, true><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+  } else if (a.d + 1 >= 100) {
+    smem_optin(ctx, (const void*)k_ipm<true, false>, 227 * 1024);
+    k_ipm<true, false><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
   } else {
-    smem_optin(ctx, (const void*)k_ipm<false>, 227 * 1024);
-    k_ipm<false><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
+    smem_optin(ctx, (const void*)k_ipm<false, true>, 227 * 1024);
+    k_ipm<false, true><<<1, IPM_THREADS, sm, ctx->stream>>>(b);
   }
   check_launch(ctx);
 }
