@@ -62,6 +62,11 @@ struct IpmArgs {
 // state layout: S (k*k), T (k*k), eta, zeta, omega, mu, has_eta, k, valid
 __host__ __device__ inline int state_len(int k) { return 2 * k * k + 7; }
 
+#ifdef USBS_CHOL_PROF
+constexpr int IPM_PROF_SLOTS = 128;
+#else
+constexpr int IPM_PROF_SLOTS = 16;
+#endif
 constexpr int IPM_THREADS = 512;
 constexpr int SMEM_D = 210;
 constexpr int KMAX = 32;
@@ -539,11 +544,19 @@ __device__ void chol_diag16_warp(double* __restrict__ Mp, int N, int j0, double*
 // without block barriers, all threads solve the panel rows (x L_JJ^T = v, a
 // thread per row, right-looking inside the row: the substitution's
 // operations in its order), the trailing update is 16 deep (four m8n8k4
-// per tile, groups of four tiles per warp); warp 0 looks ahead: it updates
+// per tile, groups of four tiles dealt round-robin over the warps); warp 0 looks ahead: it updates
 // the next diagonal block's tiles first and factors it while the other
 // warps run the rest of the trailing update.  Two barriers per panel.
 // rdiag[j] = 1 / L_jj.  Returns 0 on failure (uniform).  Own register
 // allocation (noinline).
+#ifdef USBS_CHOL_PROF
+__device__ unsigned long long* g_cholprof = nullptr;
+#define CP_T(v) const long long v = clock64()
+#define CP_ADD(slot, dt) do { if (g_cholprof) atomicAdd(&g_cholprof[10 + slot], (unsigned long long)(dt)); } while (0)
+#else
+#define CP_T(v)
+#define CP_ADD(slot, dt)
+#endif
 template <bool MSM>
 __device__ __noinline__ int chol_p16(double* __restrict__ Mg, int N, double* __restrict__ rdiag_g, int* flag) {
   double* __restrict__ Mp = MSM ? as_shared(Mg) : Mg;
@@ -556,6 +569,7 @@ __device__ __noinline__ int chol_p16(double* __restrict__ Mg, int N, double* __r
   for (int j0 = 0; j0 < N; j0 += 16) {
     const int JB = min(16, N - j0), r0 = j0 + JB;
     if (r0 >= N) break;  // JB == 16 from here on
+    CP_T(t0);
     for (int i = r0 + tid; i < N; i += nth) {
       double* ri = Mp + pidx(i, j0);
       double v[16];
@@ -570,7 +584,9 @@ __device__ __noinline__ int chol_p16(double* __restrict__ Mg, int N, double* __r
 #pragma unroll
       for (int c = 0; c < 16; ++c) ri[c] = v[c];
     }
+    CP_T(t1);
     __syncthreads();
+    CP_T(t2);
     const int a = r0 >> 3;  // first trailing tile row
     if (warp == 0) {
       tiles_update<16, 1>(Mp, N, j0, a, a, 1);
@@ -578,10 +594,31 @@ __device__ __noinline__ int chol_p16(double* __restrict__ Mg, int N, double* __r
       __syncwarp();
       chol_diag16_warp(Mp, N, r0, rdiag, flag);
     } else {
-      for (int I = T - warp; I >= a + 2; I -= nwp - 1)
-        for (int K0 = a; K0 <= I; K0 += 4) tiles_update<16, 4>(Mp, N, j0, I, K0, min(4, I - K0 + 1));
+      // groups of four tiles (I, K0) dealt round-robin over the 15 warps in
+      // row order from the longest row: every warp within one group of the
+      // mean (whole tile rows per warp left warp 1 with 35 of 325 tiles at
+      // the first panel, 1.6x the mean)
+      int I = T - 1, first = 0;
+      for (int idx = warp - 1;; idx += nwp - 1) {
+        while (I >= a + 2 && idx >= first + ((I - a + 4) >> 2)) {
+          first += (I - a + 4) >> 2;
+          --I;
+        }
+        if (I < a + 2) break;
+        const int K0 = a + 4 * (idx - first);
+        tiles_update<16, 4>(Mp, N, j0, I, K0, min(4, I - K0 + 1));
+      }
     }
+    CP_T(t3);
     __syncthreads();
+    CP_T(t4);
+#ifdef USBS_CHOL_PROF
+    { const int pn = j0 >> 4;
+    if (tid == 0) { CP_ADD(6 + pn, t1 - t0); CP_ADD(6 + 16 + pn, t3 - t2); }
+    if (tid == 32) { CP_ADD(6 + 32 + pn, t3 - t2); }
+    if (tid == 256) { CP_ADD(6 + 48 + pn, t3 - t2); }
+    if (tid == 480) { CP_ADD(6 + 64 + pn, t3 - t2); } }
+#endif
     if (!*flag) return 0;
   }
   return 1;
@@ -754,6 +791,10 @@ __global__ void __launch_bounds__(IPM_THREADS, 1) k_ipm(IpmArgs a) {
   unsigned long long ipm_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long ipm_last = 0;
   if (a.prof && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ipm_last));
+#ifdef USBS_CHOL_PROF
+  if (tid == 0) g_cholprof = a.prof;
+  __syncthreads();
+#endif
   const double SQ2 = 1.4142135623730951;
   for (it = 1; it <= a.o.max_newton; ++it) {
     issue_q();  // M is dead here
@@ -1150,9 +1191,9 @@ extern "C" usbs_status usbs_ipm_solve(usbs_ctx* ctx, int k, int has_eta, const d
   a.prof = nullptr;
   if (getenv("USBS_IPM_PROF")) {
     static bool zeroed = false;
-    a.prof = (unsigned long long*)ctx->ws.get(WS_IPM + 1, 16 * sizeof(unsigned long long));
+    a.prof = (unsigned long long*)ctx->ws.get(WS_IPM + 1, IPM_PROF_SLOTS * sizeof(unsigned long long));
     if (!zeroed) {
-      USBS_CUDA(cudaMemsetAsync(a.prof, 0, 16 * sizeof(unsigned long long), ctx->stream));
+      USBS_CUDA(cudaMemsetAsync(a.prof, 0, IPM_PROF_SLOTS * sizeof(unsigned long long), ctx->stream));
       zeroed = true;
     }
   }
@@ -1172,9 +1213,13 @@ extern "C" int usbs_ipm_state_len(int k) { return state_len(k); }
 // Phase timers of k_ipm (ns) accumulated while USBS_IPM_PROF is set.
 extern "C" usbs_status usbs_ipm_profile(usbs_ctx* ctx, unsigned long long* out, int reset) {
   USBS_API_BEGIN
-  auto* p = (unsigned long long*)ctx->ws.get(WS_IPM + 1, 16 * sizeof(unsigned long long));
+  auto* p = (unsigned long long*)ctx->ws.get(WS_IPM + 1, IPM_PROF_SLOTS * sizeof(unsigned long long));
+#ifdef USBS_CHOL_PROF
+  USBS_CUDA(cudaMemcpyAsync(out, p, IPM_PROF_SLOTS * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+#else
   USBS_CUDA(cudaMemcpyAsync(out, p, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+#endif
   USBS_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, 16 * sizeof(unsigned long long), ctx->stream));
+  if (reset) USBS_CUDA(cudaMemsetAsync(p, 0, IPM_PROF_SLOTS * sizeof(unsigned long long), ctx->stream));
   USBS_API_END
 }
