@@ -511,11 +511,17 @@ __device__ __forceinline__ void tiles_update(double* __restrict__ Mp, int N, int
 // The 16 x 16 diagonal block at j0 by warp 0 alone (no block barrier):
 // diag8, the 8 rows below it by substitution (a lane per row), their 8 x 8
 // tile update on the tensor cores, diag8.  Sets *flag (potrf semantics).
-__device__ void chol_diag16_warp(double* __restrict__ Mp, int N, int j0, double* __restrict__ rdiag, int* flag) {
+// wait_peer: the tiles of the block's second tile row come from warp 1
+// (named barrier 1, 64 threads: warp 1 arrives when they are stored), so
+// their 16-deep update runs beside the first 8 x 8 block instead of ahead of
+// it on this warp's chain.
+__device__ void chol_diag16_warp(double* __restrict__ Mp, int N, int j0, double* __restrict__ rdiag, int* flag,
+                                 bool wait_peer = false) {
   const int lane = threadIdx.x & 31;
   const int JB = min(16, N - j0);
   chol_diag8(Mp, N, j0 >> 3, rdiag, flag);
   __syncwarp();
+  if (wait_peer) asm volatile("bar.sync 1, 64;" ::: "memory");  // always taken when set: the arrival count stays paired
   if (JB <= 8 || !*(volatile int*)flag) return;
   const int i = j0 + 8 + lane;
   if (lane < JB - 8) {
@@ -546,7 +552,9 @@ __device__ void chol_diag16_warp(double* __restrict__ Mp, int N, int j0, double*
 // operations in its order), the trailing update is 16 deep (four m8n8k4
 // per tile, groups of four tiles dealt round-robin over the warps); warp 0 looks ahead: it updates
 // the next diagonal block's tiles first and factors it while the other
-// warps run the rest of the trailing update.  Two barriers per panel.
+// warps run the rest of the trailing update (warp 1 first updates the next
+// diagonal block's second tile row and hands it over through a named
+// barrier).  Two block barriers per panel.
 // rdiag[j] = 1 / L_jj.  Returns 0 on failure (uniform).  Own register
 // allocation (noinline).
 #ifdef USBS_CHOL_PROF
@@ -590,10 +598,15 @@ __device__ __noinline__ int chol_p16(double* __restrict__ Mg, int N, double* __r
     const int a = r0 >> 3;  // first trailing tile row
     if (warp == 0) {
       tiles_update<16, 1>(Mp, N, j0, a, a, 1);
-      if (a + 1 < T) tiles_update<16, 2>(Mp, N, j0, a + 1, a, 2);
       __syncwarp();
-      chol_diag16_warp(Mp, N, r0, rdiag, flag);
+      chol_diag16_warp(Mp, N, r0, rdiag, flag, a + 1 < T);
     } else {
+      if (warp == 1 && a + 1 < T) {
+        // the next diagonal block's second tile row, handed to warp 0
+        tiles_update<16, 2>(Mp, N, j0, a + 1, a, 2);
+        __threadfence_block();
+        asm volatile("bar.arrive 1, 64;" ::: "memory");
+      }
       // groups of four tiles (I, K0) dealt round-robin over the 15 warps in
       // row order from the longest row: every warp within one group of the
       // mean (whole tile rows per warp left warp 1 with 35 of 325 tiles at
