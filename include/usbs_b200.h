@@ -277,6 +277,21 @@ usbs_status usbs_gather(usbs_ctx* ctx, int64_t n, const int64_t* idx_dev, const 
 usbs_status usbs_gather_rows(usbs_ctx* ctx, int64_t n, int k, const int64_t* idx_dev, const double* src_dev,
                              int64_t lds, double* dst_dev, int64_t ldd);
 
+/* ---- device-controlled loop (alternating_max, subqp.py:552-614) -------------
+ * Everything the context launches between usbs_loop_begin and usbs_loop_end is
+ * captured as the body of a CUDA-graph WHILE node instead of being run; a
+ * one-thread kernel closing the body does counter[0] += 1 and continues while
+ * sqrt(max(red[0], 0)) > thresh and counter[0] < max_iters -- the reference's
+ * "until ||nu' - nu|| <= tol (1 + ||b||) or max_passes" evaluated on the device,
+ * so the passes run back to back with no host read.  usbs_loop_end launches the
+ * loop on the context's stream (the body runs at least once); the caller zeroes
+ * counter_dev first and reads it afterwards.  usbs_loop_abort drops a capture
+ * after a failed call inside the body. */
+usbs_status usbs_loop_begin(usbs_ctx* ctx);
+usbs_status usbs_loop_end(usbs_ctx* ctx, const double* red_dev, double thresh, int max_iters,
+                          int* counter_dev);
+usbs_status usbs_loop_abort(usbs_ctx* ctx);
+
 /* ---- rounding -------------------------------------- */
 /* make_test_matrix (sketch.py:25-27): rows [row0, row1) of
  * np.random.RandomState(seed & 0x7FFFFFFF).standard_normal((n, r)) into

@@ -54,6 +54,9 @@ PROTOS = {
     "usbs_lanczos_plan": (_i32, [_p, _p, _i32, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "usbs_ipm_solve": (_i32, [_p, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "usbs_ipm_state_len": (_i32, [_i32]),
+    "usbs_loop_begin": (_i32, [_p]),
+    "usbs_loop_end": (_i32, [_p, _p, C.c_double, _i32, _p]),
+    "usbs_loop_abort": (_i32, [_p]),
     "usbs_ipm_profile": (_i32, [_p, C.POINTER(C.c_uint64), _i32]),
     "usbs_cons_image": (_i32, [_p, _p, _p, _i64, _i32, _p, _i32, C.c_double, _p, C.c_double, _p, _p]),
     "usbs_cons_compressed": (_i32, [_p, _p, _p, _i64, _i32, C.c_double, _p, _p, C.c_double, _p, _p,

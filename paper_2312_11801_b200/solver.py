@@ -24,10 +24,16 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import _native as N
+from ._native import check
 from .eigen import DeviceLinOp, lanczos_top
 from .engine import Engine
 from .errors import EmptyBasisError
 from .runtime import DeviceProblem, runtime
+
+
+def _device_loop_enabled() -> bool:
+    """USBS_DEVICE_LOOP=0 keeps the host-driven alternating loop (A/B, debugging)."""
+    return os.environ.get("USBS_DEVICE_LOOP", "1") != "0"
 
 __all__ = ["LanczosSettings", "IpmOptions", "SolverConfig", "AggregateStats", "Residuals", "SolverState",
            "IterationInfo", "PrimalOutput", "DeviceSolver", "solve"]
@@ -540,6 +546,8 @@ class DeviceSolver:
         self.wv = rt.empty(m)
         self.nu_a = rt.empty(m)
         self.nu_b = rt.empty(m)
+        self.loop_cnt = None  # device int32: passes run by the device loop (lazy)
+        self.device_loop = _device_loop_enabled() and getattr(rt, "lib", None) is not None
         self.ax = rt.empty(m)
         self.ycand = rt.empty(m)
         d = k * (k + 1) // 2
@@ -701,9 +709,8 @@ class DeviceSolver:
             eng.dot_into(img[:1], img[:1], sc[S_Q22:S_Q22 + 1], scale=0.0)
         eng.apply(0, V, self.tmp_nk[:, :k], gram=self.cq)  # cost_quad = sym(V^T C V)
         eng.svec(self.cq, self.csv, scale=a)
-        warm = None
-        passes = 0
-        for passes in range(1, max_passes + 1):
+        def enqueue_pass(nu, nxt, warm):
+            """One pass of subqp.py:575-611 enqueued on the device."""
             eng.vec(N.VOP_W, self.m, x=y, y=nu, b=self.b, s0=rho, out=self.wv)
             eng.compressed(V, w=self.wv, scale_w=a, w_out=self.lin_s)
             eng.vec(N.VOP_AXPBY, self.d, x=self.lin_s, y=self.csv, s0=1.0, s1=-1.0, out=self.lin_s)
@@ -714,10 +721,26 @@ class DeviceSolver:
                 eng.dot_into(img[:1], img[:1], sc[S_LINETA:S_LINETA + 1], scale=0.0)
             eng.ipm(k, has_eta, self.Q11, self.q12 if has_eta else None, self.lin_s, sc[S_Q22:S_Q22 + 2], warm,
                     self.st_q, self.res_q, self.opts)
-            warm = self.st_q
             S = self.st_q[:k * k].view(k, k)
             eng.image(V, S, self.ax, s_scale=a, beta_dev=self.res_q[3:4] if has_eta else None,
                       beta=(a / tr) if has_eta else 0.0, base=img if has_eta else None)
+
+        def finish_pass(nu, nxt):
+            eng.vec(N.VOP_NUNEXT, self.m, x=self.ax, y=y, z=nu, b=self.b, ineq=self.ineq, s0=rho, out=nxt,
+                    red=sc[S_DNU:S_DNU + 2])
+
+        warm = None
+        passes = 0
+        thresh = tol * (1.0 + self.b_norm)
+        # after the first pass the remaining ones run as a device-controlled
+        # loop (CUDA-graph WHILE node, usbs_loop_*): no host read between
+        # passes; the host-driven loop stays for sharded solves (collectives
+        # between the kernels) and when psi is traced
+        device_loop = (self.device_loop and eng.comm is None and psi_trace is None and self.has_ineq
+                       and max_passes > 1)
+        for passes in range(1, max_passes + 1):
+            enqueue_pass(nu, None, warm)
+            warm = self.st_q
             nxt = self.nu_b if nu is self.nu_a else self.nu_a
             if psi_trace is not None:
                 from .subproblem import psi_value
@@ -725,15 +748,38 @@ class DeviceSolver:
                 eta_act = a * float(self.res_q[3].item()) / tr if has_eta else 0.0
                 c_x = eta_act * model.stats.cost_ip + float(sc[S_PSI].item())
                 psi_trace.append(psi_value(self.dp, y, rho, c_x, self.ax, nu, engine=eng))
-            eng.vec(N.VOP_NUNEXT, self.m, x=self.ax, y=y, z=nu, b=self.b, ineq=self.ineq, s0=rho, out=nxt,
-                    red=sc[S_DNU:S_DNU + 2])
+            finish_pass(nu, nxt)
             if psi_trace is not None:
                 psi_trace.append(psi_value(self.dp, y, rho, c_x, self.ax, nxt, engine=eng))
             nu = nxt
             if not self.has_ineq:
                 break
             dnu = math.sqrt(max(float(sc[S_DNU].item()), 0.0))
-            if dnu <= tol * (1.0 + self.b_norm):
+            if dnu <= thresh:
+                break
+            if device_loop:
+                # passes 2.. : nu -> other -> copied back, so the body's
+                # operands are the same buffers every time round
+                other = self.nu_b if nu is self.nu_a else self.nu_a
+                if self.loop_cnt is None:
+                    import torch
+                    self.loop_cnt = torch.zeros(1, dtype=torch.int32, device=rt.device)
+                self.loop_cnt.zero_()
+                l0 = rt.launches()
+                check(rt.lib.usbs_loop_begin(eng.h), "loop_begin")
+                try:
+                    enqueue_pass(nu, None, self.st_q)
+                    finish_pass(nu, other)
+                    eng.vec(N.VOP_AXPBY, self.m, x=other, s0=1.0, s1=0.0, out=nu)
+                except Exception:
+                    rt.lib.usbs_loop_abort(eng.h)
+                    raise
+                check(rt.lib.usbs_loop_end(eng.h, sc[S_DNU:S_DNU + 1].data_ptr(), float(thresh), max_passes - 1,
+                                           self.loop_cnt.data_ptr()), "loop_end")
+                body = rt.launches() - l0 - 1  # captured kernels (usbs_loop_end counted the graph launch)
+                done = int(self.loop_cnt.item())
+                rt.note_replays(body * done - body)  # the capture counted the body once
+                passes = 1 + done
                 break
         eng.dot_into(self.cq.view(-1), self.st_q[:k * k], sc[S_CQS:S_CQS + 1], scale=a)
         return nu, passes, has_eta

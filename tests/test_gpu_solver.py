@@ -238,6 +238,27 @@ def test_trajectory_vs_reference(name):
         assert abs(fy[-1] - z["f_y"][-1]) <= 3e-2 * (1 + abs(z["f_y"][-1]))
 
 
+@pytest.mark.parametrize("name", ["mixed40", "qap4"])
+def test_device_loop_equals_host_loop(name, monkeypatch):
+    """alternating_max's passes 2.. run as a device-controlled loop (CUDA-graph
+    WHILE node, usbs_loop_*): same kernels on the same operands as the
+    host-driven loop, so the trajectory and the pass counts are identical."""
+    engine, runtime, solver, _ = mods()
+    p = traj_problem(name)
+    kw = dict(TRAJ_CFG[name])
+    kw["max_iters"] = min(int(kw.get("max_iters", 40)), 40)
+    runs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("USBS_DEVICE_LOOP", mode)
+        rec = []
+        solver.solve(p, solver.SolverConfig(**kw), callback=rec.append)
+        runs[mode] = ([r.f_y for r in rec], [r.alt_passes for r in rec], [r.step for r in rec])
+    assert max(runs["0"][1]) > 2  # the loop ran (several passes per iteration)
+    assert runs["0"][1] == runs["1"][1]
+    assert runs["0"][2] == runs["1"][2]
+    np.testing.assert_array_equal(np.array(runs["0"][0]), np.array(runs["1"][0]))
+
+
 @pytest.mark.parametrize("name", ["er60", "mixed40"])
 def test_converged_objective_vs_oracle(name):
     """Tier iii: both runs reach converged(1e-3); objectives agree at the
