@@ -766,7 +766,10 @@ class DeviceSolver:
                     self.loop_cnt = torch.zeros(1, dtype=torch.int32, device=rt.device)
                 self.loop_cnt.zero_()
                 l0 = rt.launches()
-                check(rt.lib.usbs_loop_begin(eng.h), "loop_begin")
+                if rt.lib.usbs_loop_begin(eng.h) != 0:
+                    # no conditional graph nodes on this driver: keep the host-driven loop
+                    self.device_loop = device_loop = False
+                    continue
                 try:
                     enqueue_pass(nu, None, self.st_q)
                     finish_pass(nu, other)
