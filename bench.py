@@ -189,6 +189,15 @@ def cpu_run(cfg_b, steps, warmup, budget_s=120.0):
     return done / dt, done, dt
 
 
+def bench_config(name, world):
+    """The `config` object of the JSON line -- identical for the device arm and
+    the reference arm (the driver compares them key by key)."""
+    return {"workload": WORKLOADS[name],
+            "parallelism": f"replicas x{world}" if world > 1 else "single process",
+            "l2": "inputs larger than L2; also flushed (256 MiB write) between timed iterations (device arm)",
+            "step": "one USBS outer iteration"}
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -207,7 +216,7 @@ def run_reference(args):
         "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": done, "warmup": warm, "ms_per_step": 1e3 * dt / max(done, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "parallelism": "host"},
+        "config": bench_config(args.config, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "port",
                          "sample": f"{done} outer iterations (of {args.steps} asked; timed work capped at "
                                    f"{args.ref_budget:.0f} s) after cold start + {warm} warm-up iterations "
@@ -378,10 +387,7 @@ def run_device(args):
             "metric": metric_name(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": total_ms / max(steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config],
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2; also flushed (256 MiB write) between timed iterations",
-                       "step": "one USBS outer iteration"},
+            "config": bench_config(args.config, world),
             "roofline": {"kernel": lz_kernel,
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
