@@ -297,7 +297,8 @@ usbs_status usbs_loop_abort(usbs_ctx* ctx);
  * np.random.RandomState(seed & 0x7FFFFFFF).standard_normal((n, r)) into
  * host memory out (C order), bit-identical to numpy's legacy MT19937 +
  * polar Gaussian.  Host-only (no device, no context): native so the fill
- * runs outside the Python GIL while the problem is planned. */
+ * runs outside the Python GIL while the problem is planned; pipelined over
+ * host threads (USBS_PSI_THREADS overrides the count; 0 = the caller only). */
 usbs_status usbs_make_test_matrix(int64_t seed, int64_t n, int r, int64_t row0, int64_t row1, double* out);
 
 /* maxcut_round (rounding.py:34-51): for every column j of the factor U
