@@ -687,6 +687,10 @@ static void create_problem(usbs_ctx* ctx, int64_t n, int64_t n_cols, int64_t m, 
   p->spmv_group = pick_group(avg);
   const int SEG = 16 * p->spmv_group;
   std::vector<int32_t> irow, ibeg, iend, islot, srow, sfirst, scount;
+  {
+    const size_t cap = (size_t)n + (size_t)(p->nnz / SEG) + 16;  // one item per row plus the extra pieces of split rows
+    irow.reserve(cap); ibeg.reserve(cap); iend.reserve(cap); islot.reserve(cap);
+  }
   int nsplit = 0;
   for (int64_t i = 0; i < n; ++i) {
     int32_t b = rp32[i], e = rp32[i + 1];
