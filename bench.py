@@ -337,9 +337,12 @@ def run_device(args):
     torch.cuda.synchronize()
     d2h = {"bytes": 0}
 
+    e2e_marks = []
+
     def cb_e2e(info):
         yh = info.y  # D2H of the iteration's dual iterate
         d2h["bytes"] += yh.nbytes + 8 * 16
+        e2e_marks.append(time.perf_counter())
 
     cfg_e = _solver_cfg(S, cfg_b, eps=1e-12, max_iters=args.steps)
     cost = p.cost
@@ -349,6 +352,10 @@ def run_device(args):
     st_e, _ = S.solve(p, cfg_e, callback=cb_e2e)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    if os.environ.get("USBS_BENCH_E2E_DEBUG") and e2e_marks:
+        print(f"[e2e] total {e2e_s * 1e3:.0f} ms: first callback {1e3 * (e2e_marks[0] - t0):.0f}, iterations "
+              f"{1e3 * (e2e_marks[-1] - e2e_marks[0]):.0f}, exit {1e3 * (t0 + e2e_s - e2e_marks[-1]):.0f}; intervals "
+              f"{[round(1e3 * (b - a)) for a, b in zip(e2e_marks, e2e_marks[1:])]}", file=sys.stderr, flush=True)
     e2e_steps = st_e.iterations
     e2e_value = world * e2e_steps / e2e_s
 
